@@ -1,0 +1,430 @@
+#!/usr/bin/env python
+"""bench.py -- throughput of the B200 elementwise primality path (arXiv
+2108.04791 "isprime_fast") in Gints/s, one JSON line on rank 0.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config C5] [--impl reference]
+    python -m torch.distributed.run --nproc-per-node N --master-addr 127.0.0.1 bench.py --gpus N
+
+A step is one isprime_device() call over one batch: plan -> sieve -> classify
+(trial division + compaction) -> Miller-Rabin base 2 -> remaining bases, every
+row of SURVEY.md 8(a).  The headline workload is BASELINE.json configs[4]
+("C5": n = 2^28 mixed magnitudes with Chernick and 2^64-59 inserts), the one
+configuration that exercises every row in a single step; C1-C4 are reported
+under "per_config".  Multi-GPU is weak scaling: rank r classifies generator
+indices [r n, (r+1) n) with no collective on the path (NCCL only reduces the
+prime count and the max time).  Inputs are 2 GiB per step (> 126 MB L2), so L2
+is not flushed between steps.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import workloads  # noqa: E402
+
+METRIC = "Gints/sec classified (1/2/4/8 B200) per magnitude class; % of IMAD or HBM roofline"
+UNIT = "Gints/s"
+# Integer-multiply lane-ops of one Montgomery multiplication on sm_100a (SASS
+# of csrc/modmath.cuh): 32-bit = IMAD.WIDE.U32 + IMAD +
+# IMAD.HI.U32; 64-bit = 4 IMAD.WIDE.U32 (+.X) for a*b, 3 for m = lo*ninv, 4 for
+# hi(m*n), plus carries = 14.
+IMAD_PER_MULMOD32 = 3
+IMAD_PER_MULMOD64 = 14
+IMAD_LANES_PER_CLK_SM = 64  # FMA-heavy pipe: 16 lanes/clk per SMSP x 4 (B300_MICROARCH.md "Pipe rates")
+HBM_BYTES_PER_ELEM = 9      # 8-B value read + 1-B result written
+
+
+def _env_int(k, d):
+    try:
+        return int(os.environ.get(k, d))
+    except ValueError:
+        return d
+
+
+def measured_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(p) as f:
+            d = json.load(f)
+        return d, "measured"
+    except Exception:
+        return {"hbm_gbs": 6650.0, "sm_max_mhz": 1965.0}, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled while the timed region runs."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, dev: int):
+        self.dev = dev
+        self.samples = []
+        self.proc = None
+        self.thread = None
+        self.marks = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.dev), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "20"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except FileNotFoundError:
+            return
+        self.thread = threading.Thread(target=self._read, daemon=True)
+        self.thread.start()
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.samples.append((time.perf_counter(), line.strip()))
+
+    def mark(self):
+        self.marks.append(time.perf_counter())
+
+    def stop(self):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        rows = []
+        if len(self.marks) >= 2:
+            t0, t1 = self.marks[0], self.marks[-1]
+            rows = [s for t, s in self.samples if t0 <= t <= t1 + 0.05]
+        if not rows:  # timed region shorter than the sampling interval: nearest samples under load
+            rows = [s for _, s in self.samples[-5:]]
+        sm, smax, reasons = [], 0.0, set()
+        names = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
+        for r in rows:
+            parts = [p.strip() for p in r.split(",")]
+            if len(parts) < 7:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                smax = max(smax, float(parts[1]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[3:7]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        if not sm:
+            return None
+        return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": smax, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def load_counts():
+    out = {}
+    with open(os.path.join(ROOT, "tests", "golden", "config_counts.txt")) as f:
+        for line in f:
+            line = line.split("#", 1)[0].split()
+            if line:
+                out[line[0]] = int(line[2])
+    out["C4"] = 203280221  # pi(2^32)
+    return out
+
+
+def make_input(cfg, rank, torch, dev):
+    """Rank's batch on the device (weak scaling: generator indices [r n, (r+1) n))."""
+    n = workloads.CONFIGS[cfg][1]
+    if cfg == "C4":
+        if rank != 0:
+            raise SystemExit("C4 is the fixed range 0..2^32-1; run it at --gpus 1")
+        return torch.arange(n, dtype=torch.int64, device=dev), None
+    host = workloads.generate(cfg, start=rank * n, count=n)
+    ht = torch.from_numpy(host.view(np.int64))
+    return ht.to(dev), host
+
+
+def time_steps(isp, torch, dN, dout, n, steps, warmup, stream, dist, sampler=None):
+    for _ in range(warmup):
+        isp.isprime_device(dN, dout, n, stream)
+    torch.cuda.synchronize()
+    if dist is not None:
+        dist.barrier()
+    torch.cuda.synchronize()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    l0 = isp.get_stats()["kernel_launches"]
+    if sampler:
+        sampler.mark()
+    e0.record(stream)
+    for _ in range(steps):
+        isp.isprime_device(dN, dout, n, stream)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    if sampler:
+        sampler.mark()
+    if dist is not None:
+        dist.barrier()
+    launches = isp.get_stats()["kernel_launches"] - l0
+    return e0.elapsed_time(e1) / steps, launches
+
+
+def kernel_profile(isp, torch, dN, dout, n, steps, stream):
+    """Instrumented pass (events around every launch + algorithmic work counters)."""
+    isp.set_option("kernel_timing", 1)
+    isp.reset_kernel_times()
+    isp.reset_stats()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(steps):
+        isp.isprime_device(dN, dout, n, stream)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    kt = isp.get_kernel_times()
+    st = isp.get_stats()
+    isp.set_option("kernel_timing", 0)
+    step_ms = e0.elapsed_time(e1) / steps
+    per_step = {k: v[1] / steps for k, v in kt.items() if v[0] > 0}
+    return per_step, st, step_ms
+
+
+def roofline(kern_ms, stats, n, steps, peaks, peaks_kind, clocks):
+    """Roofline of the dominant kernel (largest share of the step)."""
+    if not kern_ms:
+        return None
+    name = max(kern_ms, key=kern_ms.get)
+    ms = kern_ms[name]
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(tpath):
+        try:
+            traffic = json.load(open(tpath)).get(name)
+        except Exception:
+            traffic = None
+    if name in ("mr1", "mr2"):
+        mm = stats["mulmods"]
+        if name == "mr1":
+            imad = mm[0] * IMAD_PER_MULMOD32 + mm[1] * IMAD_PER_MULMOD64
+        else:
+            imad = mm[2] * IMAD_PER_MULMOD32 + mm[3] * IMAD_PER_MULMOD64
+        achieved = imad / steps / (ms * 1e-3) / 1e12
+        mhz = peaks.get("sm_max_mhz", 1965.0)
+        peak = 148 * IMAD_LANES_PER_CLK_SM * mhz * 1e6 / 1e12
+        return {"kernel": name, "bound": "alu", "achieved": round(achieved, 4), "peak": round(peak, 3),
+                "unit": "T IMAD-lane-ops/s", "frac": round(achieved / peak, 4), "traffic": traffic,
+                "peak_source": f"derived: 148 SMs x {IMAD_LANES_PER_CLK_SM} IMAD lanes/clk x {mhz:.0f} MHz "
+                               "(B300_MICROARCH.md fma pipe rt=2/SMSP; MEASURED_PEAKS sm_max_mhz)",
+                "work": f"{imad / steps:.4g} algorithmic IMAD per step = mulmods x {IMAD_PER_MULMOD32} (32-bit) "
+                        f"/ {IMAD_PER_MULMOD64} (64-bit)", "ms_per_step": round(ms, 4)}
+    nbytes = HBM_BYTES_PER_ELEM * n
+    if name == "sieve":
+        nbytes = stats["sieved_integers"] / steps / 16.0 if stats["sieved_integers"] else 0.0
+    elif name != "classify":
+        nbytes = n
+    achieved = nbytes / (ms * 1e-3) / 1e9
+    peak = float(peaks.get("hbm_gbs", 6650.0))
+    return {"kernel": name, "bound": "hbm", "achieved": round(achieved, 2), "peak": peak, "unit": "GB/s",
+            "frac": round(achieved / peak, 4), "traffic": traffic, "peak_source": f"{peaks_kind} hbm_gbs",
+            "work": f"{nbytes:.4g} algorithmic bytes per step", "ms_per_step": round(ms, 4)}
+
+
+def cpu_baseline_run(cfg, host, sample_n):
+    import oracle  # test infrastructure: the cpu_baseline leg only
+    if host is None:
+        sample = np.arange(sample_n, dtype=np.uint64)
+    else:
+        sample = host[:sample_n]
+    threads = os.cpu_count() or 1
+    t = time.perf_counter()
+    out = oracle.isprime(sample, threads=threads)
+    dt = time.perf_counter() - t
+    return {"value": round(sample.shape[0] / dt / 1e9, 6), "unit": UNIT, "cores": threads, "kind": "oracle",
+            "sample": f"first {sample.shape[0]} elements of {cfg} ({dt:.2f} s wall, {int(out.sum())} primes)"}
+
+
+def run_reference(args, rank, world):
+    """--impl reference: the CPU oracle (this tier's reference arm), rank 0 only."""
+    if rank != 0:
+        return
+    import oracle
+    cfg = args.config
+    n = workloads.CONFIGS[cfg][1]
+    sample_n = min(n, args.ref_sample)
+    if cfg == "C4":
+        sample = np.arange(sample_n, dtype=np.uint64)
+    else:
+        sample = workloads.generate(cfg, count=sample_n)
+    threads = os.cpu_count() or 1
+    for _ in range(args.warmup):
+        oracle.isprime(sample, threads=threads)
+    t = time.perf_counter()
+    for _ in range(args.steps):
+        oracle.isprime(sample, threads=threads)
+    dt = (time.perf_counter() - t) / args.steps
+    value = sample_n / dt / 1e9
+    line = {
+        "impl": "reference", "metric": METRIC, "value": round(value, 6), "unit": UNIT, "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(dt * 1e3, 3), "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "u64", "data": "synthetic",
+        "config": config_block(cfg, world),
+        "cpu_baseline": {"value": round(value, 6), "unit": UNIT, "cores": threads, "kind": "oracle",
+                         "sample": f"first {sample_n} elements of {cfg} per step"},
+        "e2e": {"value": round(value, 6), "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def config_block(cfg, world):
+    n = workloads.CONFIGS[cfg][1]
+    return {"workload": f"{cfg}: {workloads.CONFIGS[cfg][2]} (BASELINE.json configs[{int(cfg[1]) - 1}])",
+            "n_per_rank": n, "global_n": n * world, "parallelism": f"dp{world} (contiguous shards, no collective)",
+            "l2": "no flush: inputs larger than L2 (%.2f GiB per step)" % (n * 8 / 2**30)}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="C5", choices=sorted(workloads.CONFIGS))
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-per-config", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--cpu-sample", type=int, default=1 << 24)
+    ap.add_argument("--ref-sample", type=int, default=1 << 22)
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+
+    rank = _env_int("RANK", 0)
+    world = _env_int("WORLD_SIZE", 1)
+    local = _env_int("LOCAL_RANK", 0)
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+        return
+
+    import torch
+    import torch.distributed as tdist
+    import paper_2108_04791_b200 as isp
+
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    dist = None
+    if world > 1:
+        tdist.init_process_group("nccl", device_id=dev)
+        dist = tdist
+    isp.load(build_if_missing=False)
+    stream = torch.cuda.current_stream()
+    peaks, peaks_kind = measured_peaks()
+    counts = load_counts()
+
+    cfg = args.config
+    n = workloads.CONFIGS[cfg][1]
+    dN, host = make_input(cfg, rank, torch, dev)
+    dout = torch.empty(n, dtype=torch.uint8, device=dev)
+
+    sampler = ClockSampler(local)
+    sampler.start()
+    time.sleep(0.2)
+    ms, launches = time_steps(isp, torch, dN, dout, n, args.steps, args.warmup, stream, dist, sampler)
+    sampler.stop()
+    clocks = sampler.summary()
+
+    t = torch.tensor([ms], dtype=torch.float64, device=dev)
+    if dist:
+        dist.all_reduce(t, op=tdist.ReduceOp.MAX)
+    ms_max = float(t.item())
+    value = world * n / (ms_max * 1e-3) / 1e9
+
+    # validation: count per rank -> NCCL sum
+    dcount = torch.zeros(1, dtype=torch.int64, device=dev)
+    isp.isprime_popcount_device(dout, dcount, n, stream)
+    torch.cuda.synchronize()
+    my_count = int(dcount.item())
+    tot = dcount.clone()
+    if dist:
+        dist.all_reduce(tot)
+    total_count = int(tot.item())
+    correct = (my_count == counts[cfg]) if rank == 0 else None
+
+    kern_ms, st, inst_ms = kernel_profile(isp, torch, dN, dout, n, args.steps, stream)
+    roof = roofline(kern_ms, st, n, args.steps, peaks, peaks_kind, clocks)
+
+    e2e = None
+    if not args.no_e2e:
+        if host is None:
+            hN = torch.arange(n, dtype=torch.int64).pin_memory()
+        else:
+            hN = torch.from_numpy(host.view(np.int64)).pin_memory()
+        hout = torch.empty(n, dtype=torch.uint8).pin_memory()
+        for _ in range(1):
+            isp.isprime_into(hN, hout)
+        torch.cuda.synchronize()
+        if dist:
+            dist.barrier()
+        t0 = time.perf_counter()
+        esteps = max(1, min(args.steps, 5))
+        for _ in range(esteps):
+            isp.isprime_into(hN, hout)
+        et = torch.tensor([(time.perf_counter() - t0) / esteps], dtype=torch.float64, device=dev)
+        if dist:
+            dist.all_reduce(et, op=tdist.ReduceOp.MAX)
+        e2e = {"value": round(world * n / float(et.item()) / 1e9, 4), "unit": UNIT,
+               "h2d_bytes_per_step": int(n * 8), "d2h_bytes_per_step": int(n),
+               "ms_per_step": round(float(et.item()) * 1e3, 3),
+               "how": "isprime() host C-ABI on pinned host buffers; host wall clock around the synchronous call",
+               "matches_device": bool(np.array_equal(hout.numpy(), dout.cpu().numpy()))}
+        del hN, hout
+
+    line = {
+        "metric": METRIC, "value": round(value, 4), "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": round(ms_max, 4), "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "u64", "data": "synthetic (seeded generator, SURVEY.md 8(d))",
+        "config": config_block(cfg, world),
+        "roofline": roof, "e2e": e2e, "gpu_launches": int(launches), "clocks": clocks,
+        "kernels_ms_per_step": {k: round(v, 4) for k, v in kern_ms.items()},
+        "instrumented_ms_per_step": round(inst_ms, 4),
+        "prime_count": {"rank0": my_count, "total": total_count, "expected_rank0": counts[cfg], "correct": correct},
+        "stats_per_step": {k: (v / args.steps if isinstance(v, int) else [x / args.steps for x in v])
+                           for k, v in st.items() if k not in ("window_lo", "window_hi", "kernel_launches")},
+    }
+    del dN, dout
+    torch.cuda.empty_cache()
+
+    if rank == 0 and world == 1:
+        line["cpu_baseline"] = cpu_baseline_run(cfg, host, min(n, args.cpu_sample))
+        if not args.no_per_config:
+            per = {}
+            for c in ("C1", "C2", "C3", "C4"):
+                if c == cfg:
+                    continue
+                cn = workloads.CONFIGS[c][1]
+                cN, _ = make_input(c, 0, torch, dev)
+                cout = torch.empty(cn, dtype=torch.uint8, device=dev)
+                csteps = args.steps if c != "C1" else max(args.steps, 100)
+                cms, cl = time_steps(isp, torch, cN, cout, cn, csteps, args.warmup, stream, None)
+                isp.isprime_popcount_device(cout, dcount, cn, stream)
+                torch.cuda.synchronize()
+                ckm, cst, _ = kernel_profile(isp, torch, cN, cout, cn, csteps, stream)
+                croof = roofline(ckm, cst, cn, csteps, peaks, peaks_kind, clocks)
+                per[c] = {"value": round(cn / (cms * 1e-3) / 1e9, 4), "unit": UNIT, "ms_per_step": round(cms, 4),
+                          "n": cn, "correct": int(dcount.item()) == counts[c], "gpu_launches_per_step": cl / csteps,
+                          "kernels_ms_per_step": {k: round(v, 4) for k, v in ckm.items()}, "roofline": croof}
+                del cN, cout
+                torch.cuda.empty_cache()
+            line["per_config"] = per
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if dist:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,144 @@
+/*
+ * isprime.h -- C-ABI of libisprime.so, the B200 (sm_100a) elementwise
+ * primality classifier of arXiv 2108.04791 ("isprime_fast").
+ *
+ * Operation (section 1): "MATLAB's isprime function accepts
+ * an input array, N, then returns which elements in the array are prime";
+ * isprime([1,2,3,4,5]) = [0 1 1 0 1].  isprime_fast's "inputs and outputs are
+ * identical"; its domain is 0 .. 2^64-1 (reading
+ * G10).  Arrays of any shape are allowed: this library takes
+ * the flattened array, preserves element order, and leaves shape to the
+ * caller.
+ *
+ * Result: out[i] = 1 if N[i] is prime, else 0 (0 and 1 are not prime).  The
+ * result is exact for every uint64 value: the large-integer class uses the
+ * deterministic Miller-Rabin bases of Eq 4, the array path
+ * uses a sieve of Eratosthenes when the values are small,
+ * and small-prime trial division ("shrinking") in front of
+ * both.  The path chosen for an element never changes its result.
+ *
+ * Every call returns ISP_OK (0) or a negative isp_status.  Calls are
+ * thread-safe (serialised internally).  No call keeps a reference to a
+ * caller buffer after it returns (host API) or after the work it enqueued
+ * completes (device API).  There is no CPU fallback: without a CUDA device
+ * every compute call returns ISP_ENODEV.
+ */
+#ifndef ISPRIME_H
+#define ISPRIME_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+    ISP_OK = 0,
+    ISP_EINVAL = -1, /* NULL pointer with n > 0, out overlapping N, bad option */
+    ISP_ENOMEM = -2, /* device or pinned-host allocation failed */
+    ISP_ECUDA = -3,  /* a CUDA runtime call or kernel failed; out is undefined */
+    ISP_ENODEV = -4  /* no CUDA device */
+} isp_status;
+
+/* Host-pointer front door: out[i] = isprime(N[i]) for i < n.
+ *   N    host array of n uint64 values (pinned or pageable; any 8-B alignment)
+ *   out  host array of n bytes, written with 0/1; must not overlap N
+ * Synchronous: returns after out is complete.  Internally stages chunks to the
+ * current CUDA device with overlapped H2D / compute / D2H.
+ * n == 0 returns ISP_OK and may pass NULL pointers. */
+int isprime(const uint64_t* N, uint8_t* out, size_t n);
+
+/* Device-pointer front door, stream-ordered (asynchronous w.r.t. the host):
+ *   dN     device array of n uint64 values on the current device
+ *   dout   device array of n bytes (0/1 written for every i); must not overlap dN
+ *   stream a cudaStream_t (NULL = legacy default stream)
+ * Uses internal per-device scratch (plan, bitmap, queues) ordered on `stream`;
+ * concurrent calls on different streams are serialised by the library. */
+int isprime_device(const uint64_t* dN, uint8_t* dout, size_t n, void* stream);
+
+/* As isprime_device, then *dcount (device pointer, one uint64) = number of
+ * primes in dout (used for the multi-GPU validation reduce). */
+int isprime_count_device(const uint64_t* dN, uint8_t* dout, size_t n,
+                         uint64_t* dcount, void* stream);
+
+/* *dcount = sum of dout[0..n) (device pointers, stream-ordered). */
+int isprime_popcount_device(const uint8_t* dout, size_t n, uint64_t* dcount,
+                            void* stream);
+
+/* Human-readable text for a status (includes the last CUDA error string for
+ * ISP_ECUDA).  Never NULL; the pointer stays valid until the next call. */
+const char* isprime_strerror(int status);
+
+/* Frees all cached per-device scratch (queues, bitmap, tables, streams). */
+void isprime_shutdown(void);
+
+/* ---- options (process-wide; for tests and tuning) --------------------------
+ * key                value
+ * "force_path"       0 auto (cost model), 1 sieve (window [0, 2^32) for every
+ *                    value below 2^32), 2 mr (no sieve window: trial division +
+ *                    Miller-Rabin for everything).  Default from env
+ *                    ISPRIME_FORCE_PATH=auto|sieve|mr.  Never changes a bit of
+ *                    out ("--force-path never changes any mask bit").
+ * "bases32"          3: bases {2, 7, 61} for 2^32 > n (exact below 4,759,123,141,
+ *                    Jaeschke; verified over all n < 2^32); 7: the full Eq 4 set.
+ * "td_primes32"      number of odd primes (from 3) trial-divided into values
+ *                    below 2^32 before Miller-Rabin (0..ISP_MAX_TD)
+ * "td_primes64"      same for values >= 2^32
+ * "chunk_log2"       device chunk size (elements) = 2^value, 16..31
+ * "win64"            exponent window width for the 64-bit multi-base phase (1..3)
+ * "sieve_cache"      0 (default): every call sieves its own window; 1: a call may
+ *                    reuse the bitmap an earlier call on this device produced
+ * "kernel_timing"    1: bracket every launch with CUDA events on its stream and
+ *                    accumulate per-kernel device time (isprime_get_kernel_times)
+ * Returns ISP_OK or ISP_EINVAL. */
+#define ISP_MAX_TD 128
+int isprime_set_option(const char* key, long long value);
+long long isprime_get_option(const char* key);
+
+/* ---- diagnostics (test hooks over the same device code as the path) ---- */
+typedef struct {
+    uint64_t window_lo, window_hi;   /* last chunk's sieve window [lo, hi) */
+    uint64_t sieve_runs;             /* segmented-sieve passes since last reset */
+    uint64_t sieved_integers;        /* integers covered by those passes */
+    uint64_t queued32, queued64;     /* survivors of trial division (all chunks) */
+    uint64_t passed32, passed64;     /* of those, strong probable primes to base 2 */
+    uint64_t chunks;                 /* device chunks processed */
+    uint64_t kernel_launches;        /* kernels launched by the library (host count) */
+    uint64_t mulmods[4];             /* algorithmic modular multiplications counted while
+                                        "kernel_timing" is 1: mr1 32-bit, mr1 64-bit,
+                                        mr2 32-bit, mr2 64-bit (square-and-multiply count) */
+} isprime_stats;
+
+/* Synchronises the current device, copies the accumulated statistics. */
+int isprime_get_stats(isprime_stats* st);
+int isprime_reset_stats(void);
+
+/* Per-kernel device time accumulated while option "kernel_timing" is 1
+ * (synchronises the device).  Fills up to `max` entries; *count = entries
+ * available.  Names: plan, sieve, classify, mr1, mr2, popcount. */
+typedef struct {
+    char name[16];
+    uint64_t launches;
+    double ms_total;
+} isprime_kernel_time;
+int isprime_get_kernel_times(isprime_kernel_time* out, int max, int* count);
+int isprime_reset_kernel_times(void);
+
+/* out[i] = 1 iff n[i] (odd, >= 3) is a strong probable prime to base a[i]
+ * (Eq 1-3; a reduced mod n, 0 passes), computed with the
+ * device Montgomery library of the witness kernels (32-bit when n < 2^32).
+ * Device pointers, stream-ordered.  Elements with n even or < 3 give 0. */
+int isprime_sprp_device(const uint64_t* dn, const uint64_t* da, uint8_t* dout,
+                        size_t count, void* stream);
+
+/* out[i] = a[i] * b[i] mod m[i] through Montgomery form (odd m >= 3; a, b are
+ * reduced mod m first).  Device pointers, stream-ordered.  m even -> 0. */
+int isprime_mulmod_device(const uint64_t* da, const uint64_t* db,
+                          const uint64_t* dm, uint64_t* dout, size_t count,
+                          void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* ISPRIME_H */

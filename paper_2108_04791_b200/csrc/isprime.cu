@@ -1,0 +1,640 @@
+// isprime.cu -- libisprime.so: C-ABI front end (layer L3) and planner /
+// launcher (layer L2) of the B200 elementwise primality classifier.
+//
+// See include/isprime.h for the contract and DESIGN.md for the design.  Every
+// step of the path runs in the kernels of kernels.cuh; the host only
+// validates arguments, owns scratch memory and enqueues launches.  There is
+// no CPU fallback: without a CUDA device every compute call fails with
+// ISP_ENODEV.
+#include <cuda_runtime.h>
+
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "../../include/isprime.h"
+#include "kernels.cuh"
+
+using namespace isp;
+
+namespace {
+
+struct Options {
+    int force_path = 0;      // 0 auto, 1 sieve, 2 mr
+    int bases32 = 3;         // 3 -> {2,7,61}; 7 -> full Eq 4 set
+    int td32 = 24;           // odd primes 3..97
+    int td64 = 24;
+    int chunk_log2 = 28;
+    int win64 = 2;
+    int warp_p = 2048;
+    long long sieve_fs_per_int = 300;     // femtoseconds per integer of window
+    long long sieve_fixed_ns = 4000;
+    long long mr32_fs_per_bit = 80;       // femtoseconds per odd element per bit
+    unsigned long long sieve_max = 1ull << 32;
+    int kernel_timing = 0;
+    int sieve_cache = 0;     // 1: a call may reuse the bitmap sieved by an earlier call
+};
+
+Options g_opt;
+bool g_opt_env_read = false;
+std::mutex g_mu;
+std::string g_err;
+unsigned long long g_launches = 0;
+
+struct Ctx {
+    int dev = -1;
+    int sms = 0;
+    uint2* bp = nullptr;
+    int nbp = 0;
+    std::vector<uint2> hbp;
+    uint8_t* patt = nullptr;
+    uint32_t* bitmap = nullptr;
+    DevPlan* plan = nullptr;
+    unsigned char* qmem = nullptr;
+    size_t qcap = 0;
+    Queues q{};
+    int grid_cls = 0, grid_mr1 = 0, grid_mr2 = 0, grid_sieve = 0;
+    cudaEvent_t last_done = nullptr;
+    void* last_stream = nullptr;
+    bool has_last = false;
+    // host-API staging
+    cudaStream_t hs[2] = {nullptr, nullptr};
+    cudaEvent_t ev_h2d[2] = {nullptr, nullptr};
+    cudaEvent_t ev_d2h[2] = {nullptr, nullptr};
+    unsigned long long* din[2] = {nullptr, nullptr};
+    uint8_t* dout[2] = {nullptr, nullptr};
+    unsigned long long* hin[2] = {nullptr, nullptr};
+    uint8_t* hout[2] = {nullptr, nullptr};
+    size_t hcap = 0;
+};
+
+std::vector<Ctx*> g_ctx;
+
+// ---- optional per-kernel timing (events on the launching stream)
+enum { K_PLAN, K_SIEVE, K_CLASSIFY, K_MR1, K_MR2, K_POPCOUNT, K_NUM };
+const char* const k_names[K_NUM] = {"plan", "sieve", "classify", "mr1", "mr2", "popcount"};
+struct KTPending { cudaEvent_t a, b; int kid; };
+std::vector<KTPending> g_kt_pending;
+std::vector<cudaEvent_t> g_ev_pool;
+double g_kt_ms[K_NUM] = {0};
+unsigned long long g_kt_n[K_NUM] = {0};
+
+cudaEvent_t ev_get() {
+    if (!g_ev_pool.empty()) { cudaEvent_t e = g_ev_pool.back(); g_ev_pool.pop_back(); return e; }
+    cudaEvent_t e = nullptr;
+    cudaEventCreate(&e);
+    return e;
+}
+
+void kt_drain() {
+    if (g_kt_pending.empty()) return;
+    for (auto& p : g_kt_pending) {
+        float ms = 0.f;
+        cudaEventSynchronize(p.b);
+        if (cudaEventElapsedTime(&ms, p.a, p.b) == cudaSuccess) { g_kt_ms[p.kid] += ms; g_kt_n[p.kid]++; }
+        g_ev_pool.push_back(p.a);
+        g_ev_pool.push_back(p.b);
+    }
+    g_kt_pending.clear();
+}
+
+struct KScope {
+    int kid; cudaStream_t s; cudaEvent_t a = nullptr;
+    KScope(int k, cudaStream_t st) : kid(k), s(st) {
+        if (g_opt.kernel_timing) { a = ev_get(); cudaEventRecord(a, s); }
+    }
+    ~KScope() {
+        if (a) {
+            cudaEvent_t b = ev_get();
+            cudaEventRecord(b, s);
+            g_kt_pending.push_back({a, b, kid});
+            if (g_kt_pending.size() > 4096) kt_drain();
+        }
+    }
+};
+
+void read_env_once() {
+    if (g_opt_env_read) return;
+    g_opt_env_read = true;
+    if (const char* e = getenv("ISPRIME_FORCE_PATH")) {
+        if (!strcmp(e, "sieve")) g_opt.force_path = 1;
+        else if (!strcmp(e, "mr")) g_opt.force_path = 2;
+        else g_opt.force_path = 0;
+    }
+    if (const char* e = getenv("ISPRIME_BASES32")) g_opt.bases32 = atoi(e) == 7 ? 7 : 3;
+    if (const char* e = getenv("ISPRIME_TD32")) g_opt.td32 = atoi(e);
+    if (const char* e = getenv("ISPRIME_TD64")) g_opt.td64 = atoi(e);
+    if (const char* e = getenv("ISPRIME_WIN64")) g_opt.win64 = atoi(e);
+    if (const char* e = getenv("ISPRIME_CHUNK_LOG2")) g_opt.chunk_log2 = atoi(e);
+    if (const char* e = getenv("ISPRIME_SIEVE_MAX")) g_opt.sieve_max = strtoull(e, nullptr, 0);
+}
+
+int cuda_fail(cudaError_t e, const char* what) {
+    g_err = std::string(what) + ": " + cudaGetErrorString(e);
+    return ISP_ECUDA;
+}
+
+#define CK(call)                                         \
+    do {                                                 \
+        cudaError_t e_ = (call);                         \
+        if (e_ != cudaSuccess) return cuda_fail(e_, #call); \
+    } while (0)
+
+#define CKL(what)                                        \
+    do {                                                 \
+        g_launches++;                                    \
+        cudaError_t e_ = cudaGetLastError();             \
+        if (e_ != cudaSuccess) return cuda_fail(e_, what); \
+    } while (0)
+
+int occupancy(const void* fn, int threads, size_t smem) {
+    int b = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, fn, threads, smem) != cudaSuccess || b < 1) b = 1;
+    return b;
+}
+
+int init_ctx(Ctx* c) {
+    CK(cudaGetDevice(&c->dev));
+    CK(cudaDeviceGetAttribute(&c->sms, cudaDevAttrMultiProcessorCount, c->dev));
+    CK(cudaMalloc(&c->bp, 8192 * sizeof(uint2)));
+    int* dcount = nullptr;
+    CK(cudaMalloc(&dcount, sizeof(int)));
+    init_base_primes_kernel<<<1, 1024>>>(c->bp, dcount);
+    CKL("init_base_primes_kernel");
+    CK(cudaMemcpy(&c->nbp, dcount, sizeof(int), cudaMemcpyDeviceToHost));
+    CK(cudaFree(dcount));
+    if (c->nbp != 6541) {  // odd primes below 65536
+        g_err = "base prime table has " + std::to_string(c->nbp) + " entries, expected 6541";
+        return ISP_ECUDA;
+    }
+    c->hbp.resize(c->nbp);
+    CK(cudaMemcpy(c->hbp.data(), c->bp, c->nbp * sizeof(uint2), cudaMemcpyDeviceToHost));
+    // trial-division constants -> __constant__
+    {
+        uint32_t *p32, *i32, *l32;
+        unsigned long long *i64, *l64;
+        CK(cudaMalloc(&p32, MAX_TD * 4));
+        CK(cudaMalloc(&i32, MAX_TD * 4));
+        CK(cudaMalloc(&l32, MAX_TD * 4));
+        CK(cudaMalloc(&i64, MAX_TD * 8));
+        CK(cudaMalloc(&l64, MAX_TD * 8));
+        init_td_kernel<<<1, MAX_TD>>>(c->bp, p32, i32, l32, i64, l64);
+        CKL("init_td_kernel");
+        CK(cudaMemcpyToSymbol(c_td_p, p32, MAX_TD * 4, 0, cudaMemcpyDeviceToDevice));
+        CK(cudaMemcpyToSymbol(c_td_inv32, i32, MAX_TD * 4, 0, cudaMemcpyDeviceToDevice));
+        CK(cudaMemcpyToSymbol(c_td_lim32, l32, MAX_TD * 4, 0, cudaMemcpyDeviceToDevice));
+        CK(cudaMemcpyToSymbol(c_td_inv64, i64, MAX_TD * 8, 0, cudaMemcpyDeviceToDevice));
+        CK(cudaMemcpyToSymbol(c_td_lim64, l64, MAX_TD * 8, 0, cudaMemcpyDeviceToDevice));
+        CK(cudaDeviceSynchronize());
+        cudaFree(p32); cudaFree(i32); cudaFree(l32); cudaFree(i64); cudaFree(l64);
+    }
+    CK(cudaMalloc(&c->patt, (size_t)PRESIEVE_COPIES * PRESIEVE_LEN));
+    init_presieve_kernel<<<256, 256>>>(c->patt);
+    CKL("init_presieve_kernel");
+    const size_t words = (size_t)(g_opt.sieve_max >> 6) + 1;
+    CK(cudaMalloc(&c->bitmap, words * 4));
+    CK(cudaMalloc(&c->plan, sizeof(DevPlan)));
+    CK(cudaMemset(c->plan, 0, sizeof(DevPlan)));
+    CK(cudaFuncSetAttribute(sieve_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SEG_ODD));
+    c->grid_sieve = c->sms * occupancy((const void*)sieve_kernel, SIEVE_THREADS, SEG_ODD);
+    c->grid_cls = c->sms * occupancy((const void*)classify_kernel<true>, CLS_THREADS, 0);
+    c->grid_mr1 = c->sms * occupancy((const void*)mr1_kernel, MR_THREADS, 0);
+    c->grid_mr2 = c->sms * occupancy((const void*)mr2_kernel<2, false>, MR_THREADS, 0);
+    CK(cudaEventCreateWithFlags(&c->last_done, cudaEventDisableTiming));
+    for (int k = 0; k < 2; k++) {
+        CK(cudaStreamCreateWithFlags(&c->hs[k], cudaStreamNonBlocking));
+        CK(cudaEventCreateWithFlags(&c->ev_h2d[k], cudaEventDisableTiming));
+        CK(cudaEventCreateWithFlags(&c->ev_d2h[k], cudaEventDisableTiming));
+    }
+    CK(cudaDeviceSynchronize());
+    return ISP_OK;
+}
+
+int get_ctx(Ctx** out) {
+    read_env_once();
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) {
+        cudaGetLastError();
+        g_err = "no CUDA device";
+        return ISP_ENODEV;
+    }
+    int dev = 0;
+    CK(cudaGetDevice(&dev));
+    if ((int)g_ctx.size() <= dev) g_ctx.resize(dev + 1, nullptr);
+    if (!g_ctx[dev]) {
+        Ctx* c = new Ctx();
+        int rc = init_ctx(c);
+        if (rc != ISP_OK) { delete c; return rc; }
+        g_ctx[dev] = c;
+    }
+    *out = g_ctx[dev];
+    return ISP_OK;
+}
+
+int ensure_queues(Ctx* c, size_t cap) {
+    if (cap <= c->qcap) return ISP_OK;
+    if (c->qmem) { CK(cudaFree(c->qmem)); c->qmem = nullptr; c->qcap = 0; }
+    cap = (cap + 4095) & ~(size_t)4095;
+    // per entry: q32 4+4, q64 4+8, p32 4+4, p64 4+8 = 40 bytes
+    const size_t bytes = cap * 40;
+    if (cudaMalloc(&c->qmem, bytes) != cudaSuccess) {
+        cudaGetLastError();
+        g_err = "queue allocation of " + std::to_string(bytes) + " bytes failed";
+        return ISP_ENOMEM;
+    }
+    unsigned char* p = c->qmem;
+    c->q.q64_val = reinterpret_cast<unsigned long long*>(p); p += cap * 8;
+    c->q.p64_val = reinterpret_cast<unsigned long long*>(p); p += cap * 8;
+    c->q.q32_idx = reinterpret_cast<uint32_t*>(p); p += cap * 4;
+    c->q.q32_val = reinterpret_cast<uint32_t*>(p); p += cap * 4;
+    c->q.q64_idx = reinterpret_cast<uint32_t*>(p); p += cap * 4;
+    c->q.p32_idx = reinterpret_cast<uint32_t*>(p); p += cap * 4;
+    c->q.p32_val = reinterpret_cast<uint32_t*>(p); p += cap * 4;
+    c->q.p64_idx = reinterpret_cast<uint32_t*>(p); p += cap * 4;
+    c->qcap = cap;
+    return ISP_OK;
+}
+
+bool overlaps(const void* a, size_t an, const void* b, size_t bn) {
+    const uintptr_t a0 = (uintptr_t)a, b0 = (uintptr_t)b;
+    return a0 < b0 + bn && b0 < a0 + an;
+}
+
+int launch_mr2(Ctx* c, cudaStream_t s, uint8_t* out) {
+    const bool full = g_opt.bases32 == 7;
+    const int cw = g_opt.kernel_timing;
+    switch (g_opt.win64 * 2 + (full ? 1 : 0)) {
+        case 2: mr2_kernel<1, false><<<c->grid_mr2, MR_THREADS, 0, s>>>(c->plan, c->q, out, cw); break;
+        case 3: mr2_kernel<1, true><<<c->grid_mr2, MR_THREADS, 0, s>>>(c->plan, c->q, out, cw); break;
+        case 4: mr2_kernel<2, false><<<c->grid_mr2, MR_THREADS, 0, s>>>(c->plan, c->q, out, cw); break;
+        case 5: mr2_kernel<2, true><<<c->grid_mr2, MR_THREADS, 0, s>>>(c->plan, c->q, out, cw); break;
+        case 6: mr2_kernel<3, false><<<c->grid_mr2, MR_THREADS, 0, s>>>(c->plan, c->q, out, cw); break;
+        default: mr2_kernel<3, true><<<c->grid_mr2, MR_THREADS, 0, s>>>(c->plan, c->q, out, cw); break;
+    }
+    CKL("mr2_kernel");
+    return ISP_OK;
+}
+
+// The whole hot path for dN[0..n) on stream s.  Caller holds g_mu.
+int device_impl(Ctx* c, const unsigned long long* dN, uint8_t* dout, size_t n, cudaStream_t s) {
+    const size_t chunk = (size_t)1 << g_opt.chunk_log2;
+    int rc = ensure_queues(c, n < chunk ? n : chunk);
+    if (rc != ISP_OK) return rc;
+    if (c->has_last && c->last_stream != (void*)s) CK(cudaStreamWaitEvent(s, c->last_done, 0));
+    PlanParams P;
+    P.force = g_opt.force_path;
+    P.wmax = g_opt.sieve_max;
+    P.sieve_ps_per_int = (float)g_opt.sieve_fs_per_int * 1e-3f;
+    P.sieve_fixed_ps = (float)g_opt.sieve_fixed_ns * 1e3f;
+    P.mr32_ps_per_bit = (float)g_opt.mr32_fs_per_bit * 1e-3f;
+    TDParams td;
+    td.n32 = g_opt.td32;
+    td.n64 = g_opt.td64;
+    {
+        const unsigned long long pn = c->hbp[td.n32].x;  // first prime not trial-divided
+        const unsigned long long sq = pn * pn;
+        td.sq32 = sq > 0xFFFFFFFFull ? 0xFFFFFFFFu : (uint32_t)sq;
+    }
+    for (size_t base = 0; base < n; base += chunk) {
+        const uint32_t len = (uint32_t)((n - base) < chunk ? (n - base) : chunk);
+        const unsigned long long* N = dN + base;
+        uint8_t* out = dout + base;
+        P.invalidate = (base == 0 && !g_opt.sieve_cache) ? 1 : 0;
+        {
+            KScope ks(K_PLAN, s);
+            plan_kernel<<<1, 1024, 0, s>>>(N, len, c->plan, P);
+            CKL("plan_kernel");
+        }
+        {
+            KScope ks(K_SIEVE, s);
+            sieve_kernel<<<c->grid_sieve, SIEVE_THREADS, SEG_ODD, s>>>(c->plan, c->bitmap, c->bp, c->nbp, c->patt,
+                                                                         (uint32_t)g_opt.warp_p);
+            CKL("sieve_kernel");
+        }
+        const uint32_t ntiles = (len + CLS_TILE - 1) / CLS_TILE;
+        const int gcls = (int)(ntiles < (uint32_t)c->grid_cls ? ntiles : (uint32_t)c->grid_cls);
+        const bool vec = (((uintptr_t)N & 15) == 0) && (((uintptr_t)out & 1) == 0);
+        {
+            KScope ks(K_CLASSIFY, s);
+            if (vec) classify_kernel<true><<<gcls, CLS_THREADS, 0, s>>>(N, out, len, c->plan, c->bitmap, c->q, td);
+            else classify_kernel<false><<<gcls, CLS_THREADS, 0, s>>>(N, out, len, c->plan, c->bitmap, c->q, td);
+            CKL("classify_kernel");
+        }
+        {
+            KScope ks(K_MR1, s);
+            mr1_kernel<<<c->grid_mr1, MR_THREADS, 0, s>>>(c->plan, c->q, g_opt.kernel_timing);
+            CKL("mr1_kernel");
+        }
+        {
+            KScope ks(K_MR2, s);
+            rc = launch_mr2(c, s, out);
+        }
+        if (rc != ISP_OK) return rc;
+    }
+    CK(cudaEventRecord(c->last_done, s));
+    c->has_last = true;
+    c->last_stream = (void*)s;
+    return ISP_OK;
+}
+
+int ensure_staging(Ctx* c, size_t cap, bool need_hin, bool need_hout) {
+    if (cap > c->hcap) {
+        for (int k = 0; k < 2; k++) {
+            if (c->din[k]) cudaFree(c->din[k]);
+            if (c->dout[k]) cudaFree(c->dout[k]);
+            if (c->hin[k]) cudaFreeHost(c->hin[k]);
+            if (c->hout[k]) cudaFreeHost(c->hout[k]);
+            c->din[k] = nullptr; c->dout[k] = nullptr; c->hin[k] = nullptr; c->hout[k] = nullptr;
+        }
+        c->hcap = 0;
+        for (int k = 0; k < 2; k++) {
+            if (cudaMalloc(&c->din[k], cap * 8) != cudaSuccess || cudaMalloc(&c->dout[k], cap) != cudaSuccess) {
+                cudaGetLastError();
+                g_err = "staging allocation failed";
+                return ISP_ENOMEM;
+            }
+        }
+        c->hcap = cap;
+    }
+    for (int k = 0; k < 2; k++) {
+        if (need_hin && !c->hin[k] && cudaMallocHost(&c->hin[k], c->hcap * 8) != cudaSuccess) {
+            cudaGetLastError(); g_err = "pinned allocation failed"; return ISP_ENOMEM;
+        }
+        if (need_hout && !c->hout[k] && cudaMallocHost(&c->hout[k], c->hcap) != cudaSuccess) {
+            cudaGetLastError(); g_err = "pinned allocation failed"; return ISP_ENOMEM;
+        }
+    }
+    return ISP_OK;
+}
+
+bool is_pinned(const void* p) {
+    cudaPointerAttributes a;
+    if (cudaPointerGetAttributes(&a, p) != cudaSuccess) { cudaGetLastError(); return false; }
+    return a.type == cudaMemoryTypeHost;
+}
+
+}  // namespace
+
+extern "C" {
+
+int isprime_device(const uint64_t* dN, uint8_t* dout, size_t n, void* stream) {
+    if (n == 0) return ISP_OK;
+    if (!dN || !dout) return ISP_EINVAL;
+    if (overlaps(dN, n * 8, dout, n)) return ISP_EINVAL;
+    std::lock_guard<std::mutex> lk(g_mu);
+    Ctx* c = nullptr;
+    int rc = get_ctx(&c);
+    if (rc != ISP_OK) return rc;
+    return device_impl(c, reinterpret_cast<const unsigned long long*>(dN), dout, n, (cudaStream_t)stream);
+}
+
+int isprime_popcount_device(const uint8_t* dout, size_t n, uint64_t* dcount, void* stream) {
+    if (!dcount) return ISP_EINVAL;
+    if (n > 0 && !dout) return ISP_EINVAL;
+    std::lock_guard<std::mutex> lk(g_mu);
+    Ctx* c = nullptr;
+    int rc = get_ctx(&c);
+    if (rc != ISP_OK) return rc;
+    cudaStream_t s = (cudaStream_t)stream;
+    CK(cudaMemsetAsync(dcount, 0, 8, s));
+    if (n == 0) return ISP_OK;
+    KScope ks(K_POPCOUNT, s);
+    popcount_kernel<<<c->sms * 4, 256, 0, s>>>(dout, n, reinterpret_cast<unsigned long long*>(dcount));
+    CKL("popcount_kernel");
+    return ISP_OK;
+}
+
+int isprime_count_device(const uint64_t* dN, uint8_t* dout, size_t n, uint64_t* dcount, void* stream) {
+    int rc = isprime_device(dN, dout, n, stream);
+    if (rc != ISP_OK) return rc;
+    return isprime_popcount_device(dout, n, dcount, stream);
+}
+
+int isprime(const uint64_t* N, uint8_t* out, size_t n) {
+    if (n == 0) return ISP_OK;
+    if (!N || !out) return ISP_EINVAL;
+    if (overlaps(N, n * 8, out, n)) return ISP_EINVAL;
+    std::lock_guard<std::mutex> lk(g_mu);
+    Ctx* c = nullptr;
+    int rc = get_ctx(&c);
+    if (rc != ISP_OK) return rc;
+    const bool in_pinned = is_pinned(N);
+    const bool out_pinned = is_pinned(out);
+    const size_t hchunk = n < ((size_t)1 << 24) ? n : ((size_t)1 << 24);
+    rc = ensure_staging(c, hchunk, !in_pinned, !out_pinned);
+    if (rc != ISP_OK) return rc;
+    size_t pend_base[2] = {0, 0}, pend_len[2] = {0, 0};
+    int ci = 0;
+    for (size_t base = 0; base < n; base += hchunk, ci++) {
+        const int k = ci & 1;
+        cudaStream_t s = c->hs[k];
+        const size_t len = (n - base) < hchunk ? (n - base) : hchunk;
+        const void* src = N + base;
+        if (!in_pinned) {
+            CK(cudaEventSynchronize(c->ev_h2d[k]));  // slot's previous upload finished
+            memcpy(c->hin[k], N + base, len * 8);
+            src = c->hin[k];
+        }
+        CK(cudaMemcpyAsync(c->din[k], src, len * 8, cudaMemcpyHostToDevice, s));
+        CK(cudaEventRecord(c->ev_h2d[k], s));
+        rc = device_impl(c, c->din[k], c->dout[k], len, s);
+        if (rc != ISP_OK) return rc;
+        if (!out_pinned) {
+            CK(cudaEventSynchronize(c->ev_d2h[k]));
+            if (pend_len[k]) memcpy(out + pend_base[k], c->hout[k], pend_len[k]);
+            pend_len[k] = 0;
+            CK(cudaMemcpyAsync(c->hout[k], c->dout[k], len, cudaMemcpyDeviceToHost, s));
+            pend_base[k] = base;
+            pend_len[k] = len;
+        } else {
+            CK(cudaMemcpyAsync(out + base, c->dout[k], len, cudaMemcpyDeviceToHost, s));
+        }
+        CK(cudaEventRecord(c->ev_d2h[k], s));
+    }
+    for (int k = 0; k < 2; k++) {
+        CK(cudaStreamSynchronize(c->hs[k]));
+        if (pend_len[k]) memcpy(out + pend_base[k], c->hout[k], pend_len[k]);
+    }
+    return ISP_OK;
+}
+
+const char* isprime_strerror(int status) {
+    static thread_local std::string msg;
+    switch (status) {
+        case ISP_OK: msg = "ok"; break;
+        case ISP_EINVAL: msg = "invalid argument (NULL pointer with n > 0, overlapping buffers, or bad option)"; break;
+        case ISP_ENOMEM: msg = "out of memory: " + g_err; break;
+        case ISP_ECUDA: msg = "CUDA error: " + g_err; break;
+        case ISP_ENODEV: msg = "no CUDA device"; break;
+        default: msg = "unknown status"; break;
+    }
+    return msg.c_str();
+}
+
+void isprime_shutdown(void) {
+    std::lock_guard<std::mutex> lk(g_mu);
+    int cur = 0;
+    cudaGetDevice(&cur);
+    for (size_t d = 0; d < g_ctx.size(); d++) {
+        Ctx* c = g_ctx[d];
+        if (!c) continue;
+        cudaSetDevice((int)d);
+        cudaDeviceSynchronize();
+        cudaFree(c->bp); cudaFree(c->patt); cudaFree(c->bitmap); cudaFree(c->plan);
+        if (c->qmem) cudaFree(c->qmem);
+        for (int k = 0; k < 2; k++) {
+            if (c->din[k]) cudaFree(c->din[k]);
+            if (c->dout[k]) cudaFree(c->dout[k]);
+            if (c->hin[k]) cudaFreeHost(c->hin[k]);
+            if (c->hout[k]) cudaFreeHost(c->hout[k]);
+            if (c->hs[k]) cudaStreamDestroy(c->hs[k]);
+            if (c->ev_h2d[k]) cudaEventDestroy(c->ev_h2d[k]);
+            if (c->ev_d2h[k]) cudaEventDestroy(c->ev_d2h[k]);
+        }
+        if (c->last_done) cudaEventDestroy(c->last_done);
+        delete c;
+        g_ctx[d] = nullptr;
+    }
+    cudaSetDevice(cur);
+}
+
+int isprime_set_option(const char* key, long long v) {
+    if (!key) return ISP_EINVAL;
+    std::lock_guard<std::mutex> lk(g_mu);
+    read_env_once();
+    if (!strcmp(key, "force_path")) { if (v < 0 || v > 2) return ISP_EINVAL; g_opt.force_path = (int)v; }
+    else if (!strcmp(key, "bases32")) { if (v != 3 && v != 7) return ISP_EINVAL; g_opt.bases32 = (int)v; }
+    else if (!strcmp(key, "td_primes32")) { if (v < 0 || v > MAX_TD) return ISP_EINVAL; g_opt.td32 = (int)v; }
+    else if (!strcmp(key, "td_primes64")) { if (v < 0 || v > MAX_TD) return ISP_EINVAL; g_opt.td64 = (int)v; }
+    else if (!strcmp(key, "chunk_log2")) { if (v < 16 || v > 31) return ISP_EINVAL; g_opt.chunk_log2 = (int)v; }
+    else if (!strcmp(key, "win64")) { if (v < 1 || v > 3) return ISP_EINVAL; g_opt.win64 = (int)v; }
+    else if (!strcmp(key, "warp_p")) { if (v < 17 || v > 65536) return ISP_EINVAL; g_opt.warp_p = (int)v; }
+    else if (!strcmp(key, "sieve_fs_per_int")) { if (v < 0) return ISP_EINVAL; g_opt.sieve_fs_per_int = v; }
+    else if (!strcmp(key, "sieve_fixed_ns")) { if (v < 0) return ISP_EINVAL; g_opt.sieve_fixed_ns = v; }
+    else if (!strcmp(key, "mr32_fs_per_bit")) { if (v < 0) return ISP_EINVAL; g_opt.mr32_fs_per_bit = v; }
+    else if (!strcmp(key, "kernel_timing")) { if (v < 0 || v > 1) return ISP_EINVAL; g_opt.kernel_timing = (int)v; }
+    else if (!strcmp(key, "sieve_cache")) { if (v < 0 || v > 1) return ISP_EINVAL; g_opt.sieve_cache = (int)v; }
+    else return ISP_EINVAL;
+    return ISP_OK;
+}
+
+long long isprime_get_option(const char* key) {
+    if (!key) return -1;
+    std::lock_guard<std::mutex> lk(g_mu);
+    read_env_once();
+    if (!strcmp(key, "force_path")) return g_opt.force_path;
+    if (!strcmp(key, "bases32")) return g_opt.bases32;
+    if (!strcmp(key, "td_primes32")) return g_opt.td32;
+    if (!strcmp(key, "td_primes64")) return g_opt.td64;
+    if (!strcmp(key, "chunk_log2")) return g_opt.chunk_log2;
+    if (!strcmp(key, "win64")) return g_opt.win64;
+    if (!strcmp(key, "warp_p")) return g_opt.warp_p;
+    if (!strcmp(key, "sieve_fs_per_int")) return g_opt.sieve_fs_per_int;
+    if (!strcmp(key, "sieve_fixed_ns")) return g_opt.sieve_fixed_ns;
+    if (!strcmp(key, "mr32_fs_per_bit")) return g_opt.mr32_fs_per_bit;
+    if (!strcmp(key, "kernel_timing")) return g_opt.kernel_timing;
+    if (!strcmp(key, "sieve_cache")) return g_opt.sieve_cache;
+    return -1;
+}
+
+int isprime_get_stats(isprime_stats* st) {
+    if (!st) return ISP_EINVAL;
+    std::lock_guard<std::mutex> lk(g_mu);
+    Ctx* c = nullptr;
+    int rc = get_ctx(&c);
+    if (rc != ISP_OK) return rc;
+    CK(cudaDeviceSynchronize());
+    DevPlan p;
+    CK(cudaMemcpy(&p, c->plan, sizeof(p), cudaMemcpyDeviceToHost));
+    st->window_lo = p.wlo;
+    st->window_hi = p.whi;
+    st->sieve_runs = p.sieve_runs;
+    st->sieved_integers = p.sieved_ints;
+    st->queued32 = p.total[0] + p.counts[0];
+    st->queued64 = p.total[1] + p.counts[1];
+    st->passed32 = p.total[2] + p.counts[2];
+    st->passed64 = p.total[3] + p.counts[3];
+    st->chunks = p.chunks;
+    st->kernel_launches = g_launches;
+    for (int k = 0; k < 4; k++) st->mulmods[k] = p.work[k];
+    return ISP_OK;
+}
+
+int isprime_reset_stats(void) {
+    std::lock_guard<std::mutex> lk(g_mu);
+    Ctx* c = nullptr;
+    int rc = get_ctx(&c);
+    if (rc != ISP_OK) return rc;
+    CK(cudaDeviceSynchronize());
+    DevPlan p;
+    CK(cudaMemcpy(&p, c->plan, sizeof(p), cudaMemcpyDeviceToHost));
+    for (int k = 0; k < 4; k++) { p.total[k] = 0; p.counts[k] = 0; }
+    p.sieve_runs = 0;
+    p.sieved_ints = 0;
+    p.chunks = 0;
+    for (int k = 0; k < 4; k++) p.work[k] = 0;
+    p.valid_lo = p.valid_hi = 0;  // forget the bitmap: the next call sieves again
+    CK(cudaMemcpy(c->plan, &p, sizeof(p), cudaMemcpyHostToDevice));
+    g_launches = 0;
+    return ISP_OK;
+}
+
+int isprime_get_kernel_times(isprime_kernel_time* out, int max, int* count) {
+    std::lock_guard<std::mutex> lk(g_mu);
+    kt_drain();
+    if (count) *count = K_NUM;
+    if (!out) return ISP_OK;
+    for (int k = 0; k < K_NUM && k < max; k++) {
+        memset(out[k].name, 0, sizeof(out[k].name));
+        strncpy(out[k].name, k_names[k], sizeof(out[k].name) - 1);
+        out[k].launches = g_kt_n[k];
+        out[k].ms_total = g_kt_ms[k];
+    }
+    return ISP_OK;
+}
+
+int isprime_reset_kernel_times(void) {
+    std::lock_guard<std::mutex> lk(g_mu);
+    kt_drain();
+    for (int k = 0; k < K_NUM; k++) { g_kt_ms[k] = 0; g_kt_n[k] = 0; }
+    return ISP_OK;
+}
+
+int isprime_sprp_device(const uint64_t* dn, const uint64_t* da, uint8_t* dout, size_t count, void* stream) {
+    if (count == 0) return ISP_OK;
+    if (!dn || !da || !dout) return ISP_EINVAL;
+    std::lock_guard<std::mutex> lk(g_mu);
+    Ctx* c = nullptr;
+    int rc = get_ctx(&c);
+    if (rc != ISP_OK) return rc;
+    const unsigned blocks = (unsigned)((count + 255) / 256);
+    cudaStream_t s = (cudaStream_t)stream;
+    const auto* n = reinterpret_cast<const unsigned long long*>(dn);
+    const auto* a = reinterpret_cast<const unsigned long long*>(da);
+    if (g_opt.win64 == 1) sprp_diag_kernel<1><<<blocks, 256, 0, s>>>(n, a, dout, count);
+    else if (g_opt.win64 == 2) sprp_diag_kernel<2><<<blocks, 256, 0, s>>>(n, a, dout, count);
+    else sprp_diag_kernel<3><<<blocks, 256, 0, s>>>(n, a, dout, count);
+    CKL("sprp_diag_kernel");
+    return ISP_OK;
+}
+
+int isprime_mulmod_device(const uint64_t* da, const uint64_t* db, const uint64_t* dm, uint64_t* dout, size_t count,
+                          void* stream) {
+    if (count == 0) return ISP_OK;
+    if (!da || !db || !dm || !dout) return ISP_EINVAL;
+    std::lock_guard<std::mutex> lk(g_mu);
+    Ctx* c = nullptr;
+    int rc = get_ctx(&c);
+    if (rc != ISP_OK) return rc;
+    const unsigned blocks = (unsigned)((count + 255) / 256);
+    mulmod_diag_kernel<<<blocks, 256, 0, (cudaStream_t)stream>>>(
+        reinterpret_cast<const unsigned long long*>(da), reinterpret_cast<const unsigned long long*>(db),
+        reinterpret_cast<const unsigned long long*>(dm), reinterpret_cast<unsigned long long*>(dout), count);
+    CKL("mulmod_diag_kernel");
+    return ISP_OK;
+}
+
+}  // extern "C"

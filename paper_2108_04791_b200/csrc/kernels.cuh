@@ -1,0 +1,662 @@
+// kernels.cuh -- the hot-path kernels of libisprime (layer L1), sm_100a.
+//
+//   plan_kernel       A0  strided sample of N -> sieve window (cost model)
+//   sieve_kernel      A1  odd-only segmented sieve of Eratosthenes in shared
+//                         memory -> global bitmap for the window [wlo, whi)
+//   classify_kernel   A2  one streaming pass over N: trivial cases, window
+//                         gather out[i] = bit(N[i]), small-prime trial
+//                         division, ballot/scan compaction of survivors
+//   mr1_kernel        A3  Miller-Rabin base 2 on the compacted survivors,
+//                         compacting strong probable primes again
+//   mr2_kernel        A4  the remaining bases, lockstep per element, out = 1
+//
+// Cites: PAPER.md:22 / 279 (sieve, membership instead of division), :275-276
+// (shrinking by small primes), :37-56 (Miller-Rabin, Eq 4 bases), :299-330
+// (choosing the array path from the element count and the maximum).
+#pragma once
+#include <stdint.h>
+#include "witness.cuh"
+
+namespace isp {
+
+constexpr int MAX_TD = 128;             // trial-division primes held in constant memory
+constexpr uint32_t SEG_ODD = 96 * 1024; // odd integers (bytes) per sieve segment
+constexpr int SIEVE_THREADS = 512;
+constexpr int PRESIEVE_PERIOD = 3 * 5 * 7 * 11 * 13;  // 15015 (odd-index period)
+constexpr int PRESIEVE_COPIES = 16;                   // shifted copies for 16-B loads
+constexpr int PRESIEVE_LEN = ((PRESIEVE_PERIOD + SEG_ODD + 64 + 15) / 16) * 16;
+constexpr int FIRST_CROSS_PRIME_IDX = 5;              // odd primes 3,5,7,11,13 pre-sieved
+constexpr int CLS_THREADS = 256;
+constexpr int CLS_PAIRS = 4;                          // 2 elements per pair -> 8 per thread
+constexpr int CLS_TILE = CLS_THREADS * 2 * CLS_PAIRS; // 2048 elements per tile
+constexpr int MR_THREADS = 256;
+
+// Device-resident plan and counters (one per device context).
+struct DevPlan {
+    unsigned long long wlo, whi;            // window for the current chunk
+    unsigned long long valid_lo, valid_hi;  // range the bitmap currently holds
+    unsigned int sieve_needed;
+    unsigned int counts[4];                 // Q32, Q64, P32, P64 of the current chunk
+    unsigned int pad;
+    unsigned long long total[4];            // accumulated Q32, Q64, P32, P64
+    unsigned long long sieve_runs, sieved_ints, chunks;
+    // algorithmic modular multiplications (square-and-multiply count of the
+    // method), accumulated only when work counting is on:
+    // [mr1 32-bit, mr1 64-bit, mr2 32-bit, mr2 64-bit]
+    unsigned long long work[4];
+};
+
+// Host -> plan kernel parameters (cost model in picoseconds on a full GPU).
+struct PlanParams {
+    int force;                 // 0 auto, 1 sieve, 2 mr
+    unsigned long long wmax;   // largest window span (bitmap capacity, <= 2^32)
+    float sieve_ps_per_int;    // sieve cost per integer of span
+    float sieve_fixed_ps;      // fixed cost of one sieve pass
+    float mr32_ps_per_bit;     // MR cost per odd element per bit (n < 2^32)
+    int invalidate;            // 1: forget the bitmap held from an earlier call (first chunk of a call)
+};
+
+struct Queues {
+    uint32_t* q32_idx; uint32_t* q32_val;
+    uint32_t* q64_idx; unsigned long long* q64_val;
+    uint32_t* p32_idx; uint32_t* p32_val;
+    uint32_t* p64_idx; unsigned long long* p64_val;
+};
+
+struct TDParams {
+    int n32, n64;              // primes used for the 32-bit / 64-bit classes
+    uint32_t sq32;             // (first prime not tested)^2 capped: v below it with no factor is prime
+};
+
+// Trial-division constants: p, p^-1 mod 2^32 / 2^64, floor((2^k - 1) / p).
+// p | v  <=>  v * p^-1 mod 2^k <= floor((2^k - 1) / p)   (v < 2^k, p odd)
+__constant__ uint32_t c_td_p[MAX_TD];
+__constant__ uint32_t c_td_inv32[MAX_TD];
+__constant__ uint32_t c_td_lim32[MAX_TD];
+__constant__ unsigned long long c_td_inv64[MAX_TD];
+__constant__ unsigned long long c_td_lim64[MAX_TD];
+
+// Remaining Eq 4 bases after base 2, and the {7, 61} set for
+// n < 2^32 (Jaeschke: exact below 4,759,123,141 > 2^32; verified exhaustively
+// over [0, 2^32) by the force-path equivalence test).
+__constant__ unsigned long long c_bases64[6] = {325ull, 9375ull, 28178ull, 450775ull, 9780504ull, 1795265022ull};
+__constant__ uint32_t c_bases32_full[6] = {325u, 9375u, 28178u, 450775u, 9780504u, 1795265022u};
+__constant__ uint32_t c_bases32_red[2] = {7u, 61u};
+
+// ------------------------------------------------------------- init kernels
+// Odd primes below 65536 in increasing order (6541 of them), with
+// ceil(2^32 / p) for the sieve's remainder computation.  One block.
+__global__ void __launch_bounds__(1024) init_base_primes_kernel(uint2* out, int* count) {
+    __shared__ uint8_t comp[32768];  // comp[j] <-> odd 2j+1
+    __shared__ int warp_tot[32];
+    const int tid = threadIdx.x;
+    for (int j = tid; j < 32768; j += blockDim.x) comp[j] = (j == 0);
+    __syncthreads();
+    for (int j = 1 + tid; j < 128; j += blockDim.x) {  // odd p = 2j+1 < 256
+        if (comp[j]) continue;
+        uint32_t p = 2 * j + 1;
+        for (uint32_t m = p * p; m < 65536; m += 2 * p) comp[m >> 1] = 1;
+    }
+    __syncthreads();
+    // ordered compaction, blockDim == 1024: each thread owns 32 consecutive j
+    const int j0 = tid * 32;
+    int c = 0;
+    for (int k = 0; k < 32; k++) c += (j0 + k > 0) && !comp[j0 + k];
+    int incl = c;
+    const int lane = tid & 31, wid = tid >> 5;
+    for (int o = 1; o < 32; o <<= 1) {
+        int y = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += y;
+    }
+    if (lane == 31) warp_tot[wid] = incl;
+    __syncthreads();
+    if (wid == 0) {
+        int t = warp_tot[lane];
+        int ti = t;
+        for (int o = 1; o < 32; o <<= 1) {
+            int y = __shfl_up_sync(0xffffffffu, ti, o);
+            if (lane >= o) ti += y;
+        }
+        warp_tot[lane] = ti - t;  // exclusive
+        if (lane == 31) *count = ti;
+    }
+    __syncthreads();
+    int pos = warp_tot[wid] + incl - c;
+    for (int k = 0; k < 32; k++) {
+        const int j = j0 + k;
+        if (j > 0 && !comp[j]) {
+            const uint32_t p = 2u * j + 1u;
+            const uint32_t cinv = (uint32_t)(0xFFFFFFFFu / p) + 1u;  // ceil(2^32/p), p not a power of 2
+            out[pos++] = make_uint2(p, cinv);
+        }
+    }
+}
+
+// Trial-division constants for the first MAX_TD odd primes (one warp-block).
+__global__ void init_td_kernel(const uint2* bp, uint32_t* p32, uint32_t* inv32v, uint32_t* lim32,
+                               unsigned long long* inv64v, unsigned long long* lim64) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= MAX_TD) return;
+    const uint32_t p = bp[i].x;
+    p32[i] = p;
+    inv32v[i] = inv32(p);
+    lim32[i] = 0xFFFFFFFFu / p;
+    inv64v[i] = inv64(p);
+    lim64[i] = 0xFFFFFFFFFFFFFFFFull / p;
+}
+
+// Pre-sieve pattern for 3, 5, 7, 11, 13 over odd indices g (odd v = 2g + 1):
+// copy r holds ext[j + r] with ext[g] = 1 iff gcd(2g+1, 15015) == 1.
+__global__ void init_presieve_kernel(uint8_t* patt) {
+    const int total = PRESIEVE_COPIES * PRESIEVE_LEN;
+    for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < total; t += gridDim.x * blockDim.x) {
+        const int r = t / PRESIEVE_LEN, j = t % PRESIEVE_LEN;
+        const uint32_t v = 2u * (uint32_t)((j + r) % PRESIEVE_PERIOD) + 1u;
+        patt[t] = (v % 3 != 0) && (v % 5 != 0) && (v % 7 != 0) && (v % 11 != 0) && (v % 13 != 0);
+    }
+}
+
+// ------------------------------------------------------------- A0: plan
+// One block of 1024 threads.  Samples up to 32768 elements at evenly spaced
+// positions, builds a histogram of bit lengths of the odd values below 2^32
+// and their min / max, and chooses the window minimising
+//   sieve cost (fixed + span) + MR cost of the small odd values it misses.
+// The plan changes only the time, never the result: any element outside the
+// window takes the trial-division / Miller-Rabin route.
+__global__ void __launch_bounds__(1024) plan_kernel(const unsigned long long* __restrict__ N, unsigned long long len,
+                            DevPlan* plan, PlanParams P) {
+    __shared__ unsigned int hist[33];
+    __shared__ unsigned long long smin, smax;
+    __shared__ unsigned int in_valid, nsamp_small;
+    const int tid = threadIdx.x;
+    if (tid < 33) hist[tid] = 0;
+    if (tid == 0) { smin = ~0ull; smax = 0; in_valid = 0; nsamp_small = 0; }
+    __syncthreads();
+    const unsigned long long vlo = P.invalidate ? 0ull : plan->valid_lo;
+    const unsigned long long vhi = P.invalidate ? 0ull : plan->valid_hi;
+    const unsigned long long S = len < 32768ull ? len : 32768ull;
+    unsigned long long lmin = ~0ull, lmax = 0;
+    unsigned int lin = 0, lcnt = 0;
+    if (P.force == 0) {
+        for (unsigned long long k = tid; k < S; k += blockDim.x) {
+            const unsigned long long v = N[(k * len) / S];
+            if ((v & 1ull) && v < (1ull << 32) && v > 1) {
+                atomicAdd(&hist[64 - __clzll((long long)v)], 1u);
+                lmin = v < lmin ? v : lmin;
+                lmax = v > lmax ? v : lmax;
+                lin += (v >= vlo && v < vhi);
+                lcnt++;
+            }
+        }
+        atomicMin(&smin, lmin);
+        atomicMax(&smax, lmax);
+        atomicAdd(&in_valid, lin);
+        atomicAdd(&nsamp_small, lcnt);
+    }
+    __syncthreads();
+    if (tid != 0) return;
+    unsigned long long wlo = 0, whi = 0;
+    const unsigned long long wmax = P.wmax;
+    if (P.force == 1) {
+        wlo = 0; whi = wmax;
+    } else if (P.force == 0 && nsamp_small > 0 && S > 0) {
+        const double scale = (double)len / (double)S;  // elements per sample
+        double mr_all = 0.0;
+        double mr_b[33];
+        for (int b = 0; b <= 32; b++) {
+            mr_b[b] = (double)hist[b] * scale * (double)P.mr32_ps_per_bit * b;
+            mr_all += mr_b[b];
+        }
+        double best = mr_all;  // no window
+        // candidate: the range the bitmap already holds (no sieve cost)
+        if (vhi > vlo) {
+            const double miss = mr_all * (1.0 - (double)in_valid / (double)nsamp_small);
+            if (miss < best) { best = miss; wlo = vlo; whi = vhi; }
+        }
+        // candidates [0, 2^k)
+        double covered = 0.0;
+        for (int k = 1; k <= 32; k++) {
+            covered += mr_b[k];
+            const unsigned long long span = 1ull << k;
+            if (span > wmax) break;
+            const double c = P.sieve_fixed_ps + (double)span * P.sieve_ps_per_int + (mr_all - covered);
+            if (c < best) { best = c; wlo = 0; whi = span; }
+        }
+        // candidate [min - margin, max + margin) of the sampled small values
+        {
+            const unsigned long long mn = smin, mx = smax;
+            const unsigned long long margin = (unsigned long long)(((double)(mx - mn) / (double)nsamp_small) * 4.0) + 64;
+            unsigned long long lo = mn > margin ? mn - margin : 0;
+            unsigned long long hi = mx + margin + 1;
+            if (hi > (1ull << 32)) hi = 1ull << 32;
+            lo &= ~63ull;
+            hi = (hi + 63) & ~63ull;
+            if (hi - lo <= wmax) {
+                const double c = P.sieve_fixed_ps + (double)(hi - lo) * P.sieve_ps_per_int;
+                if (c < best) { best = c; wlo = lo; whi = hi; }
+            }
+        }
+    }
+    if (whi > wmax) whi = wmax;  // (force mode only)
+    unsigned int need = 0;
+    if (whi > wlo && !(wlo >= vlo && whi <= vhi)) {
+        need = 1;
+        plan->valid_lo = wlo;
+        plan->valid_hi = whi;
+        plan->sieve_runs += 1;
+        plan->sieved_ints += whi - wlo;
+    }
+    plan->wlo = wlo;
+    plan->whi = whi;
+    plan->sieve_needed = need;
+    for (int q = 0; q < 4; q++) { plan->total[q] += plan->counts[q]; plan->counts[q] = 0; }
+    plan->chunks += 1;
+}
+
+// ------------------------------------------------------------- A1: sieve
+// Odd-only segmented sieve over [wlo, whi) (wlo, whi multiples of 64,
+// whi <= 2^32).  Byte k of a segment stands for v = seg_lo + 2k + 1.  Bytes are
+// initialised from the {3,5,7,11,13} pre-sieve pattern, primes 17 <= p with
+// p^2 < seg_hi cross off their odd multiples from max(p^2, first in segment):
+// warp-cooperatively (lane l takes every 32nd multiple) for p < warp_p, one
+// prime per thread above.  Byte stores of 0 need no atomics.  The segment is
+// packed to bits with warp ballots and stored coalesced.
+__global__ void __launch_bounds__(SIEVE_THREADS, 2)
+sieve_kernel(const DevPlan* __restrict__ plan, uint32_t* __restrict__ bitmap,
+             const uint2* __restrict__ bp, int nbp, const uint8_t* __restrict__ patt,
+             uint32_t warp_p) {
+    extern __shared__ __align__(16) uint8_t seg[];
+    if (!plan->sieve_needed) return;
+    const unsigned long long wlo = plan->wlo, whi = plan->whi;
+    const unsigned long long span_odd = (whi - wlo) >> 1;
+    const unsigned long long nseg = (span_odd + SEG_ODD - 1) / SEG_ODD;
+    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+    constexpr int NWARPS = SIEVE_THREADS / 32;
+    for (unsigned long long sgi = blockIdx.x; sgi < nseg; sgi += gridDim.x) {
+        const unsigned long long seg_lo = wlo + 2ull * sgi * SEG_ODD;
+        const unsigned long long rem_odd = span_odd - sgi * SEG_ODD;
+        const uint32_t seg_len = rem_odd < SEG_ODD ? (uint32_t)rem_odd : SEG_ODD;
+        const unsigned long long seg_hi = seg_lo + 2ull * seg_len;  // exclusive
+        // init from the pre-sieve pattern (16-B loads and stores)
+        {
+            const uint32_t g0mod = (uint32_t)((seg_lo >> 1) % PRESIEVE_PERIOD);
+            const uint32_t r = g0mod & 15u;
+            const uint4* src = reinterpret_cast<const uint4*>(patt + (size_t)r * PRESIEVE_LEN + (g0mod - r));
+            uint4* dst = reinterpret_cast<uint4*>(seg);
+            for (uint32_t k = tid; k < SEG_ODD / 16; k += SIEVE_THREADS) dst[k] = __ldg(src + k);
+        }
+        __syncthreads();
+        if (seg_lo == 0 && tid == 0) {  // v = 1 is not prime; 3, 5, 7, 11, 13 are
+            seg[0] = 0; seg[1] = 1; seg[2] = 1; seg[3] = 1; seg[5] = 1; seg[6] = 1;
+        }
+        const uint32_t x = (uint32_t)(seg_lo + 1);  // first odd value, < 2^32
+        // warp-cooperative crossing, small primes
+        int i = FIRST_CROSS_PRIME_IDX + wid;
+        for (; i < nbp; i += NWARPS) {
+            const uint2 pc = bp[i];
+            const uint32_t p = pc.x;
+            if (p >= warp_p || (unsigned long long)p * p >= seg_hi) break;
+            uint32_t q = __umulhi(x, pc.y);
+            int32_t rr = (int32_t)(x - q * p);
+            if (rr < 0) rr += (int32_t)p;
+            unsigned long long m = (unsigned long long)x + (rr ? (p - (uint32_t)rr) : 0u);
+            if (!(m & 1ull)) m += p;
+            const unsigned long long pp = (unsigned long long)p * p;
+            if (m < pp) m = pp;
+            const unsigned long long k0 = (m - x) >> 1;
+            const uint32_t stride = 32u * p;
+            for (unsigned long long k = k0 + (unsigned long long)lane * p; k < seg_len; k += stride) seg[k] = 0;
+        }
+        // one prime per thread, larger primes: first index with p >= warp_p
+        {
+            // binary search for the first prime >= warp_p (uniform)
+            int lo = FIRST_CROSS_PRIME_IDX, hi = nbp;
+            while (lo < hi) {
+                const int mid = (lo + hi) >> 1;
+                if (bp[mid].x < warp_p) lo = mid + 1; else hi = mid;
+            }
+            for (int j = lo + tid; j < nbp; j += SIEVE_THREADS) {
+                const uint2 pc = bp[j];
+                const uint32_t p = pc.x;
+                if ((unsigned long long)p * p >= seg_hi) break;
+                uint32_t q = __umulhi(x, pc.y);
+                int32_t rr = (int32_t)(x - q * p);
+                if (rr < 0) rr += (int32_t)p;
+                unsigned long long m = (unsigned long long)x + (rr ? (p - (uint32_t)rr) : 0u);
+                if (!(m & 1ull)) m += p;
+                const unsigned long long pp = (unsigned long long)p * p;
+                if (m < pp) m = pp;
+                for (unsigned long long k = (m - x) >> 1; k < seg_len; k += p) seg[k] = 0;
+            }
+        }
+        __syncthreads();
+        // pack: word w of the segment = bytes [32w, 32w+32); 32 words per warp pass
+        {
+            const uint32_t nwords = seg_len >> 5;  // seg_len is a multiple of 32
+            uint32_t* dstw = bitmap + ((sgi * SEG_ODD) >> 5);
+            for (uint32_t w0 = (uint32_t)wid * 32u; w0 < nwords; w0 += NWARPS * 32u) {
+                uint32_t mine = 0;
+#pragma unroll 8
+                for (int j = 0; j < 32; j++) {
+                    const uint32_t w = w0 + j;
+                    const uint8_t b = (w < nwords) ? seg[w * 32u + lane] : 0;
+                    const uint32_t word = __ballot_sync(0xffffffffu, b != 0);
+                    if (lane == j) mine = word;
+                }
+                if (w0 + lane < nwords) dstw[w0 + lane] = mine;
+            }
+        }
+        __syncthreads();
+    }
+}
+
+// ------------------------------------------------------------- A2: classify
+// Per element v (PAPER.md:11-20 semantics):
+//   v < 2 -> 0;  v even -> (v == 2);  wlo <= v < whi -> bit of the sieve;
+//   v < 2^32: composite if an odd prime p <= p_n32 divides it (v != p), prime
+//             if no such p and v < (next prime)^2, else queue Q32;
+//   v >= 2^32: composite if an odd prime p <= p_n64 divides it, else queue Q64.
+// out[i] is written for every i (survivors get 0; phase 2 sets primes to 1).
+struct Item {
+    uint32_t cls;  // 0 resolved, 1 -> Q32, 2 -> Q64
+};
+
+__device__ __forceinline__ uint8_t classify_one(unsigned long long v, unsigned long long wlo, unsigned long long whi,
+                                                const uint32_t* __restrict__ bitmap, const TDParams& td,
+                                                uint32_t& cls) {
+    cls = 0;
+    if (v < 2ull) return 0;
+    if (!(v & 1ull)) return v == 2ull;
+    if (v >= wlo && v < whi) {
+        const unsigned long long b = (v - wlo) >> 1;
+        return (uint8_t)((__ldg(bitmap + (b >> 5)) >> (b & 31)) & 1u);
+    }
+    if (v < (1ull << 32)) {
+        const uint32_t v32 = (uint32_t)v;
+        bool comp = false;
+#pragma unroll 8
+        for (int k = 0; k < td.n32; k++)
+            comp |= (v32 * c_td_inv32[k] <= c_td_lim32[k]) && (v32 != c_td_p[k]);
+        if (comp) return 0;
+        if (v32 < td.sq32) return 1;
+        cls = 1;
+        return 0;
+    }
+    bool comp = false;
+#pragma unroll 8
+    for (int k = 0; k < td.n64; k++) comp |= (v * c_td_inv64[k] <= c_td_lim64[k]);
+    if (comp) return 0;
+    cls = 2;
+    return 0;
+}
+
+template <bool VEC>
+__global__ void __launch_bounds__(CLS_THREADS)
+classify_kernel(const unsigned long long* __restrict__ N, uint8_t* __restrict__ out, uint32_t len,
+                DevPlan* __restrict__ plan, const uint32_t* __restrict__ bitmap, Queues q, TDParams td) {
+    __shared__ uint32_t warp_tot[CLS_THREADS / 32];
+    __shared__ uint32_t blk_base32, blk_base64;
+    const unsigned long long wlo = plan->wlo, whi = plan->whi;
+    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+    const uint32_t ntiles = (len + CLS_TILE - 1) / CLS_TILE;
+    for (uint32_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+        const uint32_t tbase = tile * CLS_TILE;
+        unsigned long long v[2 * CLS_PAIRS];
+        uint32_t cls[2 * CLS_PAIRS];
+        uint8_t r[2 * CLS_PAIRS];
+        const bool full = tbase + CLS_TILE <= len;
+        if (VEC && full) {
+#pragma unroll
+            for (int j = 0; j < CLS_PAIRS; j++) {
+                const ulonglong2 t = __ldcs(reinterpret_cast<const ulonglong2*>(N + tbase + 2 * tid + 2 * CLS_THREADS * j));
+                v[2 * j] = t.x;
+                v[2 * j + 1] = t.y;
+            }
+        } else {
+#pragma unroll
+            for (int j = 0; j < CLS_PAIRS; j++) {
+#pragma unroll
+                for (int h = 0; h < 2; h++) {
+                    const uint32_t i = tbase + 2 * tid + 2 * CLS_THREADS * j + h;
+                    v[2 * j + h] = i < len ? N[i] : 0ull;
+                }
+            }
+        }
+        uint32_t c32 = 0, c64 = 0;
+#pragma unroll
+        for (int e = 0; e < 2 * CLS_PAIRS; e++) {
+            r[e] = classify_one(v[e], wlo, whi, bitmap, td, cls[e]);
+            const uint32_t i = tbase + 2 * tid + 2 * CLS_THREADS * (e >> 1) + (e & 1);
+            if (i >= len) cls[e] = 0;
+            c32 += cls[e] == 1;
+            c64 += cls[e] == 2;
+        }
+        // results
+        if (VEC && full) {
+#pragma unroll
+            for (int j = 0; j < CLS_PAIRS; j++) {
+                const unsigned short w = (unsigned short)(r[2 * j] | (r[2 * j + 1] << 8));
+                __stcs(reinterpret_cast<unsigned short*>(out + tbase + 2 * tid + 2 * CLS_THREADS * j), w);
+            }
+        } else {
+#pragma unroll
+            for (int e = 0; e < 2 * CLS_PAIRS; e++) {
+                const uint32_t i = tbase + 2 * tid + 2 * CLS_THREADS * (e >> 1) + (e & 1);
+                if (i < len) out[i] = r[e];
+            }
+        }
+        // block-wide exclusive scan of (c32, c64) packed in 16-bit halves
+        const uint32_t packed = c32 | (c64 << 16);
+        uint32_t incl = packed;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= o) incl += y;
+        }
+        if (lane == 31) warp_tot[wid] = incl;
+        __syncthreads();
+        if (wid == 0) {
+            const uint32_t t = lane < CLS_THREADS / 32 ? warp_tot[lane] : 0u;
+            uint32_t ti = t;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const uint32_t y = __shfl_up_sync(0xffffffffu, ti, o);
+                if (lane >= o) ti += y;
+            }
+            if (lane < CLS_THREADS / 32) warp_tot[lane] = ti - t;
+            if (lane == CLS_THREADS / 32 - 1) {
+                const uint32_t t32 = ti & 0xFFFFu, t64 = ti >> 16;
+                blk_base32 = t32 ? atomicAdd(&plan->counts[0], t32) : 0u;
+                blk_base64 = t64 ? atomicAdd(&plan->counts[1], t64) : 0u;
+            }
+        }
+        __syncthreads();
+        const uint32_t excl = warp_tot[wid] + incl - packed;
+        uint32_t p32 = blk_base32 + (excl & 0xFFFFu);
+        uint32_t p64 = blk_base64 + (excl >> 16);
+#pragma unroll
+        for (int e = 0; e < 2 * CLS_PAIRS; e++) {
+            const uint32_t i = tbase + 2 * tid + 2 * CLS_THREADS * (e >> 1) + (e & 1);
+            if (cls[e] == 1) { q.q32_idx[p32] = i; q.q32_val[p32] = (uint32_t)v[e]; p32++; }
+            else if (cls[e] == 2) { q.q64_idx[p64] = i; q.q64_val[p64] = v[e]; p64++; }
+        }
+        __syncthreads();  // warp_tot / bases reused by the next tile
+    }
+}
+
+// ------------------------------------------------------------- A3: MR phase 1
+// Warp-aggregated append of (idx, val) when `pred`.
+template <typename T>
+__device__ __forceinline__ void warp_append(bool pred, uint32_t idx, T val, unsigned int* counter,
+                                            uint32_t* qidx, T* qval) {
+    const unsigned int mask = __ballot_sync(0xffffffffu, pred);
+    if (!mask) return;
+    const int lane = threadIdx.x & 31;
+    const int leader = __ffs(mask) - 1;
+    unsigned int base = 0;
+    if (lane == leader) base = atomicAdd(counter, (unsigned int)__popc(mask));
+    base = __shfl_sync(0xffffffffu, base, leader);
+    if (pred) {
+        const unsigned int pos = base + __popc(mask & ((1u << lane) - 1u));
+        qidx[pos] = idx;
+        qval[pos] = val;
+    }
+}
+
+__device__ __forceinline__ unsigned long long warp_sum(unsigned long long v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+
+// Algorithmic multiplications of ModExp for exponent d (odd): (bitlen - 1)
+// squarings, plus (popcount - 1) multiplications by the base.
+__device__ __forceinline__ unsigned int modexp_squarings(unsigned long long d) { return 63 - __clzll((long long)d); }
+__device__ __forceinline__ unsigned int modexp_mults(unsigned long long d) { return __popcll(d) - 1; }
+__device__ __forceinline__ unsigned long long odd_part(unsigned long long n) { return (n - 1) >> (__ffsll((long long)(n - 1)) - 1); }
+
+__global__ void __launch_bounds__(MR_THREADS)
+mr1_kernel(DevPlan* __restrict__ plan, Queues q, int count_work) {
+    const unsigned int c32 = plan->counts[0], c64 = plan->counts[1];
+    unsigned long long w32 = 0, w64 = 0;
+    const unsigned int lane = threadIdx.x & 31;
+    const unsigned int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const unsigned int nwarps = (gridDim.x * blockDim.x) >> 5;
+    for (unsigned int b = warp * 32; b < c32; b += nwarps * 32) {
+        const unsigned int i = b + lane;
+        bool pass = false;
+        uint32_t n = 0, idx = 0;
+        if (i < c32) {
+            n = q.q32_val[i];
+            idx = q.q32_idx[i];
+            pass = sprp2_32(n);
+            if (count_work) w32 += modexp_squarings(odd_part(n));
+        }
+        warp_append<uint32_t>(pass, idx, n, &plan->counts[2], q.p32_idx, q.p32_val);
+    }
+    for (unsigned int b = warp * 32; b < c64; b += nwarps * 32) {
+        const unsigned int i = b + lane;
+        bool pass = false;
+        unsigned long long n = 0;
+        uint32_t idx = 0;
+        if (i < c64) {
+            n = q.q64_val[i];
+            idx = q.q64_idx[i];
+            pass = sprp2_64(n);
+            if (count_work) w64 += modexp_squarings(odd_part(n));
+        }
+        warp_append<unsigned long long>(pass, idx, n, &plan->counts[3], q.p64_idx, q.p64_val);
+    }
+    if (count_work) {
+        w32 = warp_sum(w32);
+        w64 = warp_sum(w64);
+        if ((threadIdx.x & 31) == 0) {
+            if (w32) atomicAdd(&plan->work[0], w32);
+            if (w64) atomicAdd(&plan->work[1], w64);
+        }
+    }
+}
+
+// ------------------------------------------------------------- A4: MR phase 2
+template <int WIN, bool FULL32>
+__global__ void __launch_bounds__(MR_THREADS)
+mr2_kernel(DevPlan* __restrict__ plan, Queues q, uint8_t* __restrict__ out, int count_work) {
+    const unsigned int c32 = plan->counts[2], c64 = plan->counts[3];
+    unsigned long long w32 = 0, w64 = 0;
+    const unsigned int stride = gridDim.x * blockDim.x;
+    const unsigned int t0 = blockIdx.x * blockDim.x + threadIdx.x;
+    for (unsigned int i = t0; i < c32; i += stride) {
+        const uint32_t n = q.p32_val[i];
+        const bool prime = FULL32 ? sprp_multi32<6>(n, c_bases32_full) : sprp_multi32<2>(n, c_bases32_red);
+        if (prime) out[q.p32_idx[i]] = 1;
+        if (count_work) {
+            const unsigned long long d = odd_part(n);
+            w32 += (unsigned long long)(FULL32 ? 6 : 2) * (modexp_squarings(d) + modexp_mults(d));
+        }
+    }
+    for (unsigned int i = t0; i < c64; i += stride) {
+        const unsigned long long n = q.p64_val[i];
+        if (sprp_multi64<6, WIN>(n, c_bases64)) out[q.p64_idx[i]] = 1;
+        if (count_work) {
+            const unsigned long long d = odd_part(n);
+            w64 += 6ull * (modexp_squarings(d) + modexp_mults(d));
+        }
+    }
+    if (count_work) {
+        w32 = warp_sum(w32);
+        w64 = warp_sum(w64);
+        if ((threadIdx.x & 31) == 0) {
+            if (w32) atomicAdd(&plan->work[2], w32);
+            if (w64) atomicAdd(&plan->work[3], w64);
+        }
+    }
+}
+
+// ------------------------------------------------------------- harness
+__global__ void popcount_kernel(const uint8_t* __restrict__ out, unsigned long long n,
+                                unsigned long long* __restrict__ count) {
+    unsigned long long c = 0;
+    const unsigned long long stride = (unsigned long long)gridDim.x * blockDim.x;
+    const unsigned long long t = blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x;
+    const unsigned long long nv = n / 16;
+    const uint4* o4 = reinterpret_cast<const uint4*>(out);
+    const bool aligned = (reinterpret_cast<uintptr_t>(out) & 15) == 0;
+    if (aligned) {
+        for (unsigned long long k = t; k < nv; k += stride) {
+            const uint4 w = o4[k];
+            c += __popc(w.x) + __popc(w.y) + __popc(w.z) + __popc(w.w);  // bytes are 0/1
+        }
+        for (unsigned long long k = nv * 16 + t; k < n; k += stride) c += out[k];
+    } else {
+        for (unsigned long long k = t; k < n; k += stride) c += out[k];
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) c += __shfl_down_sync(0xffffffffu, c, o);
+    if ((threadIdx.x & 31) == 0 && c) atomicAdd(count, c);
+}
+
+// diagnostics: per-pair strong test and Montgomery mulmod through the same code
+template <int WIN>
+__global__ void sprp_diag_kernel(const unsigned long long* __restrict__ n, const unsigned long long* __restrict__ a,
+                                 uint8_t* __restrict__ out, unsigned long long count) {
+    const unsigned long long i = blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x;
+    if (i >= count) return;
+    const unsigned long long nn = n[i], aa = a[i];
+    bool r = false;
+    if (nn >= 3 && (nn & 1ull)) {
+        if (nn < (1ull << 32)) {
+            const uint32_t am = (uint32_t)(aa % nn);
+            if (am == 2u) r = sprp2_32((uint32_t)nn);
+            else { const uint32_t b[1] = {am}; r = sprp_multi32<1>((uint32_t)nn, b); }
+        } else {
+            const unsigned long long am = aa % nn;
+            if (am == 2ull) r = sprp2_64(nn);
+            else { const unsigned long long b[1] = {am}; r = sprp_multi64<1, WIN>(nn, b); }
+        }
+    }
+    out[i] = r;
+}
+
+__global__ void mulmod_diag_kernel(const unsigned long long* __restrict__ a, const unsigned long long* __restrict__ b,
+                                   const unsigned long long* __restrict__ m, unsigned long long* __restrict__ out,
+                                   unsigned long long count) {
+    const unsigned long long i = blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x;
+    if (i >= count) return;
+    const unsigned long long mm = m[i];
+    if (mm < 3 || !(mm & 1ull)) { out[i] = 0; return; }
+    if (mm < (1ull << 32)) {
+        const Mont32 M = mont32_setup((uint32_t)mm);
+        const uint32_t R2 = mont32_r2(M);
+        const uint32_t am = mmul32((uint32_t)(a[i] % mm), R2, M);
+        const uint32_t bm = mmul32((uint32_t)(b[i] % mm), R2, M);
+        out[i] = mmul32(mmul32(am, bm, M), 1u, M);  // REDC(x * 1) leaves Montgomery form
+    } else {
+        const Mont64 M = mont64_setup(mm);
+        const unsigned long long R2 = mont64_r2(M);
+        const unsigned long long am = mmul64(a[i] % mm, R2, M);
+        const unsigned long long bm = mmul64(b[i] % mm, R2, M);
+        out[i] = mmul64(mmul64(am, bm, M), 1ull, M);
+    }
+}
+
+}  // namespace isp

@@ -1,0 +1,191 @@
+// witness.cuh -- strong-probable-prime (Miller-Rabin witness) tests on the
+// device, per element, for the two phases of the witness kernels.
+//
+// The test (Eq 1-3, reading G2): write n - 1 = 2^s d with d
+// odd; n passes base a iff a^d == 1 (mod n) or a^(2^r d) == -1 (mod n) for
+// some 0 <= r < s.  Bases are reduced mod n and a reduced base of 0 passes
+// (reading G3).  All values live in Montgomery form, where 1 and -1 are
+// M.one and M.mone.
+//
+// ModExp is left-to-right exponentiation by squaring.  The
+// per-lane bits of d differ across a warp, so the conditional multiply is a
+// SELECT, never a branch (no divergence); for base 2 the multiply is the
+// ModMultiply case-3 doubling, for other bases a fixed
+// window of WIN bits (table of a^0 .. a^(2^WIN - 1)) trades multiplies for a
+// register table.  Several bases of one n share d, so their chains run in
+// lockstep (NB independent chains per thread = instruction-level parallelism
+// for the IMAD pipe).
+#pragma once
+#include "modmath.cuh"
+
+namespace isp {
+
+// ---------------------------------------------------------------- 32-bit ----
+// Phase 1 (base 2).  n odd, 3 <= n < 2^32.
+__device__ __forceinline__ bool sprp2_32(uint32_t n) {
+    const Mont32 M = mont32_setup(n);
+    uint32_t d = n - 1;
+    const int s = __ffs(d) - 1;
+    d >>= s;
+    const int top = 31 - __clz(d);
+    uint32_t x = madd32(M.one, M.one, n);  // mont(2): top bit of d
+    for (int b = top - 1; b >= 0; b--) {
+        x = mmul32(x, x, M);
+        const uint32_t y = madd32(x, x, n);  // * 2 (ModMultiply case 3)
+        x = ((d >> b) & 1u) ? y : x;
+    }
+    if (x == M.one || x == M.mone) return true;
+    for (int r = 1; r < s; r++) {
+        x = mmul32(x, x, M);
+        if (x == M.mone) return true;
+        if (x == M.one) return false;
+    }
+    return false;
+}
+
+// Phase 2: all NB bases of `bases` (each reduced mod n) in lockstep.  Returns
+// true iff n passes every base.  n odd, 3 <= n < 2^32.
+template <int NB>
+__device__ __forceinline__ bool sprp_multi32(uint32_t n, const uint32_t* bases) {
+    const Mont32 M = mont32_setup(n);
+    const uint32_t R2 = mont32_r2(M);
+    uint32_t d = n - 1;
+    const int s = __ffs(d) - 1;
+    d >>= s;
+    const int top = 31 - __clz(d);
+    uint32_t A[NB], x[NB];
+    bool done[NB], pass[NB];
+#pragma unroll
+    for (int i = 0; i < NB; i++) {
+        uint32_t a = bases[i];
+        if (a >= n) a %= n;
+        done[i] = pass[i] = (a == 0);  // reading G3: a == 0 (mod n) passes
+        A[i] = mmul32(a, R2, M);
+        x[i] = A[i];
+    }
+    for (int b = top - 1; b >= 0; b--) {
+        const bool bit = (d >> b) & 1u;
+#pragma unroll
+        for (int i = 0; i < NB; i++) {
+            const uint32_t sq = mmul32(x[i], x[i], M);
+            const uint32_t y = mmul32(sq, A[i], M);
+            x[i] = bit ? y : sq;
+        }
+    }
+#pragma unroll
+    for (int i = 0; i < NB; i++) {
+        if (!done[i] && (x[i] == M.one || x[i] == M.mone)) done[i] = pass[i] = true;
+    }
+    for (int r = 1; r < s; r++) {
+        bool all = true;
+#pragma unroll
+        for (int i = 0; i < NB; i++) {
+            if (!done[i]) {
+                x[i] = mmul32(x[i], x[i], M);
+                if (x[i] == M.mone) done[i] = pass[i] = true;
+                else if (x[i] == M.one) done[i] = true;
+            }
+            all &= done[i];
+        }
+        if (all) break;
+    }
+    bool ok = true;
+#pragma unroll
+    for (int i = 0; i < NB; i++) ok &= pass[i];
+    return ok;
+}
+
+// ---------------------------------------------------------------- 64-bit ----
+// Phase 1 (base 2).  n odd, n >= 3 (used for n >= 2^32).
+__device__ __forceinline__ bool sprp2_64(uint64_t n) {
+    const Mont64 M = mont64_setup(n);
+    uint64_t d = n - 1;
+    const int s = __ffsll((long long)d) - 1;
+    d >>= s;
+    const int top = 63 - __clzll((long long)d);
+    uint64_t x = mdbl64(M.one, n);  // mont(2)
+    for (int b = top - 1; b >= 0; b--) {
+        x = msqr64(x, M);
+        const uint64_t y = mdbl64(x, n);
+        x = ((d >> b) & 1ull) ? y : x;
+    }
+    if (x == M.one || x == M.mone) return true;
+    for (int r = 1; r < s; r++) {
+        x = msqr64(x, M);
+        if (x == M.mone) return true;
+        if (x == M.one) return false;
+    }
+    return false;
+}
+
+// Select table[digit] (table[0] = one) without dynamic register indexing.
+template <int T>
+__device__ __forceinline__ uint64_t sel_table(const uint64_t (&tab)[T], uint32_t digit, uint64_t one) {
+    uint64_t m = one;
+#pragma unroll
+    for (int k = 1; k <= T; k++) m = (digit == (uint32_t)k) ? tab[k - 1] : m;
+    return m;
+}
+
+// Phase 2: NB bases in lockstep with a fixed WIN-bit window.  Returns true iff
+// n passes every base.  n odd >= 3.  Bases are reduced mod n.
+template <int NB, int WIN>
+__device__ __forceinline__ bool sprp_multi64(uint64_t n, const unsigned long long* bases) {
+    constexpr int T = (1 << WIN) - 1;
+    const Mont64 M = mont64_setup(n);
+    const uint64_t R2 = mont64_r2(M);
+    uint64_t d = n - 1;
+    const int s = __ffsll((long long)d) - 1;
+    d >>= s;
+    const int nbits = 64 - __clzll((long long)d);
+    const int nw = (nbits + WIN - 1) / WIN;
+    uint64_t tab[NB][T], x[NB];
+    bool done[NB], pass[NB];
+#pragma unroll
+    for (int i = 0; i < NB; i++) {
+        uint64_t a = bases[i];
+        if (a >= n) a %= n;
+        done[i] = pass[i] = (a == 0);
+        tab[i][0] = mmul64(a, R2, M);
+#pragma unroll
+        for (int k = 1; k < T; k++) tab[i][k] = mmul64(tab[i][k - 1], tab[i][0], M);
+    }
+    {
+        const uint32_t lead = (uint32_t)(d >> (WIN * (nw - 1)));  // nonzero
+#pragma unroll
+        for (int i = 0; i < NB; i++) x[i] = sel_table<T>(tab[i], lead, M.one);
+    }
+    for (int w = nw - 2; w >= 0; w--) {
+        const uint32_t digit = (uint32_t)(d >> (WIN * w)) & (uint32_t)T;
+#pragma unroll
+        for (int j = 0; j < WIN; j++) {
+#pragma unroll
+            for (int i = 0; i < NB; i++) x[i] = msqr64(x[i], M);
+        }
+#pragma unroll
+        for (int i = 0; i < NB; i++) x[i] = mmul64(x[i], sel_table<T>(tab[i], digit, M.one), M);
+    }
+#pragma unroll
+    for (int i = 0; i < NB; i++) {
+        if (!done[i] && (x[i] == M.one || x[i] == M.mone)) done[i] = pass[i] = true;
+    }
+    for (int r = 1; r < s; r++) {
+        bool all = true;
+#pragma unroll
+        for (int i = 0; i < NB; i++) {
+            if (!done[i]) {
+                x[i] = msqr64(x[i], M);
+                if (x[i] == M.mone) done[i] = pass[i] = true;
+                else if (x[i] == M.one) done[i] = true;
+            }
+            all &= done[i];
+        }
+        if (all) break;
+    }
+    bool ok = true;
+#pragma unroll
+    for (int i = 0; i < NB; i++) ok &= pass[i];
+    return ok;
+}
+
+}  // namespace isp

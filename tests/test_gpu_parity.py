@@ -1,0 +1,320 @@
+"""GPU parity: the CUDA path (through the C-ABI) against the CPU oracle,
+bit-exact (integer output: SURVEY.md 8(c), no tolerance), on the seeded
+workloads of BASELINE.json, the number-theory pin lists and the edge cases of
+the boundary (include/isprime.h)."""
+import os
+
+import numpy as np
+import pytest
+
+import oracle
+import workloads
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+if not torch.cuda.is_available():  # collected on CPU boxes, skipped there
+    pytest.skip("no CUDA device", allow_module_level=True)
+
+import paper_2108_04791_b200 as isp  # noqa: E402
+
+GOLDEN = os.path.join(os.path.dirname(__file__), "golden")
+DEV = torch.device("cuda:0")
+
+
+def _rows(name):
+    with open(os.path.join(GOLDEN, name)) as f:
+        for line in f:
+            line = line.split("#", 1)[0].strip()
+            if line:
+                yield line.split()
+
+
+def gpu(N: np.ndarray) -> np.ndarray:
+    N = np.ascontiguousarray(N, dtype=np.uint64)
+    dN = torch.from_numpy(N.view(np.int64)).to(DEV)
+    dout = torch.full((N.shape[0],), 7, dtype=torch.uint8, device=DEV)  # poison
+    isp.isprime_device(dN, dout, N.shape[0])
+    torch.cuda.synchronize()
+    return dout.cpu().numpy()
+
+
+def assert_same(got, exp, N=None):
+    bad = np.nonzero(got != exp)[0]
+    if bad.size:
+        first = bad[:8].tolist()
+        vals = N[first].tolist() if N is not None else None
+        pytest.fail(f"{bad.size} mismatches; first idx {first} values {vals} got {got[first].tolist()} "
+                    f"expected {exp[first].tolist()}")
+
+
+@pytest.fixture(autouse=True)
+def _default_options():
+    saved = {k: isp.get_option(k) for k in ("force_path", "bases32", "td_primes32", "td_primes64",
+                                             "chunk_log2", "win64", "warp_p")}
+    yield
+    for k, v in saved.items():
+        isp.set_option(k, v)
+
+
+# ------------------------------------------------------------------ pins
+def test_paper_worked_example():
+    """isprime([1,2,3,4,5]) = [0 1 1 0 1]."""
+    assert gpu(np.array([1, 2, 3, 4, 5], dtype=np.uint64)).tolist() == [0, 1, 1, 0, 1]
+
+
+def test_special_values_all_paths():
+    vals = np.array([int(r[0]) for r in _rows("special_values.txt")], dtype=np.uint64)
+    exp = np.array([int(r[1]) for r in _rows("special_values.txt")], dtype=np.uint8)
+    assert np.array_equal(oracle.isprime(vals), exp)
+    for fp in (0, 1, 2):
+        isp.set_option("force_path", fp)
+        assert_same(gpu(vals), exp, vals)
+        # repeated so the values fill whole tiles, warps and queues
+        rep = np.tile(vals, 257)
+        assert_same(gpu(rep), np.tile(exp, 257), rep)
+
+
+def test_chernick_and_pseudoprimes():
+    cs = np.array(workloads.chernick_numbers(), dtype=np.uint64)
+    sp2 = np.array([2047, 3277, 4033, 4681, 8321, 15841, 29341, 42799, 49141, 52633, 65281, 74665,
+                    80581, 85489, 88357, 90751, 3215031751, 2152302898747, 3474749660383,
+                    341550071728321, 3825123056546413051], dtype=np.uint64)
+    N = np.concatenate([cs, sp2])
+    got = gpu(N)
+    assert got.sum() == 0
+    assert_same(got, oracle.isprime(N), N)
+
+
+def test_boundary_primes_and_neighbours():
+    centres = [2**18, 2**20, 2**31, 2**32, 2**33, 2**49, 2**52, 2**53, 2**62, 2**63, 2**64 - 1]
+    vals = []
+    for c in centres:
+        lo = max(0, c - 3000)
+        hi = min(2**64, c + 3000)
+        vals.extend(range(lo, hi))
+    N = np.array(vals, dtype=np.uint64)
+    assert_same(gpu(N), oracle.isprime(N), N)
+
+
+def test_all_below_2_20_every_path():
+    N = np.arange(1 << 20, dtype=np.uint64)
+    exp = oracle.sieve(1 << 20)
+    for fp in (0, 1, 2):
+        isp.set_option("force_path", fp)
+        assert_same(gpu(N), exp, N)
+    assert exp.sum() == 82025
+
+
+# ------------------------------------------------------------------ configs, reduced sizes (bit-exact)
+@pytest.mark.parametrize("cfg,count", [("C1", 100_000), ("C2", (1 << 20) + 777), ("C3", (1 << 18) + 3),
+                                       ("C5", (1 << 20) + 4097)])
+def test_config_prefix_bit_exact(cfg, count):
+    N = workloads.generate(cfg, count=count)
+    assert_same(gpu(N), oracle.isprime(N), N)
+
+
+def test_c4_prefix_bit_exact():
+    n = (1 << 24) + 13
+    N = np.arange(n, dtype=np.uint64)
+    assert_same(gpu(N), oracle.dense_range(0, n), N)
+
+
+def test_c4_shard_window_bit_exact():
+    lo = (1 << 32) - (1 << 22) - 99
+    N = np.arange(lo, 1 << 32, dtype=np.uint64)
+    assert_same(gpu(N), oracle.dense_range(lo, N.shape[0]), N)
+
+
+# ------------------------------------------------------------------ full sizes (count + sampled elements)
+def _counts():
+    return {r[0]: int(r[2]) for r in _rows("config_counts.txt")}
+
+
+@pytest.mark.parametrize("cfg", ["C1", "C2", "C3", "C5"])
+def test_config_full_size(cfg):
+    """Full BASELINE.json size through isprime_count_device (the launch
+    configuration bench.py times): prime count equals the oracle's (stored by
+    tests/golden/make_golden.py) and 65,536 sampled elements equal the oracle."""
+    N = workloads.generate(cfg)
+    dN = torch.from_numpy(N.view(np.int64)).to(DEV)
+    dout = torch.empty(N.shape[0], dtype=torch.uint8, device=DEV)
+    dcount = torch.zeros(1, dtype=torch.int64, device=DEV)
+    isp.isprime_count_device(dN, dout, dcount)
+    torch.cuda.synchronize()
+    assert int(dcount.item()) == _counts()[cfg]
+    got = dout.cpu().numpy()
+    assert int(got.sum()) == _counts()[cfg]
+    rng = np.random.default_rng(5)
+    idx = rng.choice(N.shape[0], size=min(65536, N.shape[0]), replace=False)
+    assert_same(got[idx], oracle.isprime(N[idx]), N[idx])
+    if cfg == "C5":
+        assert np.all(got[4095::4096] == 1)          # 2^64 - 59
+        assert np.all(got[1023::1024][(np.arange(1023, N.shape[0], 1024) & 4095) != 4095] == 0)  # Chernick
+
+
+def test_c4_full_dense_range_pi_2_32():
+    """Config C4: N = 0 .. 2^32-1; count = pi(2^32) = 203,280,221 and sampled
+    elements equal the oracle."""
+    n = 1 << 32
+    dN = torch.arange(n, dtype=torch.int64, device=DEV)
+    dout = torch.empty(n, dtype=torch.uint8, device=DEV)
+    dcount = torch.zeros(1, dtype=torch.int64, device=DEV)
+    isp.isprime_count_device(dN, dout, dcount)
+    torch.cuda.synchronize()
+    assert int(dcount.item()) == 203280221
+    rng = np.random.default_rng(9)
+    idx = np.sort(rng.choice(n, size=65536, replace=False)).astype(np.int64)
+    got = dout[torch.from_numpy(idx).to(DEV)].cpu().numpy()
+    assert_same(got, oracle.isprime(idx.astype(np.uint64)), idx.astype(np.uint64))
+    del dN, dout
+    torch.cuda.empty_cache()
+
+
+def test_force_path_equivalence_all_32bit():
+    """SPEC.md:392 analogue over the ENTIRE 32-bit domain: sieve path vs
+    trial-division + Miller-Rabin path ({2,7,61}) vs Miller-Rabin with the full
+    Eq 4 base set.  Exhaustive GPU self-consistency; with the C4 count above it
+    ties the reduced base set to pi(2^32)."""
+    step = 1 << 28
+    outs = {}
+    dN = torch.empty(step, dtype=torch.int64, device=DEV)
+    o = {k: torch.empty(step, dtype=torch.uint8, device=DEV) for k in ("sieve", "mr3", "mr7")}
+    total = 0
+    for base in range(0, 1 << 32, step):
+        torch.arange(base, base + step, dtype=torch.int64, device=DEV, out=dN)
+        isp.set_option("force_path", 1); isp.set_option("bases32", 3)
+        isp.isprime_device(dN, o["sieve"])
+        isp.set_option("force_path", 2); isp.set_option("bases32", 3)
+        isp.isprime_device(dN, o["mr3"])
+        isp.set_option("bases32", 7)
+        isp.isprime_device(dN, o["mr7"])
+        torch.cuda.synchronize()
+        assert torch.equal(o["sieve"], o["mr3"]), base
+        assert torch.equal(o["sieve"], o["mr7"]), base
+        total += int(o["sieve"].sum(dtype=torch.int64).item())
+    assert total == 203280221
+
+
+# ------------------------------------------------------------------ options never change a bit
+def test_options_do_not_change_results():
+    N = np.concatenate([workloads.generate("C5", count=300_000), workloads.generate("C2", count=100_000),
+                        workloads.generate("C1", count=50_000)])
+    exp = oracle.isprime(N)
+    for key, vals in (("td_primes32", (0, 1, 5, 128)), ("td_primes64", (0, 3, 128)), ("win64", (1, 2, 3)),
+                      ("force_path", (0, 1, 2)), ("chunk_log2", (16, 17, 28)), ("warp_p", (17, 600, 65536))):
+        saved = isp.get_option(key)
+        for v in vals:
+            isp.set_option(key, v)
+            assert_same(gpu(N), exp, N)
+        isp.set_option(key, saved)
+
+
+# ------------------------------------------------------------------ boundary edge cases
+def test_edge_sizes_and_alignment():
+    N = workloads.generate("C5", count=70_001)
+    exp = oracle.isprime(N)
+    for n in (0, 1, 2, 3, 7, 8, 31, 2047, 2048, 2049, 4097, 70_001):
+        if n == 0:
+            isp.isprime_device(0, 0, 0)
+            continue
+        assert_same(gpu(N[:n]), exp[:n], N[:n])
+    # misaligned input (8-B but not 16-B) and odd output offsets
+    dN = torch.from_numpy(N.view(np.int64)).to(DEV)
+    dout = torch.zeros(N.shape[0] + 16, dtype=torch.uint8, device=DEV)
+    for off_in, off_out in ((1, 0), (0, 1), (1, 3), (3, 5)):
+        n = N.shape[0] - off_in
+        isp.isprime_device(dN.data_ptr() + 8 * off_in, dout.data_ptr() + off_out, n)
+        torch.cuda.synchronize()
+        got = dout[off_out:off_out + n].cpu().numpy()
+        assert_same(got, exp[off_in:off_in + n], N[off_in:])
+
+
+def test_errors():
+    lib = isp.load()
+    assert lib.isprime_device(None, None, 4, None) == isp.ISP_EINVAL
+    buf = torch.zeros(64, dtype=torch.uint8, device=DEV)
+    assert lib.isprime_device(buf.data_ptr(), buf.data_ptr() + 8, 4, None) == isp.ISP_EINVAL
+
+
+def test_host_api_pageable_and_pinned():
+    N = np.concatenate([workloads.generate("C5", count=(1 << 24) + 1001), workloads.generate("C1", count=5000)])
+    exp = oracle.isprime(N[::97])
+    got = isp.isprime(N)
+    assert_same(got[::97], exp, N[::97])
+    tN = torch.from_numpy(N.view(np.int64)).pin_memory()
+    tout = torch.empty(N.shape[0], dtype=torch.uint8).pin_memory()
+    isp.isprime_into(tN, tout)
+    assert np.array_equal(tout.numpy(), got)
+    gpu_ref = gpu(N)
+    assert np.array_equal(gpu_ref, got)
+
+
+def test_count_and_popcount():
+    N = workloads.generate("C2", count=1 << 20)
+    dN = torch.from_numpy(N.view(np.int64)).to(DEV)
+    dout = torch.empty(N.shape[0], dtype=torch.uint8, device=DEV)
+    dcount = torch.zeros(1, dtype=torch.int64, device=DEV)
+    isp.isprime_count_device(dN, dout, dcount)
+    torch.cuda.synchronize()
+    assert int(dcount.item()) == int(oracle.isprime(N).sum())
+    dc2 = torch.zeros(1, dtype=torch.int64, device=DEV)
+    isp.isprime_popcount_device(dout[3:], dc2, N.shape[0] - 3)  # unaligned
+    torch.cuda.synchronize()
+    assert int(dc2.item()) == int(dout[3:].sum(dtype=torch.int64).item())
+
+
+def test_stats_reflect_plan():
+    isp.reset_stats()
+    N = np.arange(1 << 22, dtype=np.uint64)
+    gpu(N)
+    st = isp.get_stats()
+    assert st["window_hi"] > st["window_lo"] and st["sieve_runs"] >= 1
+    isp.reset_stats()
+    isp.set_option("force_path", 2)
+    gpu(workloads.generate("C3", count=1 << 16))
+    st = isp.get_stats()
+    assert st["sieve_runs"] == 0 and st["queued64"] > 0 and st["passed64"] > 0
+    assert st["passed64"] <= st["queued64"]
+
+
+# ------------------------------------------------------------------ device modmath and witness step
+def test_mulmod_device_vs_oracle():
+    rng = np.random.default_rng(1)
+    n = 1 << 20
+    m = rng.integers(0, 2**64 - 1, size=n, dtype=np.uint64, endpoint=True) | np.uint64(1)
+    small = rng.integers(3, 2**32 - 1, size=n // 4, dtype=np.uint64) | np.uint64(1)
+    edge = np.array([3, 5, 2**32 - 5, 2**32 + 1, 2**32 - 1, 2**63 - 25, 2**63 + 1, 2**64 - 59, 2**64 - 1],
+                    dtype=np.uint64)
+    m = np.concatenate([m, small, np.repeat(edge, 1000)])
+    a = rng.integers(0, 2**64 - 1, size=m.shape[0], dtype=np.uint64, endpoint=True)
+    b = rng.integers(0, 2**64 - 1, size=m.shape[0], dtype=np.uint64, endpoint=True)
+    a[-9000:] = m[-9000:] - np.uint64(1)
+    t = [torch.from_numpy(x.view(np.int64)).to(DEV) for x in (a, b, m)]
+    out = torch.empty_like(t[0])
+    isp.isprime_mulmod_device(*t, out)
+    torch.cuda.synchronize()
+    got = out.cpu().numpy().view(np.uint64)
+    exp = oracle.mulmod_array(a % m, b % m, m)
+    assert np.array_equal(got, exp)
+
+
+@pytest.mark.parametrize("win", [1, 2, 3])
+def test_sprp_device_vs_oracle(win):
+    """The witness step base by base (32-bit and 64-bit Montgomery paths)."""
+    isp.set_option("win64", win)
+    rng = np.random.default_rng(2 + win)
+    n32 = rng.integers(3, 2**32 - 1, size=40000, dtype=np.uint64) | np.uint64(1)
+    n64 = workloads.loguniform(77 + win, 40000, 33, 64) | np.uint64(1)
+    primes = np.array([2**64 - 59, 2**63 - 25, 2**61 - 1, 4294967291, 2**49 - 81], dtype=np.uint64)
+    psp = np.array([2047, 3215031751, 3825123056546413051] + workloads.chernick_numbers()[:200], dtype=np.uint64)
+    ns = np.concatenate([n32, n64, primes, psp])
+    bases = list(oracle.BASES) + [3, 5, 7, 61, 2**63 + 5, 2**64 - 1]
+    for a in bases:
+        av = np.full(ns.shape[0], a, dtype=np.uint64)
+        dn = torch.from_numpy(ns.view(np.int64)).to(DEV)
+        da = torch.from_numpy(av.view(np.int64)).to(DEV)
+        out = torch.empty(ns.shape[0], dtype=torch.uint8, device=DEV)
+        isp.isprime_sprp_device(dn, da, out)
+        torch.cuda.synchronize()
+        assert_same(out.cpu().numpy(), oracle.sprp_array(ns, av), ns)
