@@ -30,9 +30,9 @@ struct Options {
     int chunk_log2 = 28;
     int win64 = 2;
     int warp_p = 2048;
-    long long sieve_fs_per_int = 300;     // femtoseconds per integer of window
-    long long sieve_fixed_ns = 4000;
-    long long mr32_fs_per_bit = 80;       // femtoseconds per odd element per bit
+    long long sieve_fs_per_int = 400;     // femtoseconds per integer of window
+    long long sieve_fixed_ns = 8000;
+    long long mr32_fs_per_bit = 1000;     // femtoseconds per odd element per bit (trial division + MR)
     unsigned long long sieve_max = 1ull << 32;
     int kernel_timing = 0;
     int sieve_cache = 0;     // 1: a call may reuse the bitmap sieved by an earlier call
@@ -200,7 +200,7 @@ int init_ctx(Ctx* c) {
     CK(cudaMemset(c->plan, 0, sizeof(DevPlan)));
     CK(cudaFuncSetAttribute(sieve_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SEG_ODD));
     c->grid_sieve = c->sms * occupancy((const void*)sieve_kernel, SIEVE_THREADS, SEG_ODD);
-    c->grid_cls = c->sms * occupancy((const void*)classify_kernel<true>, CLS_THREADS, 0);
+    c->grid_cls = c->sms * occupancy((const void*)classify_kernel<24, 24>, CLS_THREADS, 0);
     c->grid_mr1 = c->sms * occupancy((const void*)mr1_kernel, MR_THREADS, 0);
     c->grid_mr2 = c->sms * occupancy((const void*)mr2_kernel<2, false>, MR_THREADS, 0);
     CK(cudaEventCreateWithFlags(&c->last_done, cudaEventDisableTiming));
@@ -258,21 +258,54 @@ int ensure_queues(Ctx* c, size_t cap) {
     return ISP_OK;
 }
 
+// Persistent MR grids never need more blocks than the chunk could queue.
+int mr_grid(int full, uint32_t len) {
+    const uint32_t need = (len + MR_THREADS - 1) / MR_THREADS;
+    return (int)(need < (uint32_t)full ? need : (uint32_t)full);
+}
+
 bool overlaps(const void* a, size_t an, const void* b, size_t bn) {
     const uintptr_t a0 = (uintptr_t)a, b0 = (uintptr_t)b;
     return a0 < b0 + bn && b0 < a0 + an;
 }
 
-int launch_mr2(Ctx* c, cudaStream_t s, uint8_t* out) {
+// Trial-division prime counts available as compile-time constants (the
+// constant-bank operands then sit in the IMAD instructions themselves).
+int td_round(int v) { return v >= 32 ? 32 : v >= 24 ? 24 : v >= 16 ? 16 : v >= 8 ? 8 : 0; }
+
+template <int A>
+void launch_classify_b(int n64, int g, cudaStream_t s, const unsigned long long* N, uint8_t* out, uint32_t len,
+                       Ctx* c, const TDParams& td, int vin, int vout) {
+    switch (n64) {
+        case 32: classify_kernel<A, 32><<<g, CLS_THREADS, 0, s>>>(N, out, len, c->plan, c->bitmap, c->q, td, vin, vout); break;
+        case 24: classify_kernel<A, 24><<<g, CLS_THREADS, 0, s>>>(N, out, len, c->plan, c->bitmap, c->q, td, vin, vout); break;
+        case 16: classify_kernel<A, 16><<<g, CLS_THREADS, 0, s>>>(N, out, len, c->plan, c->bitmap, c->q, td, vin, vout); break;
+        case 8: classify_kernel<A, 8><<<g, CLS_THREADS, 0, s>>>(N, out, len, c->plan, c->bitmap, c->q, td, vin, vout); break;
+        default: classify_kernel<A, 0><<<g, CLS_THREADS, 0, s>>>(N, out, len, c->plan, c->bitmap, c->q, td, vin, vout); break;
+    }
+}
+
+void launch_classify(int n32, int n64, int g, cudaStream_t s, const unsigned long long* N, uint8_t* out,
+                     uint32_t len, Ctx* c, const TDParams& td, int vin, int vout) {
+    switch (n32) {
+        case 32: launch_classify_b<32>(n64, g, s, N, out, len, c, td, vin, vout); break;
+        case 24: launch_classify_b<24>(n64, g, s, N, out, len, c, td, vin, vout); break;
+        case 16: launch_classify_b<16>(n64, g, s, N, out, len, c, td, vin, vout); break;
+        case 8: launch_classify_b<8>(n64, g, s, N, out, len, c, td, vin, vout); break;
+        default: launch_classify_b<0>(n64, g, s, N, out, len, c, td, vin, vout); break;
+    }
+}
+
+int launch_mr2(Ctx* c, cudaStream_t s, uint8_t* out, int grid) {
     const bool full = g_opt.bases32 == 7;
     const int cw = g_opt.kernel_timing;
     switch (g_opt.win64 * 2 + (full ? 1 : 0)) {
-        case 2: mr2_kernel<1, false><<<c->grid_mr2, MR_THREADS, 0, s>>>(c->plan, c->q, out, cw); break;
-        case 3: mr2_kernel<1, true><<<c->grid_mr2, MR_THREADS, 0, s>>>(c->plan, c->q, out, cw); break;
-        case 4: mr2_kernel<2, false><<<c->grid_mr2, MR_THREADS, 0, s>>>(c->plan, c->q, out, cw); break;
-        case 5: mr2_kernel<2, true><<<c->grid_mr2, MR_THREADS, 0, s>>>(c->plan, c->q, out, cw); break;
-        case 6: mr2_kernel<3, false><<<c->grid_mr2, MR_THREADS, 0, s>>>(c->plan, c->q, out, cw); break;
-        default: mr2_kernel<3, true><<<c->grid_mr2, MR_THREADS, 0, s>>>(c->plan, c->q, out, cw); break;
+        case 2: mr2_kernel<1, false><<<grid, MR_THREADS, 0, s>>>(c->plan, c->q, out, cw); break;
+        case 3: mr2_kernel<1, true><<<grid, MR_THREADS, 0, s>>>(c->plan, c->q, out, cw); break;
+        case 4: mr2_kernel<2, false><<<grid, MR_THREADS, 0, s>>>(c->plan, c->q, out, cw); break;
+        case 5: mr2_kernel<2, true><<<grid, MR_THREADS, 0, s>>>(c->plan, c->q, out, cw); break;
+        case 6: mr2_kernel<3, false><<<grid, MR_THREADS, 0, s>>>(c->plan, c->q, out, cw); break;
+        default: mr2_kernel<3, true><<<grid, MR_THREADS, 0, s>>>(c->plan, c->q, out, cw); break;
     }
     CKL("mr2_kernel");
     return ISP_OK;
@@ -291,8 +324,8 @@ int device_impl(Ctx* c, const unsigned long long* dN, uint8_t* dout, size_t n, c
     P.sieve_fixed_ps = (float)g_opt.sieve_fixed_ns * 1e3f;
     P.mr32_ps_per_bit = (float)g_opt.mr32_fs_per_bit * 1e-3f;
     TDParams td;
-    td.n32 = g_opt.td32;
-    td.n64 = g_opt.td64;
+    td.n32 = td_round(g_opt.td32);
+    td.n64 = td_round(g_opt.td64);
     {
         const unsigned long long pn = c->hbp[td.n32].x;  // first prime not trial-divided
         const unsigned long long sq = pn * pn;
@@ -316,21 +349,21 @@ int device_impl(Ctx* c, const unsigned long long* dN, uint8_t* dout, size_t n, c
         }
         const uint32_t ntiles = (len + CLS_TILE - 1) / CLS_TILE;
         const int gcls = (int)(ntiles < (uint32_t)c->grid_cls ? ntiles : (uint32_t)c->grid_cls);
-        const bool vec = (((uintptr_t)N & 15) == 0) && (((uintptr_t)out & 1) == 0);
+        const int vin = (((uintptr_t)N & 15) == 0) ? 1 : 0;
+        const int vout = (((uintptr_t)out & 7) == 0) ? 1 : 0;
         {
             KScope ks(K_CLASSIFY, s);
-            if (vec) classify_kernel<true><<<gcls, CLS_THREADS, 0, s>>>(N, out, len, c->plan, c->bitmap, c->q, td);
-            else classify_kernel<false><<<gcls, CLS_THREADS, 0, s>>>(N, out, len, c->plan, c->bitmap, c->q, td);
+            launch_classify(td.n32, td.n64, gcls, s, N, out, len, c, td, vin, vout);
             CKL("classify_kernel");
         }
         {
             KScope ks(K_MR1, s);
-            mr1_kernel<<<c->grid_mr1, MR_THREADS, 0, s>>>(c->plan, c->q, g_opt.kernel_timing);
+            mr1_kernel<<<mr_grid(c->grid_mr1, len), MR_THREADS, 0, s>>>(c->plan, c->q, g_opt.kernel_timing);
             CKL("mr1_kernel");
         }
         {
             KScope ks(K_MR2, s);
-            rc = launch_mr2(c, s, out);
+            rc = launch_mr2(c, s, out, mr_grid(c->grid_mr2, len));
         }
         if (rc != ISP_OK) return rc;
     }

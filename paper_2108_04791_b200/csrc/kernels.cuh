@@ -157,8 +157,10 @@ __global__ void init_presieve_kernel(uint8_t* patt) {
 }
 
 // ------------------------------------------------------------- A0: plan
-// One block of 1024 threads.  Samples up to 32768 elements at evenly spaced
-// positions, builds a histogram of bit lengths of the odd values below 2^32
+// One block of 1024 threads.  Samples up to 16384 elements, one at a
+// pseudo-random offset inside each of S equal strata (a fixed stride would
+// alias with structured inputs: on the dense range every sample was even),
+// builds a histogram of bit lengths of the odd values below 2^32
 // and their min / max, and chooses the window minimising
 //   sieve cost (fixed + span) + MR cost of the small odd values it misses.
 // The plan changes only the time, never the result: any element outside the
@@ -174,12 +176,17 @@ __global__ void __launch_bounds__(1024) plan_kernel(const unsigned long long* __
     __syncthreads();
     const unsigned long long vlo = P.invalidate ? 0ull : plan->valid_lo;
     const unsigned long long vhi = P.invalidate ? 0ull : plan->valid_hi;
-    const unsigned long long S = len < 32768ull ? len : 32768ull;
+    const unsigned long long S = len < 16384ull ? len : 16384ull;
     unsigned long long lmin = ~0ull, lmax = 0;
     unsigned int lin = 0, lcnt = 0;
     if (P.force == 0) {
         for (unsigned long long k = tid; k < S; k += blockDim.x) {
-            const unsigned long long v = N[(k * len) / S];
+            const unsigned long long lo = (k * len) / S, hi = ((k + 1) * len) / S;  // stratum [lo, hi)
+            unsigned int h = (unsigned int)k * 0x9E3779B1u;
+            h ^= h >> 15;
+            h *= 0x2C1B3C6Du;
+            h ^= h >> 12;
+            const unsigned long long v = N[lo + (hi > lo ? h % (unsigned int)(hi - lo) : 0u)];
             if ((v & 1ull) && v < (1ull << 32) && v > 1) {
                 atomicAdd(&hist[64 - __clzll((long long)v)], 1u);
                 lmin = v < lmin ? v : lmin;
@@ -351,61 +358,70 @@ sieve_kernel(const DevPlan* __restrict__ plan, uint32_t* __restrict__ bitmap,
 }
 
 // ------------------------------------------------------------- A2: classify
+// One streaming pass over N, 2048-element tiles per block iteration.
 // Per element v (PAPER.md:11-20 semantics):
-//   v < 2 -> 0;  v even -> (v == 2);  wlo <= v < whi -> bit of the sieve;
-//   v < 2^32: composite if an odd prime p <= p_n32 divides it (v != p), prime
-//             if no such p and v < (next prime)^2, else queue Q32;
-//   v >= 2^32: composite if an odd prime p <= p_n64 divides it, else queue Q64.
-// out[i] is written for every i (survivors get 0; phase 2 sets primes to 1).
-struct Item {
-    uint32_t cls;  // 0 resolved, 1 -> Q32, 2 -> Q64
+//   v < 2 -> 0;  v even -> (v == 2);  wlo <= v < whi -> bit of the sieve
+//   (membership instead of division);
+//   v < 2^32: composite if an odd prime p among the first N32 divides it
+//             (v != p), prime if no such p and v < (next prime)^2, else -> Q32;
+//   v >= 2^32: composite if one of the first N64 odd primes divides it, else -> Q64
+// ("shrinking the input array", generalised to N primes).
+// Mixed-magnitude tiles would make a warp run both the 32- and the 64-bit
+// trial-division loops for every element slot, so the tile is first compacted
+// by class in shared memory (block scan), then every thread runs the uniform
+// loops over dense lists.  Survivors leave through one atomicAdd per class per
+// tile; out[] is written for every element from the shared-memory result tile.
+struct ClsSmem {
+    unsigned long long val[CLS_TILE];  // list32 grows up from 0, list64 down from CLS_TILE-1
+    unsigned short pos[CLS_TILE];      // tile-local index; bit 15 = survivor
+    uint8_t res[CLS_TILE];
+    uint32_t warp_tot[CLS_THREADS / 32];
+    uint32_t base32, base64, tot;
 };
 
-__device__ __forceinline__ uint8_t classify_one(unsigned long long v, unsigned long long wlo, unsigned long long whi,
-                                                const uint32_t* __restrict__ bitmap, const TDParams& td,
-                                                uint32_t& cls) {
-    cls = 0;
-    if (v < 2ull) return 0;
-    if (!(v & 1ull)) return v == 2ull;
-    if (v >= wlo && v < whi) {
-        const unsigned long long b = (v - wlo) >> 1;
-        return (uint8_t)((__ldg(bitmap + (b >> 5)) >> (b & 31)) & 1u);
+// Block-wide exclusive scan of a packed (lo16, hi16) count pair; returns the
+// exclusive prefix, *total gets the block total.  Contains __syncthreads.
+__device__ __forceinline__ uint32_t block_scan_pair(uint32_t packed, ClsSmem& sm, uint32_t* total) {
+    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+    uint32_t incl = packed;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += y;
     }
-    if (v < (1ull << 32)) {
-        const uint32_t v32 = (uint32_t)v;
-        bool comp = false;
-#pragma unroll 8
-        for (int k = 0; k < td.n32; k++)
-            comp |= (v32 * c_td_inv32[k] <= c_td_lim32[k]) && (v32 != c_td_p[k]);
-        if (comp) return 0;
-        if (v32 < td.sq32) return 1;
-        cls = 1;
-        return 0;
+    if (lane == 31) sm.warp_tot[wid] = incl;
+    __syncthreads();
+    if (wid == 0) {
+        const uint32_t t = lane < CLS_THREADS / 32 ? sm.warp_tot[lane] : 0u;
+        uint32_t ti = t;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(0xffffffffu, ti, o);
+            if (lane >= o) ti += y;
+        }
+        if (lane < CLS_THREADS / 32) sm.warp_tot[lane] = ti - t;
+        if (lane == CLS_THREADS / 32 - 1) sm.tot = ti;
     }
-    bool comp = false;
-#pragma unroll 8
-    for (int k = 0; k < td.n64; k++) comp |= (v * c_td_inv64[k] <= c_td_lim64[k]);
-    if (comp) return 0;
-    cls = 2;
-    return 0;
+    __syncthreads();
+    *total = sm.tot;
+    return sm.warp_tot[wid] + incl - packed;
 }
 
-template <bool VEC>
+template <int N32, int N64>
 __global__ void __launch_bounds__(CLS_THREADS)
 classify_kernel(const unsigned long long* __restrict__ N, uint8_t* __restrict__ out, uint32_t len,
-                DevPlan* __restrict__ plan, const uint32_t* __restrict__ bitmap, Queues q, TDParams td) {
-    __shared__ uint32_t warp_tot[CLS_THREADS / 32];
-    __shared__ uint32_t blk_base32, blk_base64;
+                DevPlan* __restrict__ plan, const uint32_t* __restrict__ bitmap, Queues q, TDParams td,
+                int vec_in, int vec_out) {
+    __shared__ ClsSmem sm;
     const unsigned long long wlo = plan->wlo, whi = plan->whi;
-    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+    const int tid = threadIdx.x;
     const uint32_t ntiles = (len + CLS_TILE - 1) / CLS_TILE;
     for (uint32_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
         const uint32_t tbase = tile * CLS_TILE;
-        unsigned long long v[2 * CLS_PAIRS];
-        uint32_t cls[2 * CLS_PAIRS];
-        uint8_t r[2 * CLS_PAIRS];
         const bool full = tbase + CLS_TILE <= len;
-        if (VEC && full) {
+        // ---- phase A: load, trivial cases, window gather, class
+        unsigned long long v[2 * CLS_PAIRS];
+        if (vec_in && full) {
 #pragma unroll
             for (int j = 0; j < CLS_PAIRS; j++) {
                 const ulonglong2 t = __ldcs(reinterpret_cast<const ulonglong2*>(N + tbase + 2 * tid + 2 * CLS_THREADS * j));
@@ -414,73 +430,94 @@ classify_kernel(const unsigned long long* __restrict__ N, uint8_t* __restrict__ 
             }
         } else {
 #pragma unroll
-            for (int j = 0; j < CLS_PAIRS; j++) {
-#pragma unroll
-                for (int h = 0; h < 2; h++) {
-                    const uint32_t i = tbase + 2 * tid + 2 * CLS_THREADS * j + h;
-                    v[2 * j + h] = i < len ? N[i] : 0ull;
-                }
-            }
-        }
-        uint32_t c32 = 0, c64 = 0;
-#pragma unroll
-        for (int e = 0; e < 2 * CLS_PAIRS; e++) {
-            r[e] = classify_one(v[e], wlo, whi, bitmap, td, cls[e]);
-            const uint32_t i = tbase + 2 * tid + 2 * CLS_THREADS * (e >> 1) + (e & 1);
-            if (i >= len) cls[e] = 0;
-            c32 += cls[e] == 1;
-            c64 += cls[e] == 2;
-        }
-        // results
-        if (VEC && full) {
-#pragma unroll
-            for (int j = 0; j < CLS_PAIRS; j++) {
-                const unsigned short w = (unsigned short)(r[2 * j] | (r[2 * j + 1] << 8));
-                __stcs(reinterpret_cast<unsigned short*>(out + tbase + 2 * tid + 2 * CLS_THREADS * j), w);
-            }
-        } else {
-#pragma unroll
             for (int e = 0; e < 2 * CLS_PAIRS; e++) {
                 const uint32_t i = tbase + 2 * tid + 2 * CLS_THREADS * (e >> 1) + (e & 1);
-                if (i < len) out[i] = r[e];
+                v[e] = i < len ? N[i] : 0ull;
             }
         }
-        // block-wide exclusive scan of (c32, c64) packed in 16-bit halves
-        const uint32_t packed = c32 | (c64 << 16);
-        uint32_t incl = packed;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
-            if (lane >= o) incl += y;
-        }
-        if (lane == 31) warp_tot[wid] = incl;
-        __syncthreads();
-        if (wid == 0) {
-            const uint32_t t = lane < CLS_THREADS / 32 ? warp_tot[lane] : 0u;
-            uint32_t ti = t;
-#pragma unroll
-            for (int o = 1; o < 32; o <<= 1) {
-                const uint32_t y = __shfl_up_sync(0xffffffffu, ti, o);
-                if (lane >= o) ti += y;
-            }
-            if (lane < CLS_THREADS / 32) warp_tot[lane] = ti - t;
-            if (lane == CLS_THREADS / 32 - 1) {
-                const uint32_t t32 = ti & 0xFFFFu, t64 = ti >> 16;
-                blk_base32 = t32 ? atomicAdd(&plan->counts[0], t32) : 0u;
-                blk_base64 = t64 ? atomicAdd(&plan->counts[1], t64) : 0u;
-            }
-        }
-        __syncthreads();
-        const uint32_t excl = warp_tot[wid] + incl - packed;
-        uint32_t p32 = blk_base32 + (excl & 0xFFFFu);
-        uint32_t p64 = blk_base64 + (excl >> 16);
+        uint32_t c32 = 0, c64 = 0, clsbits = 0;  // 2 bits per element: 1 -> 32-bit list, 2 -> 64-bit list
+        uint8_t r[2 * CLS_PAIRS];
 #pragma unroll
         for (int e = 0; e < 2 * CLS_PAIRS; e++) {
+            const unsigned long long x = v[e];
             const uint32_t i = tbase + 2 * tid + 2 * CLS_THREADS * (e >> 1) + (e & 1);
-            if (cls[e] == 1) { q.q32_idx[p32] = i; q.q32_val[p32] = (uint32_t)v[e]; p32++; }
-            else if (cls[e] == 2) { q.q64_idx[p64] = i; q.q64_val[p64] = v[e]; p64++; }
+            uint32_t cls = 0;
+            uint8_t rr = 0;
+            if (x < 2ull) rr = 0;
+            else if (!(x & 1ull)) rr = (x == 2ull);
+            else if (x >= wlo && x < whi) {
+                const unsigned long long b = (x - wlo) >> 1;
+                rr = (uint8_t)((__ldg(bitmap + (b >> 5)) >> (b & 31)) & 1u);
+            } else cls = (x < (1ull << 32)) ? 1u : 2u;
+            if (i >= len) cls = 0;
+            r[e] = rr;
+            c32 += cls == 1;
+            c64 += cls == 2;
+            clsbits |= cls << (2 * e);
         }
-        __syncthreads();  // warp_tot / bases reused by the next tile
+#pragma unroll
+        for (int j = 0; j < CLS_PAIRS; j++)
+            *reinterpret_cast<unsigned short*>(sm.res + 2 * tid + 2 * CLS_THREADS * j) =
+                (unsigned short)(r[2 * j] | (r[2 * j + 1] << 8));
+        {
+            uint32_t tot;
+            const uint32_t ex = block_scan_pair(c32 | (c64 << 16), sm, &tot);
+            uint32_t p32 = ex & 0xFFFFu, p64 = ex >> 16;
+            const uint32_t n32 = tot & 0xFFFFu, n64 = tot >> 16;
+#pragma unroll
+            for (int e = 0; e < 2 * CLS_PAIRS; e++) {
+                const uint32_t cls = (clsbits >> (2 * e)) & 3u;
+                const unsigned short lp = (unsigned short)(2 * tid + 2 * CLS_THREADS * (e >> 1) + (e & 1));
+                if (cls == 1) { sm.val[p32] = v[e]; sm.pos[p32] = lp; p32++; }
+                else if (cls == 2) { const uint32_t k = CLS_TILE - 1 - p64; sm.val[k] = v[e]; sm.pos[k] = lp; p64++; }
+            }
+            __syncthreads();
+            // ---- phase B: trial division over the dense lists
+            uint32_t s32 = 0, s64 = 0;
+            for (uint32_t k = tid; k < n32; k += CLS_THREADS) {
+                const uint32_t x = (uint32_t)sm.val[k];
+                bool comp = false;
+#pragma unroll
+                for (int t = 0; t < N32; t++) comp |= (x * c_td_inv32[t] <= c_td_lim32[t]) && (x != c_td_p[t]);
+                if (!comp) {
+                    if (x < td.sq32) sm.res[sm.pos[k]] = 1;
+                    else { sm.pos[k] |= 0x8000u; s32++; }
+                }
+            }
+            for (int k = CLS_TILE - 1 - tid; k >= CLS_TILE - (int)n64; k -= CLS_THREADS) {
+                const unsigned long long x = sm.val[k];
+                bool comp = false;
+#pragma unroll
+                for (int t = 0; t < N64; t++) comp |= (x * c_td_inv64[t] <= c_td_lim64[t]);
+                if (!comp) { sm.pos[k] |= 0x8000u; s64++; }
+            }
+            // ---- phase C: survivors -> global queues (one atomicAdd per class per tile)
+            uint32_t stot;
+            const uint32_t sex = block_scan_pair(s32 | (s64 << 16), sm, &stot);
+            if (tid == 0) {
+                const uint32_t t32 = stot & 0xFFFFu, t64 = stot >> 16;
+                sm.base32 = t32 ? atomicAdd(&plan->counts[0], t32) : 0u;
+                sm.base64 = t64 ? atomicAdd(&plan->counts[1], t64) : 0u;
+            }
+            __syncthreads();
+            uint32_t o32 = sm.base32 + (sex & 0xFFFFu), o64 = sm.base64 + (sex >> 16);
+            for (uint32_t k = tid; k < n32; k += CLS_THREADS) {
+                const unsigned short ps = sm.pos[k];
+                if (ps & 0x8000u) { q.q32_idx[o32] = tbase + (ps & 0x7FFFu); q.q32_val[o32] = (uint32_t)sm.val[k]; o32++; }
+            }
+            for (int k = CLS_TILE - 1 - tid; k >= CLS_TILE - (int)n64; k -= CLS_THREADS) {
+                const unsigned short ps = sm.pos[k];
+                if (ps & 0x8000u) { q.q64_idx[o64] = tbase + (ps & 0x7FFFu); q.q64_val[o64] = sm.val[k]; o64++; }
+            }
+        }
+        // ---- phase D: results tile -> out (8 bytes per thread, coalesced)
+        if (vec_out && full) {
+            __stcs(reinterpret_cast<uint2*>(out + tbase) + tid, *reinterpret_cast<const uint2*>(sm.res + 8 * tid));
+        } else {
+            for (uint32_t k = tid; k < CLS_TILE; k += CLS_THREADS)
+                if (tbase + k < len) out[tbase + k] = sm.res[k];
+        }
+        __syncthreads();  // shared tile reused by the next iteration
     }
 }
 
