@@ -30,9 +30,9 @@ struct Options {
     int chunk_log2 = 28;
     int win64 = 2;
     int warp_p = 2048;
-    long long sieve_fs_per_int = 400;     // femtoseconds per integer of window
+    long long sieve_fs_per_int = 700;     // femtoseconds per integer of window (measured: C4 0.68 ps)
     long long sieve_fixed_ns = 8000;
-    long long mr32_fs_per_bit = 1000;     // femtoseconds per odd element per bit (trial division + MR)
+    long long mr32_fs_per_bit = 900;      // femtoseconds per odd element per bit (trial division + MR, C2)
     unsigned long long sieve_max = 1ull << 32;
     int kernel_timing = 0;
     int sieve_cache = 0;     // 1: a call may reuse the bitmap sieved by an earlier call
@@ -338,7 +338,7 @@ int device_impl(Ctx* c, const unsigned long long* dN, uint8_t* dout, size_t n, c
         P.invalidate = (base == 0 && !g_opt.sieve_cache) ? 1 : 0;
         {
             KScope ks(K_PLAN, s);
-            plan_kernel<<<1, 1024, 0, s>>>(N, len, c->plan, P);
+            plan_kernel<<<1, PLAN_THREADS, 0, s>>>(N, len, c->plan, P);
             CKL("plan_kernel");
         }
         {

@@ -157,81 +157,116 @@ __global__ void init_presieve_kernel(uint8_t* patt) {
 }
 
 // ------------------------------------------------------------- A0: plan
-// One block of 1024 threads.  Samples up to 16384 elements, one at a
+// One block of PLAN_THREADS.  Samples up to PLAN_SAMPLES elements, one at a
 // pseudo-random offset inside each of S equal strata (a fixed stride would
 // alias with structured inputs: on the dense range every sample was even),
-// builds a histogram of bit lengths of the odd values below 2^32
-// and their min / max, and chooses the window minimising
-//   sieve cost (fixed + span) + MR cost of the small odd values it misses.
-// The plan changes only the time, never the result: any element outside the
-// window takes the trial-division / Miller-Rabin route.
-__global__ void __launch_bounds__(1024) plan_kernel(const unsigned long long* __restrict__ N, unsigned long long len,
-                            DevPlan* plan, PlanParams P) {
+// histograms the bit lengths of the odd values below 2^32 and takes their
+// min / max, and picks the window minimising
+//   sieve cost (fixed + span) + MR cost of the small odd values it misses
+// among: none, the bitmap already held, [0, 2^k) for k = 1..32, and
+// [min - margin, max + margin).  Warp 0 evaluates the candidates in parallel.
+// This is the GPU form of the paper's path heuristic (Eq 7
+// and 8 choose between "sieve to sqrt(M)" and "sieve to M + membership" from
+// the element count and the maximum); its constants are B200 costs, not the
+// MATLAB fits.  The plan changes only the time, never the result: any element
+// outside the window takes the trial-division / Miller-Rabin route.
+constexpr int PLAN_THREADS = 256;
+constexpr int PLAN_SAMPLES = 4096;
+
+__global__ void __launch_bounds__(PLAN_THREADS) plan_kernel(const unsigned long long* __restrict__ N,
+                                                            unsigned long long len, DevPlan* plan, PlanParams P) {
     __shared__ unsigned int hist[33];
-    __shared__ unsigned long long smin, smax;
+    __shared__ unsigned long long wmin[PLAN_THREADS / 32], wmaxv[PLAN_THREADS / 32];
     __shared__ unsigned int in_valid, nsamp_small;
-    const int tid = threadIdx.x;
+    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
     if (tid < 33) hist[tid] = 0;
-    if (tid == 0) { smin = ~0ull; smax = 0; in_valid = 0; nsamp_small = 0; }
+    if (tid == 0) { in_valid = 0; nsamp_small = 0; }
     __syncthreads();
     const unsigned long long vlo = P.invalidate ? 0ull : plan->valid_lo;
     const unsigned long long vhi = P.invalidate ? 0ull : plan->valid_hi;
-    const unsigned long long S = len < 16384ull ? len : 16384ull;
+    const unsigned long long S = len < (unsigned long long)PLAN_SAMPLES ? len : (unsigned long long)PLAN_SAMPLES;
     unsigned long long lmin = ~0ull, lmax = 0;
     unsigned int lin = 0, lcnt = 0;
     if (P.force == 0) {
-        for (unsigned long long k = tid; k < S; k += blockDim.x) {
-            const unsigned long long lo = (k * len) / S, hi = ((k + 1) * len) / S;  // stratum [lo, hi)
-            unsigned int h = (unsigned int)k * 0x9E3779B1u;
-            h ^= h >> 15;
-            h *= 0x2C1B3C6Du;
-            h ^= h >> 12;
-            const unsigned long long v = N[lo + (hi > lo ? h % (unsigned int)(hi - lo) : 0u)];
-            if ((v & 1ull) && v < (1ull << 32) && v > 1) {
-                atomicAdd(&hist[64 - __clzll((long long)v)], 1u);
-                lmin = v < lmin ? v : lmin;
-                lmax = v > lmax ? v : lmax;
-                lin += (v >= vlo && v < vhi);
+        constexpr int PER = PLAN_SAMPLES / PLAN_THREADS;
+        unsigned long long v[PER];
+#pragma unroll
+        for (int r = 0; r < PER; r++) {  // independent loads, all in flight together
+            const unsigned long long k = (unsigned long long)tid + (unsigned long long)r * PLAN_THREADS;
+            v[r] = 0;
+            if (k < S) {
+                const unsigned long long lo = (k * len) / S, hi = ((k + 1) * len) / S;  // stratum [lo, hi)
+                unsigned int h = (unsigned int)k * 0x9E3779B1u;
+                h ^= h >> 15;
+                h *= 0x2C1B3C6Du;
+                h ^= h >> 12;
+                v[r] = N[lo + (hi > lo ? h % (unsigned int)(hi - lo) : 0u)];
+            }
+        }
+#pragma unroll
+        for (int r = 0; r < PER; r++) {
+            const unsigned long long x = v[r];
+            if ((x & 1ull) && x < (1ull << 32) && x > 1) {
+                atomicAdd(&hist[64 - __clzll((long long)x)], 1u);
+                lmin = x < lmin ? x : lmin;
+                lmax = x > lmax ? x : lmax;
+                lin += (x >= vlo && x < vhi);
                 lcnt++;
             }
         }
-        atomicMin(&smin, lmin);
-        atomicMax(&smax, lmax);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        const unsigned long long a = __shfl_xor_sync(0xffffffffu, lmin, o);
+        const unsigned long long b = __shfl_xor_sync(0xffffffffu, lmax, o);
+        lmin = a < lmin ? a : lmin;
+        lmax = b > lmax ? b : lmax;
+        lin += __shfl_xor_sync(0xffffffffu, lin, o);
+        lcnt += __shfl_xor_sync(0xffffffffu, lcnt, o);
+    }
+    if (lane == 0) {
+        wmin[wid] = lmin;
+        wmaxv[wid] = lmax;
         atomicAdd(&in_valid, lin);
         atomicAdd(&nsamp_small, lcnt);
     }
     __syncthreads();
-    if (tid != 0) return;
-    unsigned long long wlo = 0, whi = 0;
+    if (wid != 0) return;
+    unsigned long long mn = ~0ull, mx = 0;
+#pragma unroll
+    for (int w = 0; w < PLAN_THREADS / 32; w++) {
+        mn = wmin[w] < mn ? wmin[w] : mn;
+        mx = wmaxv[w] > mx ? wmaxv[w] : mx;
+    }
     const unsigned long long wmax = P.wmax;
+    unsigned long long wlo = 0, whi = 0;
     if (P.force == 1) {
         wlo = 0; whi = wmax;
     } else if (P.force == 0 && nsamp_small > 0 && S > 0) {
         const double scale = (double)len / (double)S;  // elements per sample
-        double mr_all = 0.0;
-        double mr_b[33];
-        for (int b = 0; b <= 32; b++) {
-            mr_b[b] = (double)hist[b] * scale * (double)P.mr32_ps_per_bit * b;
-            mr_all += mr_b[b];
+        // lane b (1..32) owns bit length b; inclusive scan gives the MR cost covered by [0, 2^b)
+        const int b = lane + 1;
+        double mrb = (double)hist[b] * scale * (double)P.mr32_ps_per_bit * b;
+        double covered = mrb;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const double y = __shfl_up_sync(0xffffffffu, covered, o);
+            if (lane >= o) covered += y;
         }
-        double best = mr_all;  // no window
-        // candidate: the range the bitmap already holds (no sieve cost)
-        if (vhi > vlo) {
-            const double miss = mr_all * (1.0 - (double)in_valid / (double)nsamp_small);
-            if (miss < best) { best = miss; wlo = vlo; whi = vhi; }
-        }
-        // candidates [0, 2^k)
-        double covered = 0.0;
-        for (int k = 1; k <= 32; k++) {
-            covered += mr_b[k];
-            const unsigned long long span = 1ull << k;
-            if (span > wmax) break;
-            const double c = P.sieve_fixed_ps + (double)span * P.sieve_ps_per_int + (mr_all - covered);
-            if (c < best) { best = c; wlo = 0; whi = span; }
-        }
-        // candidate [min - margin, max + margin) of the sampled small values
-        {
-            const unsigned long long mn = smin, mx = smax;
+        const double mr_all = __shfl_sync(0xffffffffu, covered, 31);
+        // candidate of this lane: [0, 2^b)
+        double cost = 1e300;
+        unsigned long long clo = 0, chi = 1ull << b;
+        if (chi <= wmax) cost = P.sieve_fixed_ps + (double)chi * P.sieve_ps_per_int + (mr_all - covered);
+        int cand = 2 + lane;  // 0 none, 1 held bitmap, 2.. [0,2^b), 40 [min,max]
+        // lane 0 also weighs "none" and the held bitmap; lane 1 the [min, max] window
+        if (lane == 0) {
+            if (mr_all <= cost) { cost = mr_all; cand = 0; clo = 0; chi = 0; }
+            if (vhi > vlo) {
+                const double miss = mr_all * (1.0 - (double)in_valid / (double)nsamp_small);
+                if (miss < cost) { cost = miss; cand = 1; clo = vlo; chi = vhi; }
+            }
+        } else if (lane == 1) {
             const unsigned long long margin = (unsigned long long)(((double)(mx - mn) / (double)nsamp_small) * 4.0) + 64;
             unsigned long long lo = mn > margin ? mn - margin : 0;
             unsigned long long hi = mx + margin + 1;
@@ -240,11 +275,23 @@ __global__ void __launch_bounds__(1024) plan_kernel(const unsigned long long* __
             hi = (hi + 63) & ~63ull;
             if (hi - lo <= wmax) {
                 const double c = P.sieve_fixed_ps + (double)(hi - lo) * P.sieve_ps_per_int;
-                if (c < best) { best = c; wlo = lo; whi = hi; }
+                if (c < cost) { cost = c; cand = 40; clo = lo; chi = hi; }
             }
         }
+        // warp argmin (ties -> lowest candidate id)
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            const double oc = __shfl_xor_sync(0xffffffffu, cost, o);
+            const int ocand = __shfl_xor_sync(0xffffffffu, cand, o);
+            const unsigned long long olo = __shfl_xor_sync(0xffffffffu, clo, o);
+            const unsigned long long ohi = __shfl_xor_sync(0xffffffffu, chi, o);
+            if (oc < cost || (oc == cost && ocand < cand)) { cost = oc; cand = ocand; clo = olo; chi = ohi; }
+        }
+        wlo = clo;
+        whi = chi;
     }
-    if (whi > wmax) whi = wmax;  // (force mode only)
+    if (lane != 0) return;
+    if (whi > wmax) whi = wmax;
     unsigned int need = 0;
     if (whi > wlo && !(wlo >= vlo && whi <= vhi)) {
         need = 1;
@@ -416,25 +463,35 @@ classify_kernel(const unsigned long long* __restrict__ N, uint8_t* __restrict__ 
     const unsigned long long wlo = plan->wlo, whi = plan->whi;
     const int tid = threadIdx.x;
     const uint32_t ntiles = (len + CLS_TILE - 1) / CLS_TILE;
-    for (uint32_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-        const uint32_t tbase = tile * CLS_TILE;
-        const bool full = tbase + CLS_TILE <= len;
-        // ---- phase A: load, trivial cases, window gather, class
-        unsigned long long v[2 * CLS_PAIRS];
-        if (vec_in && full) {
+    // software pipeline: the next tile's values are loaded while this one is classified
+    unsigned long long vn[2 * CLS_PAIRS];
+    auto load_tile = [&](uint32_t tile) {
+        const uint32_t tb = tile * CLS_TILE;
+        if (tile >= ntiles) return;
+        if (vec_in && tb + CLS_TILE <= len) {
 #pragma unroll
             for (int j = 0; j < CLS_PAIRS; j++) {
-                const ulonglong2 t = __ldcs(reinterpret_cast<const ulonglong2*>(N + tbase + 2 * tid + 2 * CLS_THREADS * j));
-                v[2 * j] = t.x;
-                v[2 * j + 1] = t.y;
+                const ulonglong2 t = __ldcs(reinterpret_cast<const ulonglong2*>(N + tb + 2 * tid + 2 * CLS_THREADS * j));
+                vn[2 * j] = t.x;
+                vn[2 * j + 1] = t.y;
             }
         } else {
 #pragma unroll
             for (int e = 0; e < 2 * CLS_PAIRS; e++) {
-                const uint32_t i = tbase + 2 * tid + 2 * CLS_THREADS * (e >> 1) + (e & 1);
-                v[e] = i < len ? N[i] : 0ull;
+                const uint32_t i = tb + 2 * tid + 2 * CLS_THREADS * (e >> 1) + (e & 1);
+                vn[e] = i < len ? N[i] : 0ull;
             }
         }
+    };
+    load_tile(blockIdx.x);
+    for (uint32_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+        const uint32_t tbase = tile * CLS_TILE;
+        const bool full = tbase + CLS_TILE <= len;
+        // ---- phase A: trivial cases, window gather, class
+        unsigned long long v[2 * CLS_PAIRS];
+#pragma unroll
+        for (int e = 0; e < 2 * CLS_PAIRS; e++) v[e] = vn[e];
+        load_tile(tile + gridDim.x);
         uint32_t c32 = 0, c64 = 0, clsbits = 0;  // 2 bits per element: 1 -> 32-bit list, 2 -> 64-bit list
         uint8_t r[2 * CLS_PAIRS];
 #pragma unroll
@@ -454,6 +511,23 @@ classify_kernel(const unsigned long long* __restrict__ N, uint8_t* __restrict__ 
             c32 += cls == 1;
             c64 += cls == 2;
             clsbits |= cls << (2 * e);
+        }
+        if (!__syncthreads_or((int)(c32 | c64))) {
+            // fast path: nothing in this tile needs trial division (e.g. the whole
+            // tile is inside the sieve window) -- results straight from registers
+            if (full && vec_out) {
+#pragma unroll
+                for (int j = 0; j < CLS_PAIRS; j++)
+                    __stcs(reinterpret_cast<unsigned short*>(out + tbase + 2 * tid + 2 * CLS_THREADS * j),
+                           (unsigned short)(r[2 * j] | (r[2 * j + 1] << 8)));
+            } else {
+#pragma unroll
+                for (int e = 0; e < 2 * CLS_PAIRS; e++) {
+                    const uint32_t i = tbase + 2 * tid + 2 * CLS_THREADS * (e >> 1) + (e & 1);
+                    if (i < len) out[i] = r[e];
+                }
+            }
+            continue;
         }
 #pragma unroll
         for (int j = 0; j < CLS_PAIRS; j++)

@@ -4,9 +4,5 @@ cd "$(dirname "$0")/.."
 mkdir -p gpurun_out
 python -c "import __graft_entry__ as g; g.build()" > gpurun_out/build.log 2>&1
 {
-python tools/explore.py C1 force_path=0,1,2
-python tools/explore.py C2 force_path=0,2 td_primes32=0,8,16,24,32
-python tools/explore.py C3 win64=1,2,3 td_primes64=8,16,24,32
-python tools/explore.py C4 force_path=0,1
-python tools/explore.py C5 td_primes64=8,24
+for c in ${EXPLORE_CONFIGS:-C1 C2 C3 C4 C5}; do python tools/explore.py $c ${EXPLORE_ARGS:-}; done
 } > gpurun_out/explore.jsonl 2> gpurun_out/explore.err
