@@ -116,7 +116,7 @@ int isprime_reset_stats(void);
 
 /* Per-kernel device time accumulated while option "kernel_timing" is 1
  * (synchronises the device).  Fills up to `max` entries; *count = entries
- * available.  Names: plan, sieve, classify, mr1, mr2, popcount. */
+ * available.  Names: plan, sieve, classify, sort, mr1, mr2, popcount. */
 typedef struct {
     char name[16];
     uint64_t launches;

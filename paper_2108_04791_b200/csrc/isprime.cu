@@ -56,7 +56,7 @@ struct Ctx {
     unsigned char* qmem = nullptr;
     size_t qcap = 0;
     Queues q{};
-    int grid_cls = 0, grid_mr1 = 0, grid_mr2 = 0, grid_sieve = 0;
+    int grid_cls = 0, grid_mr1 = 0, grid_mr2 = 0, grid_sieve = 0, grid_sort = 0;
     cudaEvent_t last_done = nullptr;
     void* last_stream = nullptr;
     bool has_last = false;
@@ -74,8 +74,8 @@ struct Ctx {
 std::vector<Ctx*> g_ctx;
 
 // ---- optional per-kernel timing (events on the launching stream)
-enum { K_PLAN, K_SIEVE, K_CLASSIFY, K_MR1, K_MR2, K_POPCOUNT, K_NUM };
-const char* const k_names[K_NUM] = {"plan", "sieve", "classify", "mr1", "mr2", "popcount"};
+enum { K_PLAN, K_SIEVE, K_CLASSIFY, K_SORT, K_MR1, K_MR2, K_POPCOUNT, K_NUM };
+const char* const k_names[K_NUM] = {"plan", "sieve", "classify", "sort", "mr1", "mr2", "popcount"};
 struct KTPending { cudaEvent_t a, b; int kid; };
 std::vector<KTPending> g_kt_pending;
 std::vector<cudaEvent_t> g_ev_pool;
@@ -202,6 +202,7 @@ int init_ctx(Ctx* c) {
     c->grid_sieve = c->sms * occupancy((const void*)sieve_kernel, SIEVE_THREADS, SEG_ODD);
     c->grid_cls = c->sms * occupancy((const void*)classify_kernel<24, 24>, CLS_THREADS, 0);
     c->grid_mr1 = c->sms * occupancy((const void*)mr1_kernel, MR_THREADS, 0);
+    c->grid_sort = c->sms * occupancy((const void*)qscatter_kernel, SORT_THREADS, 0);
     c->grid_mr2 = c->sms * occupancy((const void*)mr2_kernel<2, false>, MR_THREADS, 0);
     CK(cudaEventCreateWithFlags(&c->last_done, cudaEventDisableTiming));
     for (int k = 0; k < 2; k++) {
@@ -238,8 +239,8 @@ int ensure_queues(Ctx* c, size_t cap) {
     if (cap <= c->qcap) return ISP_OK;
     if (c->qmem) { CK(cudaFree(c->qmem)); c->qmem = nullptr; c->qcap = 0; }
     cap = (cap + 4095) & ~(size_t)4095;
-    // per entry: q32 4+4, q64 4+8, p32 4+4, p64 4+8 = 40 bytes
-    const size_t bytes = cap * 40;
+    // per entry: q32 4+4, q64 4+8, s32 4+4, s64 4+8, p32 4+4, p64 4+8 = 60 bytes
+    const size_t bytes = cap * 60;
     if (cudaMalloc(&c->qmem, bytes) != cudaSuccess) {
         cudaGetLastError();
         g_err = "queue allocation of " + std::to_string(bytes) + " bytes failed";
@@ -248,6 +249,10 @@ int ensure_queues(Ctx* c, size_t cap) {
     unsigned char* p = c->qmem;
     c->q.q64_val = reinterpret_cast<unsigned long long*>(p); p += cap * 8;
     c->q.p64_val = reinterpret_cast<unsigned long long*>(p); p += cap * 8;
+    c->q.s64_val = reinterpret_cast<unsigned long long*>(p); p += cap * 8;
+    c->q.s32_idx = reinterpret_cast<uint32_t*>(p); p += cap * 4;
+    c->q.s32_val = reinterpret_cast<uint32_t*>(p); p += cap * 4;
+    c->q.s64_idx = reinterpret_cast<uint32_t*>(p); p += cap * 4;
     c->q.q32_idx = reinterpret_cast<uint32_t*>(p); p += cap * 4;
     c->q.q32_val = reinterpret_cast<uint32_t*>(p); p += cap * 4;
     c->q.q64_idx = reinterpret_cast<uint32_t*>(p); p += cap * 4;
@@ -256,6 +261,12 @@ int ensure_queues(Ctx* c, size_t cap) {
     c->q.p64_idx = reinterpret_cast<uint32_t*>(p); p += cap * 4;
     c->qcap = cap;
     return ISP_OK;
+}
+
+// Sort grids: one 2048-entry tile per block at most, capped at the resident grid.
+int sort_grid(int full, uint32_t len) {
+    const uint32_t need = (len + 2047) / 2048;
+    return (int)(need < (uint32_t)full ? (need ? need : 1) : (uint32_t)full);
 }
 
 // Persistent MR grids never need more blocks than the chunk could queue.
@@ -355,6 +366,14 @@ int device_impl(Ctx* c, const unsigned long long* dN, uint8_t* dout, size_t n, c
             KScope ks(K_CLASSIFY, s);
             launch_classify(td.n32, td.n64, gcls, s, N, out, len, c, td, vin, vout);
             CKL("classify_kernel");
+        }
+        {
+            KScope ks(K_SORT, s);
+            const int gs = sort_grid(c->grid_sort, len);
+            qhist_kernel<<<gs, SORT_THREADS, 0, s>>>(c->plan, c->q);
+            CKL("qhist_kernel");
+            qscatter_kernel<<<gs, SORT_THREADS, 0, s>>>(c->plan, c->q);
+            CKL("qscatter_kernel");
         }
         {
             KScope ks(K_MR1, s);

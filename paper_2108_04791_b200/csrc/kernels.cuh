@@ -44,6 +44,9 @@ struct DevPlan {
     // method), accumulated only when work counting is on:
     // [mr1 32-bit, mr1 64-bit, mr2 32-bit, mr2 64-bit]
     unsigned long long work[4];
+    // counting sort of the trial-division survivors by bit length (per chunk)
+    unsigned int bins32[33], bins64[65], cur32[33], cur64[65];
+    unsigned int sorted32, sorted64;
 };
 
 // Host -> plan kernel parameters (cost model in picoseconds on a full GPU).
@@ -57,9 +60,11 @@ struct PlanParams {
 };
 
 struct Queues {
-    uint32_t* q32_idx; uint32_t* q32_val;
+    uint32_t* q32_idx; uint32_t* q32_val;             // classify -> (sort) -> mr1
     uint32_t* q64_idx; unsigned long long* q64_val;
-    uint32_t* p32_idx; uint32_t* p32_val;
+    uint32_t* s32_idx; uint32_t* s32_val;             // the same entries ordered by bit length
+    uint32_t* s64_idx; unsigned long long* s64_val;
+    uint32_t* p32_idx; uint32_t* p32_val;             // base-2 strong probable primes -> mr2
     uint32_t* p64_idx; unsigned long long* p64_val;
 };
 
@@ -206,8 +211,12 @@ __global__ void __launch_bounds__(PLAN_THREADS) plan_kernel(const unsigned long 
 #pragma unroll
         for (int r = 0; r < PER; r++) {
             const unsigned long long x = v[r];
-            if ((x & 1ull) && x < (1ull << 32) && x > 1) {
-                atomicAdd(&hist[64 - __clzll((long long)x)], 1u);
+            const bool small = (x & 1ull) && x < (1ull << 32) && x > 1;
+            const unsigned int bin = small ? (unsigned int)(64 - __clzll((long long)x)) : 0u;
+            // same-bin lanes add once (a dense range puts every sample in one bin)
+            const unsigned int peers = __match_any_sync(0xffffffffu, bin);
+            if (bin && lane == __ffs(peers) - 1) atomicAdd(&hist[bin], (unsigned int)__popc(peers));
+            if (small) {
                 lmin = x < lmin ? x : lmin;
                 lmax = x > lmax ? x : lmax;
                 lin += (x >= vlo && x < vhi);
@@ -304,6 +313,9 @@ __global__ void __launch_bounds__(PLAN_THREADS) plan_kernel(const unsigned long 
     plan->whi = whi;
     plan->sieve_needed = need;
     for (int q = 0; q < 4; q++) { plan->total[q] += plan->counts[q]; plan->counts[q] = 0; }
+    for (int b = 0; b < 33; b++) { plan->bins32[b] = 0; plan->cur32[b] = 0; }
+    for (int b = 0; b < 65; b++) { plan->bins64[b] = 0; plan->cur64[b] = 0; }
+    plan->sorted32 = plan->sorted64 = 0;
     plan->chunks += 1;
 }
 
@@ -463,35 +475,25 @@ classify_kernel(const unsigned long long* __restrict__ N, uint8_t* __restrict__ 
     const unsigned long long wlo = plan->wlo, whi = plan->whi;
     const int tid = threadIdx.x;
     const uint32_t ntiles = (len + CLS_TILE - 1) / CLS_TILE;
-    // software pipeline: the next tile's values are loaded while this one is classified
-    unsigned long long vn[2 * CLS_PAIRS];
-    auto load_tile = [&](uint32_t tile) {
-        const uint32_t tb = tile * CLS_TILE;
-        if (tile >= ntiles) return;
-        if (vec_in && tb + CLS_TILE <= len) {
+    for (uint32_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+        const uint32_t tbase = tile * CLS_TILE;
+        const bool full = tbase + CLS_TILE <= len;
+        // ---- phase A: load, trivial cases, window gather, class
+        unsigned long long v[2 * CLS_PAIRS];
+        if (vec_in && full) {
 #pragma unroll
             for (int j = 0; j < CLS_PAIRS; j++) {
-                const ulonglong2 t = __ldcs(reinterpret_cast<const ulonglong2*>(N + tb + 2 * tid + 2 * CLS_THREADS * j));
-                vn[2 * j] = t.x;
-                vn[2 * j + 1] = t.y;
+                const ulonglong2 t = __ldcs(reinterpret_cast<const ulonglong2*>(N + tbase + 2 * tid + 2 * CLS_THREADS * j));
+                v[2 * j] = t.x;
+                v[2 * j + 1] = t.y;
             }
         } else {
 #pragma unroll
             for (int e = 0; e < 2 * CLS_PAIRS; e++) {
-                const uint32_t i = tb + 2 * tid + 2 * CLS_THREADS * (e >> 1) + (e & 1);
-                vn[e] = i < len ? N[i] : 0ull;
+                const uint32_t i = tbase + 2 * tid + 2 * CLS_THREADS * (e >> 1) + (e & 1);
+                v[e] = i < len ? N[i] : 0ull;
             }
         }
-    };
-    load_tile(blockIdx.x);
-    for (uint32_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-        const uint32_t tbase = tile * CLS_TILE;
-        const bool full = tbase + CLS_TILE <= len;
-        // ---- phase A: trivial cases, window gather, class
-        unsigned long long v[2 * CLS_PAIRS];
-#pragma unroll
-        for (int e = 0; e < 2 * CLS_PAIRS; e++) v[e] = vn[e];
-        load_tile(tile + gridDim.x);
         uint32_t c32 = 0, c64 = 0, clsbits = 0;  // 2 bits per element: 1 -> 32-bit list, 2 -> 64-bit list
         uint8_t r[2 * CLS_PAIRS];
 #pragma unroll
@@ -595,6 +597,125 @@ classify_kernel(const unsigned long long* __restrict__ N, uint8_t* __restrict__ 
     }
 }
 
+// ------------------------------------------------------------- A2b: order by magnitude
+// Counting sort of the survivor queues by bit length (33 keys for Q32, 65 for
+// Q64).  A warp runs the exponent loop as long as its longest element, so on
+// mixed magnitudes (config C5: bit lengths 33..64 in every warp) unsorted
+// queues waste about a quarter of the multiply pipe; sorted, neighbouring
+// lanes carry equal-length exponents.  Skipped (flag stays 0, mr1 reads the
+// unsorted queue) when the survivors span fewer than 3 bit lengths.
+constexpr int SORT_THREADS = 256;
+constexpr int SORT_TILE = 2048;
+
+__device__ __forceinline__ unsigned int bitlen32(uint32_t v) { return 32u - __clz(v); }
+__device__ __forceinline__ unsigned int bitlen64u(unsigned long long v) { return 64u - __clzll((long long)v); }
+
+__global__ void __launch_bounds__(SORT_THREADS) qhist_kernel(DevPlan* __restrict__ plan, Queues q) {
+    __shared__ unsigned int h32[33], h64[65];
+    const int tid = threadIdx.x;
+    for (int b = tid; b < 65; b += SORT_THREADS) { h64[b] = 0; if (b < 33) h32[b] = 0; }
+    __syncthreads();
+    const unsigned int c32 = plan->counts[0], c64 = plan->counts[1];
+    const unsigned int stride = gridDim.x * SORT_THREADS;
+    for (unsigned int b0 = blockIdx.x * SORT_THREADS; b0 < c32; b0 += stride) {
+        const unsigned int i = b0 + tid;
+        const unsigned int bin = i < c32 ? bitlen32(q.q32_val[i]) : 0u;
+        const unsigned int peers = __match_any_sync(0xffffffffu, bin);
+        if (i < c32 && (tid & 31) == __ffs(peers) - 1) atomicAdd(&h32[bin], (unsigned int)__popc(peers));
+    }
+    for (unsigned int b0 = blockIdx.x * SORT_THREADS; b0 < c64; b0 += stride) {
+        const unsigned int i = b0 + tid;
+        const unsigned int bin = i < c64 ? bitlen64u(q.q64_val[i]) : 0u;
+        const unsigned int peers = __match_any_sync(0xffffffffu, bin);
+        if (i < c64 && (tid & 31) == __ffs(peers) - 1) atomicAdd(&h64[bin], (unsigned int)__popc(peers));
+    }
+    __syncthreads();
+    for (int b = tid; b < 65; b += SORT_THREADS) {
+        if (h64[b]) atomicAdd(&plan->bins64[b], h64[b]);
+        if (b < 33 && h32[b]) atomicAdd(&plan->bins32[b], h32[b]);
+    }
+}
+
+template <typename T, int NB>
+__device__ __forceinline__ void scatter_sorted(const unsigned int* __restrict__ gbins, unsigned int* gcur, unsigned int count,
+                                               const uint32_t* __restrict__ src_idx, const T* __restrict__ src_val,
+                                               uint32_t* __restrict__ dst_idx, T* __restrict__ dst_val,
+                                               unsigned int* spre, unsigned int* scnt, unsigned int* sbase) {
+    const int tid = threadIdx.x;
+    // exclusive prefix of the global bins (every block computes it)
+    if (tid == 0) {
+        unsigned int acc = 0;
+        for (int b = 0; b < NB; b++) { spre[b] = acc; acc += gbins[b]; }
+    }
+    for (int b = tid; b < NB; b += SORT_THREADS) scnt[b] = 0;
+    __syncthreads();
+    constexpr int PER = SORT_TILE / SORT_THREADS;
+    for (unsigned int t0 = blockIdx.x * SORT_TILE; t0 < count; t0 += gridDim.x * SORT_TILE) {
+        uint32_t idx[PER];
+        T val[PER];
+        unsigned int bin[PER], rank[PER];
+#pragma unroll
+        for (int k = 0; k < PER; k++) {
+            const unsigned int i = t0 + tid + k * SORT_THREADS;
+            bin[k] = NB;  // sentinel: no element
+            if (i < count) {
+                idx[k] = src_idx[i];
+                val[k] = src_val[i];
+                bin[k] = (sizeof(T) == 8) ? bitlen64u((unsigned long long)val[k]) : bitlen32((uint32_t)val[k]);
+            }
+        }
+#pragma unroll
+        for (int k = 0; k < PER; k++) {
+            const unsigned int peers = __match_any_sync(0xffffffffu, bin[k]);
+            const int leader = __ffs(peers) - 1;
+            const int lane = tid & 31;
+            unsigned int base = 0;
+            if (lane == leader && bin[k] < NB) base = atomicAdd(&scnt[bin[k]], (unsigned int)__popc(peers));
+            base = __shfl_sync(0xffffffffu, base, leader);
+            rank[k] = base + __popc(peers & ((1u << lane) - 1u));
+        }
+        __syncthreads();
+        for (int b = tid; b < NB; b += SORT_THREADS)
+            if (scnt[b]) sbase[b] = spre[b] + atomicAdd(&gcur[b], scnt[b]);
+        __syncthreads();
+#pragma unroll
+        for (int k = 0; k < PER; k++) {
+            if (bin[k] < NB) {
+                const unsigned int pos = sbase[bin[k]] + rank[k];
+                dst_idx[pos] = idx[k];
+                dst_val[pos] = val[k];
+            }
+        }
+        __syncthreads();
+        for (int b = tid; b < NB; b += SORT_THREADS) scnt[b] = 0;
+        __syncthreads();
+    }
+}
+
+__device__ __forceinline__ unsigned int nonzero_bins(const unsigned int* bins, int nb) {
+    unsigned int c = 0;
+    for (int b = 0; b < nb; b++) c += bins[b] != 0;
+    return c;
+}
+
+__global__ void __launch_bounds__(SORT_THREADS) qscatter_kernel(DevPlan* __restrict__ plan, Queues q) {
+    __shared__ unsigned int spre[65], scnt[65], sbase[65];
+    __shared__ unsigned int do32, do64;
+    if (threadIdx.x == 0) {
+        do32 = nonzero_bins(plan->bins32, 33) >= 3;
+        do64 = nonzero_bins(plan->bins64, 65) >= 3;
+        if (blockIdx.x == 0) { plan->sorted32 = do32; plan->sorted64 = do64; }
+    }
+    __syncthreads();
+    if (do32)
+        scatter_sorted<uint32_t, 33>(plan->bins32, plan->cur32, plan->counts[0], q.q32_idx, q.q32_val,
+                                     q.s32_idx, q.s32_val, spre, scnt, sbase);
+    __syncthreads();
+    if (do64)
+        scatter_sorted<unsigned long long, 65>(plan->bins64, plan->cur64, plan->counts[1], q.q64_idx, q.q64_val,
+                                               q.s64_idx, q.s64_val, spre, scnt, sbase);
+}
+
 // ------------------------------------------------------------- A3: MR phase 1
 // Warp-aggregated append of (idx, val) when `pred`.
 template <typename T>
@@ -614,6 +735,50 @@ __device__ __forceinline__ void warp_append(bool pred, uint32_t idx, T val, unsi
     }
 }
 
+// Per-warp staging buffer in shared memory: appends go to the global queue 32
+// at a time (one atomicAdd per 32 entries instead of one per warp iteration).
+template <typename T>
+struct WarpStage {
+    uint32_t idx[64];
+    T val[64];
+};
+
+template <typename T>
+__device__ __forceinline__ void stage_append(bool pred, uint32_t idx, T val, WarpStage<T>& st, unsigned int& n,
+                                             unsigned int* counter, uint32_t* qidx, T* qval) {
+    const int lane = threadIdx.x & 31;
+    const unsigned int mask = __ballot_sync(0xffffffffu, pred);
+    if (pred) {
+        const unsigned int pos = n + __popc(mask & ((1u << lane) - 1u));
+        st.idx[pos] = idx;
+        st.val[pos] = val;
+    }
+    n += __popc(mask);
+    __syncwarp();
+    if (n >= 32) {
+        unsigned int base = 0;
+        if (lane == 0) base = atomicAdd(counter, 32u);
+        base = __shfl_sync(0xffffffffu, base, 0);
+        qidx[base + lane] = st.idx[lane];
+        qval[base + lane] = st.val[lane];
+        __syncwarp();
+        if (lane + 32 < n) { st.idx[lane] = st.idx[lane + 32]; st.val[lane] = st.val[lane + 32]; }
+        n -= 32;
+        __syncwarp();
+    }
+}
+
+template <typename T>
+__device__ __forceinline__ void stage_flush(WarpStage<T>& st, unsigned int n, unsigned int* counter, uint32_t* qidx,
+                                            T* qval) {
+    const int lane = threadIdx.x & 31;
+    if (!n) return;
+    unsigned int base = 0;
+    if (lane == 0) base = atomicAdd(counter, n);
+    base = __shfl_sync(0xffffffffu, base, 0);
+    if ((unsigned int)lane < n) { qidx[base + lane] = st.idx[lane]; qval[base + lane] = st.val[lane]; }
+}
+
 __device__ __forceinline__ unsigned long long warp_sum(unsigned long long v) {
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
@@ -628,40 +793,50 @@ __device__ __forceinline__ unsigned long long odd_part(unsigned long long n) { r
 
 __global__ void __launch_bounds__(MR_THREADS)
 mr1_kernel(DevPlan* __restrict__ plan, Queues q, int count_work) {
+    __shared__ WarpStage<uint32_t> st32[MR_THREADS / 32];
+    __shared__ WarpStage<unsigned long long> st64[MR_THREADS / 32];
     const unsigned int c32 = plan->counts[0], c64 = plan->counts[1];
+    const uint32_t* q32i = plan->sorted32 ? q.s32_idx : q.q32_idx;
+    const uint32_t* q32v = plan->sorted32 ? q.s32_val : q.q32_val;
+    const uint32_t* q64i = plan->sorted64 ? q.s64_idx : q.q64_idx;
+    const unsigned long long* q64v = plan->sorted64 ? q.s64_val : q.q64_val;
     unsigned long long w32 = 0, w64 = 0;
-    const unsigned int lane = threadIdx.x & 31;
+    const unsigned int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
     const unsigned int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const unsigned int nwarps = (gridDim.x * blockDim.x) >> 5;
+    unsigned int ns = 0;
     for (unsigned int b = warp * 32; b < c32; b += nwarps * 32) {
         const unsigned int i = b + lane;
         bool pass = false;
         uint32_t n = 0, idx = 0;
         if (i < c32) {
-            n = q.q32_val[i];
-            idx = q.q32_idx[i];
+            n = q32v[i];
+            idx = q32i[i];
             pass = sprp2_32(n);
             if (count_work) w32 += modexp_squarings(odd_part(n));
         }
-        warp_append<uint32_t>(pass, idx, n, &plan->counts[2], q.p32_idx, q.p32_val);
+        stage_append<uint32_t>(pass, idx, n, st32[wib], ns, &plan->counts[2], q.p32_idx, q.p32_val);
     }
+    stage_flush<uint32_t>(st32[wib], ns, &plan->counts[2], q.p32_idx, q.p32_val);
+    ns = 0;
     for (unsigned int b = warp * 32; b < c64; b += nwarps * 32) {
         const unsigned int i = b + lane;
         bool pass = false;
         unsigned long long n = 0;
         uint32_t idx = 0;
         if (i < c64) {
-            n = q.q64_val[i];
-            idx = q.q64_idx[i];
+            n = q64v[i];
+            idx = q64i[i];
             pass = sprp2_64(n);
             if (count_work) w64 += modexp_squarings(odd_part(n));
         }
-        warp_append<unsigned long long>(pass, idx, n, &plan->counts[3], q.p64_idx, q.p64_val);
+        stage_append<unsigned long long>(pass, idx, n, st64[wib], ns, &plan->counts[3], q.p64_idx, q.p64_val);
     }
+    stage_flush<unsigned long long>(st64[wib], ns, &plan->counts[3], q.p64_idx, q.p64_val);
     if (count_work) {
         w32 = warp_sum(w32);
         w64 = warp_sum(w64);
-        if ((threadIdx.x & 31) == 0) {
+        if (lane == 0) {
             if (w32) atomicAdd(&plan->work[0], w32);
             if (w64) atomicAdd(&plan->work[1], w64);
         }

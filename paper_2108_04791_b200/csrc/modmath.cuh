@@ -94,19 +94,117 @@ __device__ __forceinline__ uint64_t inv64(uint64_t n) {
     return x;
 }
 
+// 64x64 -> 128 product from four 32x32 IMAD.WIDE.U32, each folding one
+// addend into the multiplier's 64-bit accumulate (no separate carry chain):
+//   a*b = lo(p00) + lo(p10) 2^32 + (a1 b1 + hi(p01) + hi(p10)) 2^64
+// with p01 = a0 b1 + hi(p00), p10 = a1 b0 + lo(p01); the high sum never
+// exceeds 2^64 - 1.
+__device__ __forceinline__ void mul_wide64(uint64_t a, uint64_t b, uint64_t& lo, uint64_t& hi) {
+    const uint32_t a0 = (uint32_t)a, a1 = (uint32_t)(a >> 32), b0 = (uint32_t)b, b1 = (uint32_t)(b >> 32);
+    const uint64_t p00 = (uint64_t)a0 * b0;
+    const uint64_t p01 = (uint64_t)a0 * b1 + (p00 >> 32);
+    const uint64_t p10 = (uint64_t)a1 * b0 + (uint32_t)p01;
+    hi = (uint64_t)a1 * b1 + ((p01 >> 32) + (p10 >> 32));
+    lo = (p10 << 32) | (uint32_t)p00;
+}
+
+// a^2 with three products: a0^2, a0 a1 (used twice), a1^2.
+__device__ __forceinline__ void sqr_wide64(uint64_t a, uint64_t& lo, uint64_t& hi) {
+    const uint32_t a0 = (uint32_t)a, a1 = (uint32_t)(a >> 32);
+    const uint64_t p00 = (uint64_t)a0 * a0;
+    const uint64_t c = (uint64_t)a0 * a1;
+    const uint64_t s1 = (p00 >> 32) + (uint32_t)(c << 1);  // < 2^33
+    hi = (uint64_t)a1 * a1 + ((c >> 31) + (s1 >> 32));
+    lo = (s1 << 32) | (uint32_t)p00;
+}
+
+// Subtraction REDC: m = lo * n^-1 mod 2^64 (one IMAD.WIDE + two IMAD), then
+// hi(m n) from four IMAD.WIDE (its low half equals lo by construction).
 __device__ __forceinline__ uint64_t redc64(uint64_t lo, uint64_t hi, uint64_t n, uint64_t ninv) {
-    uint64_t m = lo * ninv;
-    uint64_t mh = __umul64hi(m, n);
-    uint64_t t = hi - mh;
+    const uint32_t t0 = (uint32_t)lo, t1 = (uint32_t)(lo >> 32);
+    const uint32_t i0 = (uint32_t)ninv, i1 = (uint32_t)(ninv >> 32);
+    const uint64_t mw = (uint64_t)t0 * i0;
+    const uint32_t m0 = (uint32_t)mw;
+    const uint32_t m1 = (uint32_t)(mw >> 32) + t0 * i1 + t1 * i0;
+    const uint32_t n0 = (uint32_t)n, n1 = (uint32_t)(n >> 32);
+    const uint64_t q00 = (uint64_t)m0 * n0;
+    const uint64_t q01 = (uint64_t)m0 * n1 + (q00 >> 32);
+    const uint64_t q10 = (uint64_t)m1 * n0 + (uint32_t)q01;
+    const uint64_t mh = (uint64_t)m1 * n1 + ((q01 >> 32) + (q10 >> 32));
+    const uint64_t t = hi - mh;
     return hi < mh ? t + n : t;
 }
 
+// The same squaring + REDC written as one PTX block with explicit carry
+// chains (add.cc / addc): the cross term a0*a1 is added twice instead of
+// being doubled with shifts, and hi(m*n) is assembled from four mul.wide.
+__device__ __forceinline__ uint64_t msqr64_ptx(uint64_t x, uint64_t n, uint64_t ninv) {
+    uint64_t r;
+    asm("{\n\t"
+        ".reg .u32 x0, x1, n0, n1, i0, i1, p0, p1, c0, c1, h0, h1, t1, t2, t3, m0, m1;\n\t"
+        ".reg .u32 q0, q1, a0, a1, b0, b1, d0, d1, u2, u3, r0, r1, bw, k0, k1;\n\t"
+        ".reg .u64 W;\n\t"
+        "mov.b64 {x0, x1}, %1;\n\t"
+        "mov.b64 {n0, n1}, %2;\n\t"
+        "mov.b64 {i0, i1}, %3;\n\t"
+        // T = x^2 = (t3 t2 t1 p0)
+        "mul.wide.u32 W, x0, x0;\n\t"
+        "mov.b64 {p0, p1}, W;\n\t"
+        "mul.wide.u32 W, x0, x1;\n\t"
+        "mov.b64 {c0, c1}, W;\n\t"
+        "mul.wide.u32 W, x1, x1;\n\t"
+        "mov.b64 {h0, h1}, W;\n\t"
+        "add.cc.u32 t1, p1, c0;\n\t"
+        "addc.cc.u32 t2, h0, c1;\n\t"
+        "addc.u32 t3, h1, 0;\n\t"
+        "add.cc.u32 t1, t1, c0;\n\t"
+        "addc.cc.u32 t2, t2, c1;\n\t"
+        "addc.u32 t3, t3, 0;\n\t"
+        // m = (t1 p0) * ninv mod 2^64
+        "mul.wide.u32 W, p0, i0;\n\t"
+        "mov.b64 {m0, m1}, W;\n\t"
+        "mad.lo.u32 m1, p0, i1, m1;\n\t"
+        "mad.lo.u32 m1, t1, i0, m1;\n\t"
+        // hi(m*n) = (u3 u2): columns of m0n0, m0n1, m1n0, m1n1
+        "mul.wide.u32 W, m0, n0;\n\t"
+        "mov.b64 {q0, q1}, W;\n\t"
+        "mul.wide.u32 W, m0, n1;\n\t"
+        "mov.b64 {a0, a1}, W;\n\t"
+        "mul.wide.u32 W, m1, n0;\n\t"
+        "mov.b64 {b0, b1}, W;\n\t"
+        "mul.wide.u32 W, m1, n1;\n\t"
+        "mov.b64 {d0, d1}, W;\n\t"
+        "add.cc.u32 q1, q1, a0;\n\t"
+        "addc.cc.u32 u2, d0, a1;\n\t"
+        "addc.u32 u3, d1, 0;\n\t"
+        "add.cc.u32 q1, q1, b0;\n\t"
+        "addc.cc.u32 u2, u2, b1;\n\t"
+        "addc.u32 u3, u3, 0;\n\t"
+        // r = (t3 t2) - (u3 u2), + n on borrow
+        "sub.cc.u32 r0, t2, u2;\n\t"
+        "subc.cc.u32 r1, t3, u3;\n\t"
+        "subc.u32 bw, 0, 0;\n\t"
+        "and.b32 k0, n0, bw;\n\t"
+        "and.b32 k1, n1, bw;\n\t"
+        "add.cc.u32 r0, r0, k0;\n\t"
+        "addc.u32 r1, r1, k1;\n\t"
+        "mov.b64 %0, {r0, r1};\n\t"
+        "}"
+        : "=l"(r)
+        : "l"(x), "l"(n), "l"(ninv));
+    return r;
+}
+
 __device__ __forceinline__ uint64_t mmul64(uint64_t a, uint64_t b, const Mont64& M) {
-    return redc64(a * b, __umul64hi(a, b), M.n, M.ninv);
+    uint64_t lo, hi;
+    mul_wide64(a, b, lo, hi);
+    return redc64(lo, hi, M.n, M.ninv);
 }
 
 __device__ __forceinline__ uint64_t msqr64(uint64_t a, const Mont64& M) {
-    return redc64(a * a, __umul64hi(a, a), M.n, M.ninv);
+    uint64_t lo, hi;
+    sqr_wide64(a, lo, hi);
+    return redc64(lo, hi, M.n, M.ninv);
 }
 
 // ModAdd, Property 1: a + b mod n = a - (n - b) when a >= n - b.

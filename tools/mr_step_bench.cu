@@ -1,0 +1,96 @@
+// mr_step_bench.cu -- throughput of one base-2 ladder step (Montgomery square +
+// conditional modular doubling) for several formulations of the 64-bit
+// Montgomery squaring, 8 independent chains per thread, full grid.
+//   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -o tools/mr_step_bench tools/mr_step_bench.cu
+#include <cuda_runtime.h>
+#include <cstdio>
+#include <cstdint>
+#include "../paper_2108_04791_b200/csrc/modmath.cuh"
+
+constexpr int CH = 4;
+constexpr int ITERS = 1024;
+
+// v0: the original __umul64hi formulation
+__device__ __forceinline__ uint64_t sqr_v0(uint64_t a, uint64_t n, uint64_t ninv) {
+    uint64_t lo = a * a, hi = __umul64hi(a, a);
+    uint64_t m = lo * ninv, mh = __umul64hi(m, n);
+    uint64_t t = hi - mh;
+    return hi < mh ? t + n : t;
+}
+__device__ __forceinline__ uint64_t sqr_v1(uint64_t a, uint64_t n, uint64_t ninv) {
+    uint64_t lo, hi;
+    isp::sqr_wide64(a, lo, hi);
+    return isp::redc64(lo, hi, n, ninv);
+}
+__device__ __forceinline__ uint64_t sqr_v2(uint64_t a, uint64_t n, uint64_t ninv) { return isp::msqr64_ptx(a, n, ninv); }
+
+template <int V, bool DBL>
+__global__ void k_step(unsigned long long* out, unsigned long long seed, unsigned long long dbits) {
+    const unsigned long long n = (seed | 1ull | (1ull << 63)) ^ ((unsigned long long)threadIdx.x << 20);
+    const unsigned long long ninv = isp::inv64(n);
+    unsigned long long x[CH];
+#pragma unroll
+    for (int c = 0; c < CH; c++) x[c] = ((threadIdx.x + 1) * 0x9E3779B97F4A7C15ull + c * 0x1234567ull) % n;
+    for (int i = 0; i < ITERS; i++) {
+        const bool bit = (dbits >> (i & 63)) & 1ull;
+#pragma unroll
+        for (int c = 0; c < CH; c++) {
+            unsigned long long y = V == 0 ? sqr_v0(x[c], n, ninv) : V == 1 ? sqr_v1(x[c], n, ninv) : sqr_v2(x[c], n, ninv);
+            if (DBL) {
+                const unsigned long long z = isp::mdbl64(y, n);
+                y = bit ? z : y;
+            }
+            x[c] = y;
+        }
+    }
+    unsigned long long s = 0;
+#pragma unroll
+    for (int c = 0; c < CH; c++) s ^= x[c];
+    out[blockIdx.x * blockDim.x + threadIdx.x] = s;
+}
+
+template <typename F>
+float time_ms(F f) {
+    cudaEvent_t a, b;
+    cudaEventCreate(&a); cudaEventCreate(&b);
+    f(); cudaDeviceSynchronize();
+    cudaEventRecord(a);
+    for (int r = 0; r < 5; r++) f();
+    cudaEventRecord(b); cudaEventSynchronize(b);
+    float ms = 0; cudaEventElapsedTime(&ms, a, b);
+    return ms / 5;
+}
+
+int main() {
+    int sms = 0; cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+    unsigned long long* buf; 
+    const int threads = 256;
+    int maxb = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&maxb, k_step<2, true>, threads, 0);
+    const int blocks = sms * (maxb > 0 ? maxb : 4);
+    cudaMalloc(&buf, (size_t)blocks * threads * 8);
+    const double steps = (double)blocks * threads * CH * ITERS;
+    const unsigned long long bits = 0xB5A3C96E1D4F2A87ull;
+    float t[6];
+    t[0] = time_ms([&] { k_step<0, false><<<blocks, threads>>>(buf, 0xD1B54A32D192ED03ull, bits); });
+    t[1] = time_ms([&] { k_step<1, false><<<blocks, threads>>>(buf, 0xD1B54A32D192ED03ull, bits); });
+    t[2] = time_ms([&] { k_step<2, false><<<blocks, threads>>>(buf, 0xD1B54A32D192ED03ull, bits); });
+    t[3] = time_ms([&] { k_step<0, true><<<blocks, threads>>>(buf, 0xD1B54A32D192ED03ull, bits); });
+    t[4] = time_ms([&] { k_step<1, true><<<blocks, threads>>>(buf, 0xD1B54A32D192ED03ull, bits); });
+    t[5] = time_ms([&] { k_step<2, true><<<blocks, threads>>>(buf, 0xD1B54A32D192ED03ull, bits); });
+    // cross-check: the three squarings agree
+    unsigned long long h[3];
+    cudaError_t e = cudaDeviceSynchronize();
+    for (int v = 0; v < 3; v++) {
+        if (v == 0) k_step<0, true><<<1, 32>>>(buf, 77, bits);
+        if (v == 1) k_step<1, true><<<1, 32>>>(buf, 77, bits);
+        if (v == 2) k_step<2, true><<<1, 32>>>(buf, 77, bits);
+        cudaMemcpy(&h[v], buf + 5, 8, cudaMemcpyDeviceToHost);
+    }
+    printf("{\"blocks\": %d, \"err\": \"%s\", \"agree\": %s, \"steps_per_s\": {\"sqr_v0\": %.4e, \"sqr_v1\": %.4e, \"sqr_ptx\": %.4e, "
+           "\"ladder_v0\": %.4e, \"ladder_v1\": %.4e, \"ladder_ptx\": %.4e}}\n",
+           blocks, cudaGetErrorString(e), (h[0] == h[1] && h[1] == h[2]) ? "true" : "false",
+           steps / (t[0] * 1e-3), steps / (t[1] * 1e-3), steps / (t[2] * 1e-3),
+           steps / (t[3] * 1e-3), steps / (t[4] * 1e-3), steps / (t[5] * 1e-3));
+    return 0;
+}
