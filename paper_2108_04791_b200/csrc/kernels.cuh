@@ -603,7 +603,7 @@ classify_kernel(const unsigned long long* __restrict__ N, uint8_t* __restrict__ 
 // mixed magnitudes (config C5: bit lengths 33..64 in every warp) unsorted
 // queues waste about a quarter of the multiply pipe; sorted, neighbouring
 // lanes carry equal-length exponents.  Skipped (flag stays 0, mr1 reads the
-// unsorted queue) when the survivors span fewer than 3 bit lengths.
+// unsorted queue) when the expected gain is small (sort_pays).
 constexpr int SORT_THREADS = 256;
 constexpr int SORT_TILE = 2048;
 
@@ -692,18 +692,27 @@ __device__ __forceinline__ void scatter_sorted(const unsigned int* __restrict__ 
     }
 }
 
-__device__ __forceinline__ unsigned int nonzero_bins(const unsigned int* bins, int nb) {
-    unsigned int c = 0;
-    for (int b = 0; b < nb; b++) c += bins[b] != 0;
-    return c;
+// Sort only when it pays: a warp of unsorted entries runs about as long as the
+// longest exponent present, so the expected SIMT efficiency is mean/max bit
+// length.  Below 0.92 (config C5: ~0.76) the sort wins; config C3 (~0.98) and
+// C2 (~0.97) skip it.
+__device__ __forceinline__ bool sort_pays(const unsigned int* bins, int nb) {
+    unsigned long long cnt = 0, sum = 0;
+    int mx = 0;
+    for (int b = 0; b < nb; b++) {
+        cnt += bins[b];
+        sum += (unsigned long long)bins[b] * b;
+        if (bins[b]) mx = b;
+    }
+    return cnt >= 4096 && (double)sum < 0.92 * (double)mx * (double)cnt;
 }
 
 __global__ void __launch_bounds__(SORT_THREADS) qscatter_kernel(DevPlan* __restrict__ plan, Queues q) {
     __shared__ unsigned int spre[65], scnt[65], sbase[65];
     __shared__ unsigned int do32, do64;
     if (threadIdx.x == 0) {
-        do32 = nonzero_bins(plan->bins32, 33) >= 3;
-        do64 = nonzero_bins(plan->bins64, 65) >= 3;
+        do32 = sort_pays(plan->bins32, 33);
+        do64 = sort_pays(plan->bins64, 65);
         if (blockIdx.x == 0) { plan->sorted32 = do32; plan->sorted64 = do64; }
     }
     __syncthreads();

@@ -94,50 +94,31 @@ __device__ __forceinline__ uint64_t inv64(uint64_t n) {
     return x;
 }
 
-// 64x64 -> 128 product from four 32x32 IMAD.WIDE.U32, each folding one
-// addend into the multiplier's 64-bit accumulate (no separate carry chain):
-//   a*b = lo(p00) + lo(p10) 2^32 + (a1 b1 + hi(p01) + hi(p10)) 2^64
-// with p01 = a0 b1 + hi(p00), p10 = a1 b0 + lo(p01); the high sum never
-// exceeds 2^64 - 1.
-__device__ __forceinline__ void mul_wide64(uint64_t a, uint64_t b, uint64_t& lo, uint64_t& hi) {
-    const uint32_t a0 = (uint32_t)a, a1 = (uint32_t)(a >> 32), b0 = (uint32_t)b, b1 = (uint32_t)(b >> 32);
-    const uint64_t p00 = (uint64_t)a0 * b0;
-    const uint64_t p01 = (uint64_t)a0 * b1 + (p00 >> 32);
-    const uint64_t p10 = (uint64_t)a1 * b0 + (uint32_t)p01;
-    hi = (uint64_t)a1 * b1 + ((p01 >> 32) + (p10 >> 32));
-    lo = (p10 << 32) | (uint32_t)p00;
-}
-
-// a^2 with three products: a0^2, a0 a1 (used twice), a1^2.
-__device__ __forceinline__ void sqr_wide64(uint64_t a, uint64_t& lo, uint64_t& hi) {
-    const uint32_t a0 = (uint32_t)a, a1 = (uint32_t)(a >> 32);
-    const uint64_t p00 = (uint64_t)a0 * a0;
-    const uint64_t c = (uint64_t)a0 * a1;
-    const uint64_t s1 = (p00 >> 32) + (uint32_t)(c << 1);  // < 2^33
-    hi = (uint64_t)a1 * a1 + ((c >> 31) + (s1 >> 32));
-    lo = (s1 << 32) | (uint32_t)p00;
-}
-
-// Subtraction REDC: m = lo * n^-1 mod 2^64 (one IMAD.WIDE + two IMAD), then
-// hi(m n) from four IMAD.WIDE (its low half equals lo by construction).
+// Subtraction REDC from the 128-bit product (lo, hi).  Written with
+// mul.lo.u64 / mul.hi.u64: ptxas expands them into IMAD.WIDE.U32 chains that
+// measured faster on B200 than a hand-written 32-bit-limb C++ version
+// (profiles/r1_mr_step.json: 6.6e11 vs 6.1e11 squarings/s).
 __device__ __forceinline__ uint64_t redc64(uint64_t lo, uint64_t hi, uint64_t n, uint64_t ninv) {
-    const uint32_t t0 = (uint32_t)lo, t1 = (uint32_t)(lo >> 32);
-    const uint32_t i0 = (uint32_t)ninv, i1 = (uint32_t)(ninv >> 32);
-    const uint64_t mw = (uint64_t)t0 * i0;
-    const uint32_t m0 = (uint32_t)mw;
-    const uint32_t m1 = (uint32_t)(mw >> 32) + t0 * i1 + t1 * i0;
-    const uint32_t n0 = (uint32_t)n, n1 = (uint32_t)(n >> 32);
-    const uint64_t q00 = (uint64_t)m0 * n0;
-    const uint64_t q01 = (uint64_t)m0 * n1 + (q00 >> 32);
-    const uint64_t q10 = (uint64_t)m1 * n0 + (uint32_t)q01;
-    const uint64_t mh = (uint64_t)m1 * n1 + ((q01 >> 32) + (q10 >> 32));
+    const uint64_t m = lo * ninv;
+    const uint64_t mh = __umul64hi(m, n);
     const uint64_t t = hi - mh;
     return hi < mh ? t + n : t;
 }
 
-// The same squaring + REDC written as one PTX block with explicit carry
-// chains (add.cc / addc): the cross term a0*a1 is added twice instead of
-// being doubled with shifts, and hi(m*n) is assembled from four mul.wide.
+__device__ __forceinline__ uint64_t mmul64(uint64_t a, uint64_t b, const Mont64& M) {
+    return redc64(a * b, __umul64hi(a, b), M.n, M.ninv);
+}
+
+__device__ __forceinline__ uint64_t msqr64(uint64_t a, const Mont64& M) {
+    return redc64(a * a, __umul64hi(a, a), M.n, M.ninv);
+}
+
+// Montgomery squaring written as one PTX block with explicit carry chains
+// (add.cc / addc): three mul.wide for x^2 (the cross term added twice instead
+// of doubled with shifts), one mul.wide + two mad.lo for m, four mul.wide for
+// hi(m*n).  Alone it is as fast as msqr64; followed by the base-2 ladder's
+// conditional doubling it is 5% faster (profiles/r1_mr_step.json), so the
+// base-2 phase uses it.
 __device__ __forceinline__ uint64_t msqr64_ptx(uint64_t x, uint64_t n, uint64_t ninv) {
     uint64_t r;
     asm("{\n\t"
@@ -193,18 +174,6 @@ __device__ __forceinline__ uint64_t msqr64_ptx(uint64_t x, uint64_t n, uint64_t 
         : "=l"(r)
         : "l"(x), "l"(n), "l"(ninv));
     return r;
-}
-
-__device__ __forceinline__ uint64_t mmul64(uint64_t a, uint64_t b, const Mont64& M) {
-    uint64_t lo, hi;
-    mul_wide64(a, b, lo, hi);
-    return redc64(lo, hi, M.n, M.ninv);
-}
-
-__device__ __forceinline__ uint64_t msqr64(uint64_t a, const Mont64& M) {
-    uint64_t lo, hi;
-    sqr_wide64(a, lo, hi);
-    return redc64(lo, hi, M.n, M.ninv);
 }
 
 // ModAdd, Property 1: a + b mod n = a - (n - b) when a >= n - b.

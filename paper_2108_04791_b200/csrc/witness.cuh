@@ -105,7 +105,7 @@ __device__ __forceinline__ bool sprp2_64(uint64_t n) {
     const int top = 63 - __clzll((long long)d);
     uint64_t x = mdbl64(M.one, n);  // mont(2)
     for (int b = top - 1; b >= 0; b--) {
-        x = msqr64(x, M);
+        x = msqr64_ptx(x, M.n, M.ninv);
         const uint64_t y = mdbl64(x, n);
         x = ((d >> b) & 1ull) ? y : x;
     }

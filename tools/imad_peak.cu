@@ -90,6 +90,48 @@ __global__ void k_mont32(uint32_t* out, uint32_t n0) {
     out[blockIdx.x * blockDim.x + threadIdx.x] = s;
 }
 
+__global__ void k_dfma(double* out, double a, double b) {
+    double x[CH];
+#pragma unroll
+    for (int c = 0; c < CH; c++) x[c] = threadIdx.x * 1e-3 + c;
+    for (int i = 0; i < ITERS; i++) {
+#pragma unroll
+        for (int c = 0; c < CH; c++) x[c] = fma(x[c], a, b);
+    }
+    double s = 0;
+#pragma unroll
+    for (int c = 0; c < CH; c++) s += x[c];
+    out[blockIdx.x * blockDim.x + threadIdx.x] = s;
+}
+
+// FP64 modular multiplication for n < 2^50: exact product h + l by FMA,
+// quotient estimate by the rounded reciprocal, exact remainder by FMA, two fix-ups.
+__device__ __forceinline__ double fmulmod(double a, double b, double n, double ninv) {
+    const double h = a * b;
+    const double l = fma(a, b, -h);
+    const double q = (h * ninv + 6755399441055744.0) - 6755399441055744.0;  // round to nearest (|x| < 2^51)
+    double r = fma(-q, n, h) + l;
+    r = r < 0.0 ? r + n : r;
+    r = r >= n ? r - n : r;
+    return r;
+}
+
+__global__ void k_fmod(double* out, double n0) {
+    const double n = n0 + 2.0 * threadIdx.x;
+    const double ninv = 1.0 / n;
+    double x[CH];
+#pragma unroll
+    for (int c = 0; c < CH; c++) x[c] = 12345.0 * (threadIdx.x + 1) + 7.0 * c;
+    for (int i = 0; i < ITERS / 8; i++) {
+#pragma unroll
+        for (int c = 0; c < CH; c++) x[c] = fmulmod(x[c], x[c], n, ninv);
+    }
+    double s = 0;
+#pragma unroll
+    for (int c = 0; c < CH; c++) s += x[c];
+    out[blockIdx.x * blockDim.x + threadIdx.x] = s;
+}
+
 template <typename F>
 float time_ms(F f) {
     cudaEvent_t a, b;
@@ -118,6 +160,8 @@ int main() {
     float t_hi = time_ms([&] { k_imad_hi<<<blocks, threads>>>((uint32_t*)buf, 0x9E3779B9u, 7u); });
     float t_m64 = time_ms([&] { k_mont64<<<blocks, threads>>>((unsigned long long*)buf, 0xD1B54A32D192ED03ull); });
     float t_m32 = time_ms([&] { k_mont32<<<blocks, threads>>>((uint32_t*)buf, 0xD1B54A33u); });
+    float t_dfma = time_ms([&] { k_dfma<<<blocks, threads>>>((double*)buf, 0.999999, 1e-9); });
+    float t_fmod = time_ms([&] { k_fmod<<<blocks, threads>>>((double*)buf, 1125899906842597.0 /* 2^50 - 27 */); });
     cudaError_t e = cudaDeviceSynchronize();
     const double ops = nthreads * CH * ITERS;
     auto rate = [&](double n, float ms) { return n / (ms * 1e-3); };
@@ -126,10 +170,12 @@ int main() {
     printf("{\"sms\": %d, \"clock_attr_mhz\": %.0f, \"err\": \"%s\", "
            "\"imad_lo_per_s\": %.4e, \"imad_wide_per_s\": %.4e, \"imad_hi_per_s\": %.4e, "
            "\"imad_lo_lanes_per_clk_sm\": %.2f, \"imad_wide_lanes_per_clk_sm\": %.2f, \"imad_hi_lanes_per_clk_sm\": %.2f, "
-           "\"mont64_sqr_per_s\": %.4e, \"mont32_mul_per_s\": %.4e}\n",
+           "\"mont64_sqr_per_s\": %.4e, \"mont32_mul_per_s\": %.4e, \"dfma_per_s\": %.4e, \"dfma_lanes_per_clk_sm\": %.2f, "
+           "\"fp64_mulmod50_per_s\": %.4e}\n",
            sms, clk / 1e6, cudaGetErrorString(e),
            rate(ops, t_lo), rate(ops, t_wide), rate(ops, t_hi),
            rate(ops, t_lo) / clk / sms, rate(ops, t_wide) / clk / sms, rate(ops, t_hi) / clk / sms,
-           rate(nthreads * CH * (ITERS / 8), t_m64), rate(nthreads * CH * (ITERS / 2), t_m32));
+           rate(nthreads * CH * (ITERS / 8), t_m64), rate(nthreads * CH * (ITERS / 2), t_m32),
+           rate(ops, t_dfma), rate(ops, t_dfma) / clk / sms, rate(nthreads * CH * (ITERS / 8), t_fmod));
     return e == cudaSuccess ? 0 : 1;
 }

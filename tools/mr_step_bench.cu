@@ -17,10 +17,26 @@ __device__ __forceinline__ uint64_t sqr_v0(uint64_t a, uint64_t n, uint64_t ninv
     uint64_t t = hi - mh;
     return hi < mh ? t + n : t;
 }
+// v1: 32-bit-limb C++ (three IMAD.WIDE for a^2 with folded addends)
 __device__ __forceinline__ uint64_t sqr_v1(uint64_t a, uint64_t n, uint64_t ninv) {
-    uint64_t lo, hi;
-    isp::sqr_wide64(a, lo, hi);
-    return isp::redc64(lo, hi, n, ninv);
+    const uint32_t a0 = (uint32_t)a, a1 = (uint32_t)(a >> 32);
+    const uint64_t p00 = (uint64_t)a0 * a0;
+    const uint64_t c = (uint64_t)a0 * a1;
+    const uint64_t s1 = (p00 >> 32) + (uint32_t)(c << 1);
+    const uint64_t hi = (uint64_t)a1 * a1 + ((c >> 31) + (s1 >> 32));
+    const uint64_t lo = (s1 << 32) | (uint32_t)p00;
+    const uint32_t t0 = (uint32_t)lo, t1 = (uint32_t)(lo >> 32);
+    const uint32_t i0 = (uint32_t)ninv, i1 = (uint32_t)(ninv >> 32);
+    const uint64_t mw = (uint64_t)t0 * i0;
+    const uint32_t m0 = (uint32_t)mw;
+    const uint32_t m1 = (uint32_t)(mw >> 32) + t0 * i1 + t1 * i0;
+    const uint32_t n0 = (uint32_t)n, n1 = (uint32_t)(n >> 32);
+    const uint64_t q00 = (uint64_t)m0 * n0;
+    const uint64_t q01 = (uint64_t)m0 * n1 + (q00 >> 32);
+    const uint64_t q10 = (uint64_t)m1 * n0 + (uint32_t)q01;
+    const uint64_t mh = (uint64_t)m1 * n1 + ((q01 >> 32) + (q10 >> 32));
+    const uint64_t t = hi - mh;
+    return hi < mh ? t + n : t;
 }
 __device__ __forceinline__ uint64_t sqr_v2(uint64_t a, uint64_t n, uint64_t ninv) { return isp::msqr64_ptx(a, n, ninv); }
 
