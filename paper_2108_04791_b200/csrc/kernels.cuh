@@ -704,7 +704,15 @@ __device__ __forceinline__ bool sort_pays(const unsigned int* bins, int nb) {
         sum += (unsigned long long)bins[b] * b;
         if (bins[b]) mx = b;
     }
-    return cnt >= 4096 && (double)sum < 0.92 * (double)mx * (double)cnt;
+    if (cnt < 4096) return false;
+    if ((double)sum < 0.92 * (double)mx * (double)cnt) return true;
+    // both sides of the FP64 / Montgomery boundary (bit length 49 | 50) present
+    if (nb == 65) {
+        unsigned long long lo = 0;
+        for (int b = 0; b <= 49; b++) lo += bins[b];
+        if (lo > cnt / 64 && lo < cnt - cnt / 64) return true;
+    }
+    return false;
 }
 
 __global__ void __launch_bounds__(SORT_THREADS) qscatter_kernel(DevPlan* __restrict__ plan, Queues q) {
@@ -836,7 +844,11 @@ mr1_kernel(DevPlan* __restrict__ plan, Queues q, int count_work) {
         if (i < c64) {
             n = q64v[i];
             idx = q64i[i];
-            pass = sprp2_64(n);
+        }
+        // magnitude-class dispatch: below 2^49 on the FP64 pipe, above with
+        // 64-bit Montgomery (warp-uniform on the bit-length-sorted queue)
+        if (i < c64) {
+            pass = n < FP_LIMIT ? sprp2_f64(n) : sprp2_64(n);
             if (count_work) w64 += modexp_squarings(odd_part(n));
         }
         stage_append<unsigned long long>(pass, idx, n, st64[wib], ns, &plan->counts[3], q.p64_idx, q.p64_val);
@@ -871,7 +883,8 @@ mr2_kernel(DevPlan* __restrict__ plan, Queues q, uint8_t* __restrict__ out, int 
     }
     for (unsigned int i = t0; i < c64; i += stride) {
         const unsigned long long n = q.p64_val[i];
-        if (sprp_multi64<6, WIN>(n, c_bases64)) out[q.p64_idx[i]] = 1;
+        const bool prime = n < FP_LIMIT ? sprp_multi_f64<6, WIN>(n, c_bases64) : sprp_multi64<6, WIN>(n, c_bases64);
+        if (prime) out[q.p64_idx[i]] = 1;
         if (count_work) {
             const unsigned long long d = odd_part(n);
             w64 += 6ull * (modexp_squarings(d) + modexp_mults(d));
@@ -925,8 +938,12 @@ __global__ void sprp_diag_kernel(const unsigned long long* __restrict__ n, const
             else { const uint32_t b[1] = {am}; r = sprp_multi32<1>((uint32_t)nn, b); }
         } else {
             const unsigned long long am = aa % nn;
-            if (am == 2ull) r = sprp2_64(nn);
-            else { const unsigned long long b[1] = {am}; r = sprp_multi64<1, WIN>(nn, b); }
+            const bool fp = nn < FP_LIMIT;
+            if (am == 2ull) r = fp ? sprp2_f64(nn) : sprp2_64(nn);
+            else {
+                const unsigned long long b[1] = {am};
+                r = fp ? sprp_multi_f64<1, WIN>(nn, b) : sprp_multi64<1, WIN>(nn, b);
+            }
         }
     }
     out[i] = r;

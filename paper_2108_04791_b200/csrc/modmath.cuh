@@ -217,4 +217,43 @@ __device__ __forceinline__ uint64_t mont64_r2(const Mont64& M) {
     return x;
 }
 
+// ------------------------------------------------------- FP64, n < 2^49 ----
+// The paper's medium class (2^18 .. 2^49) is the range where
+// double precision is exact -- and on B200 the FP64 pipe issues 64 DFMA
+// lanes/clk/SM (profiles/r1_imad_peak.json: 63.1) against 25 for the
+// IMAD.WIDE.U32 that 64-bit Montgomery needs.  For odd n < 2^49 and a, b < n:
+//   h = fl(ab), l = fma(a, b, -h) = ab - h exactly (|l| <= 2^45),
+//   q = nearest integer to fl(h * fl(1/n)): |q - ab/n| < 0.7,
+//   r = fma(-q, n, h) + l = ab - qn exactly (|r| < 2^50), in (-n, n),
+// and one conditional +n gives ab mod n.  Rounding to an integer uses the
+// 1.5 * 2^52 addend (valid for |x| < 2^51).
+constexpr double FP_RND = 6755399441055744.0;  // 1.5 * 2^52
+constexpr unsigned long long FP_LIMIT = 1ull << 49;
+
+struct ModF {
+    double n, ninv, nm1;  // n, fl(1/n), n - 1
+};
+
+__device__ __forceinline__ ModF modf_setup(unsigned long long n) {
+    ModF M;
+    M.n = (double)n;
+    M.ninv = 1.0 / M.n;
+    M.nm1 = M.n - 1.0;
+    return M;
+}
+
+__device__ __forceinline__ double fmulmod(double a, double b, const ModF& M) {
+    const double h = a * b;
+    const double l = fma(a, b, -h);
+    const double q = __dadd_rn(__dmul_rn(h, M.ninv), FP_RND) - FP_RND;
+    const double r = fma(-q, M.n, h) + l;
+    return r < 0.0 ? r + M.n : r;
+}
+
+// ModAdd in doubles: a + b < 2n < 2^50 is exact.
+__device__ __forceinline__ double faddmod(double a, double b, const ModF& M) {
+    const double s = a + b;
+    return s >= M.n ? s - M.n : s;
+}
+
 }  // namespace isp

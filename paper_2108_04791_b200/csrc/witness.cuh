@@ -188,4 +188,94 @@ __device__ __forceinline__ bool sprp_multi64(uint64_t n, const unsigned long lon
     return ok;
 }
 
+// ------------------------------------------------------- FP64 class ----
+// The same two phases on the FP64 pipe for odd n < 2^49 (modmath.cuh, ModF):
+// plain residues (no Montgomery form), so 1 and -1 are 1.0 and n - 1.
+__device__ __forceinline__ bool sprp2_f64(unsigned long long n) {
+    const ModF M = modf_setup(n);
+    unsigned long long d = n - 1;
+    const int s = __ffsll((long long)d) - 1;
+    d >>= s;
+    const int top = 63 - __clzll((long long)d);
+    double x = 2.0;  // top bit of d
+    for (int b = top - 1; b >= 0; b--) {
+        x = fmulmod(x, x, M);
+        const double y = faddmod(x, x, M);  // * 2 (ModMultiply case 3)
+        x = ((d >> b) & 1ull) ? y : x;
+    }
+    if (x == 1.0 || x == M.nm1) return true;
+    for (int r = 1; r < s; r++) {
+        x = fmulmod(x, x, M);
+        if (x == M.nm1) return true;
+        if (x == 1.0) return false;
+    }
+    return false;
+}
+
+template <int T>
+__device__ __forceinline__ double sel_table_f(const double (&tab)[T], uint32_t digit) {
+    double m = 1.0;
+#pragma unroll
+    for (int k = 1; k <= T; k++) m = (digit == (uint32_t)k) ? tab[k - 1] : m;
+    return m;
+}
+
+template <int NB, int WIN>
+__device__ __forceinline__ bool sprp_multi_f64(unsigned long long n, const unsigned long long* bases) {
+    constexpr int T = (1 << WIN) - 1;
+    const ModF M = modf_setup(n);
+    unsigned long long d = n - 1;
+    const int s = __ffsll((long long)d) - 1;
+    d >>= s;
+    const int nbits = 64 - __clzll((long long)d);
+    const int nw = (nbits + WIN - 1) / WIN;
+    double tab[NB][T], x[NB];
+    bool done[NB], pass[NB];
+#pragma unroll
+    for (int i = 0; i < NB; i++) {
+        unsigned long long a = bases[i];
+        if (a >= n) a %= n;
+        done[i] = pass[i] = (a == 0);
+        tab[i][0] = (double)a;
+#pragma unroll
+        for (int k = 1; k < T; k++) tab[i][k] = fmulmod(tab[i][k - 1], tab[i][0], M);
+    }
+    {
+        const uint32_t lead = (uint32_t)(d >> (WIN * (nw - 1)));
+#pragma unroll
+        for (int i = 0; i < NB; i++) x[i] = sel_table_f<T>(tab[i], lead);
+    }
+    for (int w = nw - 2; w >= 0; w--) {
+        const uint32_t digit = (uint32_t)(d >> (WIN * w)) & (uint32_t)T;
+#pragma unroll
+        for (int j = 0; j < WIN; j++) {
+#pragma unroll
+            for (int i = 0; i < NB; i++) x[i] = fmulmod(x[i], x[i], M);
+        }
+#pragma unroll
+        for (int i = 0; i < NB; i++) x[i] = fmulmod(x[i], sel_table_f<T>(tab[i], digit), M);
+    }
+#pragma unroll
+    for (int i = 0; i < NB; i++) {
+        if (!done[i] && (x[i] == 1.0 || x[i] == M.nm1)) done[i] = pass[i] = true;
+    }
+    for (int r = 1; r < s; r++) {
+        bool all = true;
+#pragma unroll
+        for (int i = 0; i < NB; i++) {
+            if (!done[i]) {
+                x[i] = fmulmod(x[i], x[i], M);
+                if (x[i] == M.nm1) done[i] = pass[i] = true;
+                else if (x[i] == 1.0) done[i] = true;
+            }
+            all &= done[i];
+        }
+        if (all) break;
+    }
+    bool ok = true;
+#pragma unroll
+    for (int i = 0; i < NB; i++) ok &= pass[i];
+    return ok;
+}
+
 }  // namespace isp
