@@ -89,6 +89,7 @@ void isprime_shutdown(void);
  * "win64"            exponent window width for the 64-bit multi-base phase (1..3)
  * "sieve_cache"      0 (default): every call sieves its own window; 1: a call may
  *                    reuse the bitmap an earlier call on this device produced
+ * "mr2_group"        3 or 6: 64-bit phase-2 bases run in lockstep groups of this size
  * "kernel_timing"    1: bracket every launch with CUDA events on its stream and
  *                    accumulate per-kernel device time (isprime_get_kernel_times)
  * Returns ISP_OK or ISP_EINVAL. */

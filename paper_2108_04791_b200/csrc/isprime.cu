@@ -35,7 +35,8 @@ struct Options {
     long long mr32_fs_per_bit = 900;      // femtoseconds per odd element per bit (trial division + MR, C2)
     unsigned long long sieve_max = 1ull << 32;
     int kernel_timing = 0;
-    int sieve_cache = 0;     // 1: a call may reuse the bitmap sieved by an earlier call
+    int sieve_cache = 0;
+    int mr2_group = 3;       // 64-bit phase-2 bases run G at a time in lockstep (3 or 6)     // 1: a call may reuse the bitmap sieved by an earlier call
 };
 
 Options g_opt;
@@ -203,7 +204,7 @@ int init_ctx(Ctx* c) {
     c->grid_cls = c->sms * occupancy((const void*)classify_kernel<24, 24>, CLS_THREADS, 0);
     c->grid_mr1 = c->sms * occupancy((const void*)mr1_kernel, MR_THREADS, 0);
     c->grid_sort = c->sms * occupancy((const void*)qscatter_kernel, SORT_THREADS, 0);
-    c->grid_mr2 = c->sms * occupancy((const void*)mr2_kernel<2, false>, MR_THREADS, 0);
+    c->grid_mr2 = c->sms * occupancy((const void*)mr2_kernel<2, false, 3>, MR_THREADS, 0);
     CK(cudaEventCreateWithFlags(&c->last_done, cudaEventDisableTiming));
     for (int k = 0; k < 2; k++) {
         CK(cudaStreamCreateWithFlags(&c->hs[k], cudaStreamNonBlocking));
@@ -307,16 +308,23 @@ void launch_classify(int n32, int n64, int g, cudaStream_t s, const unsigned lon
     }
 }
 
+template <int WIN, int G>
+void launch_mr2_w(Ctx* c, cudaStream_t s, uint8_t* out, int grid, bool full, int cw) {
+    if (full) mr2_kernel<WIN, true, G><<<grid, MR_THREADS, 0, s>>>(c->plan, c->q, out, cw);
+    else mr2_kernel<WIN, false, G><<<grid, MR_THREADS, 0, s>>>(c->plan, c->q, out, cw);
+}
+
 int launch_mr2(Ctx* c, cudaStream_t s, uint8_t* out, int grid) {
     const bool full = g_opt.bases32 == 7;
     const int cw = g_opt.kernel_timing;
-    switch (g_opt.win64 * 2 + (full ? 1 : 0)) {
-        case 2: mr2_kernel<1, false><<<grid, MR_THREADS, 0, s>>>(c->plan, c->q, out, cw); break;
-        case 3: mr2_kernel<1, true><<<grid, MR_THREADS, 0, s>>>(c->plan, c->q, out, cw); break;
-        case 4: mr2_kernel<2, false><<<grid, MR_THREADS, 0, s>>>(c->plan, c->q, out, cw); break;
-        case 5: mr2_kernel<2, true><<<grid, MR_THREADS, 0, s>>>(c->plan, c->q, out, cw); break;
-        case 6: mr2_kernel<3, false><<<grid, MR_THREADS, 0, s>>>(c->plan, c->q, out, cw); break;
-        default: mr2_kernel<3, true><<<grid, MR_THREADS, 0, s>>>(c->plan, c->q, out, cw); break;
+    const int g = g_opt.mr2_group == 6 ? 6 : 3;
+    switch (g_opt.win64 * 10 + g) {
+        case 13: launch_mr2_w<1, 3>(c, s, out, grid, full, cw); break;
+        case 16: launch_mr2_w<1, 6>(c, s, out, grid, full, cw); break;
+        case 23: launch_mr2_w<2, 3>(c, s, out, grid, full, cw); break;
+        case 26: launch_mr2_w<2, 6>(c, s, out, grid, full, cw); break;
+        case 33: launch_mr2_w<3, 3>(c, s, out, grid, full, cw); break;
+        default: launch_mr2_w<3, 6>(c, s, out, grid, full, cw); break;
     }
     CKL("mr2_kernel");
     return ISP_OK;
@@ -568,6 +576,7 @@ int isprime_set_option(const char* key, long long v) {
     else if (!strcmp(key, "sieve_fixed_ns")) { if (v < 0) return ISP_EINVAL; g_opt.sieve_fixed_ns = v; }
     else if (!strcmp(key, "mr32_fs_per_bit")) { if (v < 0) return ISP_EINVAL; g_opt.mr32_fs_per_bit = v; }
     else if (!strcmp(key, "kernel_timing")) { if (v < 0 || v > 1) return ISP_EINVAL; g_opt.kernel_timing = (int)v; }
+    else if (!strcmp(key, "mr2_group")) { if (v != 3 && v != 6) return ISP_EINVAL; g_opt.mr2_group = (int)v; }
     else if (!strcmp(key, "sieve_cache")) { if (v < 0 || v > 1) return ISP_EINVAL; g_opt.sieve_cache = (int)v; }
     else return ISP_EINVAL;
     return ISP_OK;
@@ -589,6 +598,7 @@ long long isprime_get_option(const char* key) {
     if (!strcmp(key, "mr32_fs_per_bit")) return g_opt.mr32_fs_per_bit;
     if (!strcmp(key, "kernel_timing")) return g_opt.kernel_timing;
     if (!strcmp(key, "sieve_cache")) return g_opt.sieve_cache;
+    if (!strcmp(key, "mr2_group")) return g_opt.mr2_group;
     return -1;
 }
 

@@ -865,7 +865,7 @@ mr1_kernel(DevPlan* __restrict__ plan, Queues q, int count_work) {
 }
 
 // ------------------------------------------------------------- A4: MR phase 2
-template <int WIN, bool FULL32>
+template <int WIN, bool FULL32, int G64>
 __global__ void __launch_bounds__(MR_THREADS)
 mr2_kernel(DevPlan* __restrict__ plan, Queues q, uint8_t* __restrict__ out, int count_work) {
     const unsigned int c32 = plan->counts[2], c64 = plan->counts[3];
@@ -883,7 +883,7 @@ mr2_kernel(DevPlan* __restrict__ plan, Queues q, uint8_t* __restrict__ out, int 
     }
     for (unsigned int i = t0; i < c64; i += stride) {
         const unsigned long long n = q.p64_val[i];
-        const bool prime = n < FP_LIMIT ? sprp_multi_f64<6, WIN>(n, c_bases64) : sprp_multi64<6, WIN>(n, c_bases64);
+        const bool prime = n < FP_LIMIT ? sprp_multi_f64<6, G64, WIN>(n, c_bases64) : sprp_multi64<6, G64, WIN>(n, c_bases64);
         if (prime) out[q.p64_idx[i]] = 1;
         if (count_work) {
             const unsigned long long d = odd_part(n);
@@ -942,7 +942,7 @@ __global__ void sprp_diag_kernel(const unsigned long long* __restrict__ n, const
             if (am == 2ull) r = fp ? sprp2_f64(nn) : sprp2_64(nn);
             else {
                 const unsigned long long b[1] = {am};
-                r = fp ? sprp_multi_f64<1, WIN>(nn, b) : sprp_multi64<1, WIN>(nn, b);
+                r = fp ? sprp_multi_f64<1, 1, WIN>(nn, b) : sprp_multi64<1, 1, WIN>(nn, b);
             }
         }
     }

@@ -127,16 +127,14 @@ __device__ __forceinline__ uint64_t sel_table(const uint64_t (&tab)[T], uint32_t
     return m;
 }
 
-// Phase 2: NB bases in lockstep with a fixed WIN-bit window.  Returns true iff
-// n passes every base.  n odd >= 3.  Bases are reduced mod n.
+// Phase 2: NB bases in lockstep with a fixed WIN-bit window, for a modulus
+// whose Montgomery context (M, R2, d, s) is already set up.  Returns true iff
+// n passes every base.  Bases are reduced mod n.
 template <int NB, int WIN>
-__device__ __forceinline__ bool sprp_multi64(uint64_t n, const unsigned long long* bases) {
+__device__ __forceinline__ bool sprp_lockstep64(const Mont64& M, uint64_t R2, uint64_t d, int s,
+                                                const unsigned long long* bases) {
     constexpr int T = (1 << WIN) - 1;
-    const Mont64 M = mont64_setup(n);
-    const uint64_t R2 = mont64_r2(M);
-    uint64_t d = n - 1;
-    const int s = __ffsll((long long)d) - 1;
-    d >>= s;
+    const uint64_t n = M.n;
     const int nbits = 64 - __clzll((long long)d);
     const int nw = (nbits + WIN - 1) / WIN;
     uint64_t tab[NB][T], x[NB];
@@ -188,6 +186,21 @@ __device__ __forceinline__ bool sprp_multi64(uint64_t n, const unsigned long lon
     return ok;
 }
 
+// All NB bases of `bases`, G at a time in lockstep (G | NB), stopping at the
+// first group with a witness.  One Montgomery setup per n.
+template <int NB, int G, int WIN>
+__device__ __forceinline__ bool sprp_multi64(uint64_t n, const unsigned long long* bases) {
+    const Mont64 M = mont64_setup(n);
+    const uint64_t R2 = mont64_r2(M);
+    uint64_t d = n - 1;
+    const int s = __ffsll((long long)d) - 1;
+    d >>= s;
+#pragma unroll 1
+    for (int g = 0; g < NB; g += G)
+        if (!sprp_lockstep64<G, WIN>(M, R2, d, s, bases + g)) return false;
+    return true;
+}
+
 // ------------------------------------------------------- FP64 class ----
 // The same two phases on the FP64 pipe for odd n < 2^49 (modmath.cuh, ModF):
 // plain residues (no Montgomery form), so 1 and -1 are 1.0 and n - 1.
@@ -221,12 +234,9 @@ __device__ __forceinline__ double sel_table_f(const double (&tab)[T], uint32_t d
 }
 
 template <int NB, int WIN>
-__device__ __forceinline__ bool sprp_multi_f64(unsigned long long n, const unsigned long long* bases) {
+__device__ __forceinline__ bool sprp_lockstep_f64(const ModF& M, unsigned long long n, unsigned long long d, int s,
+                                                  const unsigned long long* bases) {
     constexpr int T = (1 << WIN) - 1;
-    const ModF M = modf_setup(n);
-    unsigned long long d = n - 1;
-    const int s = __ffsll((long long)d) - 1;
-    d >>= s;
     const int nbits = 64 - __clzll((long long)d);
     const int nw = (nbits + WIN - 1) / WIN;
     double tab[NB][T], x[NB];
@@ -276,6 +286,18 @@ __device__ __forceinline__ bool sprp_multi_f64(unsigned long long n, const unsig
 #pragma unroll
     for (int i = 0; i < NB; i++) ok &= pass[i];
     return ok;
+}
+
+template <int NB, int G, int WIN>
+__device__ __forceinline__ bool sprp_multi_f64(unsigned long long n, const unsigned long long* bases) {
+    const ModF M = modf_setup(n);
+    unsigned long long d = n - 1;
+    const int s = __ffsll((long long)d) - 1;
+    d >>= s;
+#pragma unroll 1
+    for (int g = 0; g < NB; g += G)
+        if (!sprp_lockstep_f64<G, WIN>(M, n, d, s, bases + g)) return false;
+    return true;
 }
 
 }  // namespace isp

@@ -1,2 +1,1 @@
-bash tools/gpu_session.sh
-EXPLORE_CONFIGS="C3 C5" bash tools/gpu_explore.sh
+NCU_CFG=C5 bash tools/gpu_ncu.sh
