@@ -34,13 +34,19 @@ import workloads  # noqa: E402
 
 METRIC = "Gints/sec classified (1/2/4/8 B200) per magnitude class; % of IMAD or HBM roofline"
 UNIT = "Gints/s"
-# Integer-multiply lane-ops of one Montgomery multiplication on sm_100a (SASS
-# of csrc/modmath.cuh): 32-bit = IMAD.WIDE.U32 + IMAD +
-# IMAD.HI.U32; 64-bit = 4 IMAD.WIDE.U32 (+.X) for a*b, 3 for m = lo*ninv, 4 for
-# hi(m*n), plus carries = 14.
-IMAD_PER_MULMOD32 = 3
-IMAD_PER_MULMOD64 = 14
-IMAD_LANES_PER_CLK_SM = 64  # FMA-heavy pipe: 16 lanes/clk per SMSP x 4 (B300_MICROARCH.md "Pipe rates")
+# Minimal pipe work of one modular multiplication, in lane-slots of a 16-lane
+# pipe: IMAD.WIDE.U32 and IMAD.HI are half rate on the
+# FMA-heavy pipe (profiles/r1_imad_peak.json: 25.2 / 31.7 vs 63.2 lanes/clk/SM
+# for IMAD), so they count 2 slots.
+#   64-bit Montgomery: 4 WIDE (a*b) + 1 WIDE + 2 IMAD (m) + 4 WIDE (hi(m n)) -> 18 FMA-heavy slots
+#     (a squaring needs 3 WIDE for a^2 -> 16; the multiply count below does not
+#      separate squarings, so 18 is a conservative, i.e. higher, work figure)
+#   32-bit Montgomery: 1 WIDE + 1 IMAD + 1 HI -> 5 FMA-heavy slots
+#   FP64 (n < 2^49): DMUL, DFMA, DMUL, 2 DADD (rounding), DFMA, DADD, DADD -> 8 FP64 lane-ops
+SLOTS_MULMOD64 = 18
+SLOTS_MULMOD32 = 5
+FP64_OPS_MULMOD = 8
+LANES_PER_CLK_SM = 64  # FMA-heavy and FP64 pipes: 16 lanes/clk per SMSP x 4 (B300_MICROARCH.md; measured 63.2 / 63.1)
 HBM_BYTES_PER_ELEM = 9      # 8-B value read + 1-B result written
 
 
@@ -209,20 +215,23 @@ def roofline(kern_ms, stats, n, steps, peaks, peaks_kind, clocks):
         except Exception:
             traffic = None
     if name in ("mr1", "mr2"):
-        mm = stats["mulmods"]
-        if name == "mr1":
-            imad = mm[0] * IMAD_PER_MULMOD32 + mm[1] * IMAD_PER_MULMOD64
-        else:
-            imad = mm[2] * IMAD_PER_MULMOD32 + mm[3] * IMAD_PER_MULMOD64
-        achieved = imad / steps / (ms * 1e-3) / 1e12
+        mm, mf = stats["mulmods"], stats["mulmods_fp64"]
+        k = 0 if name == "mr1" else 2
+        fma_slots = mm[k] * SLOTS_MULMOD32 + mm[k + 1] * SLOTS_MULMOD64
+        fp64_ops = mf[0 if name == "mr1" else 1] * FP64_OPS_MULMOD
+        busiest = max(fma_slots, fp64_ops)
+        achieved = busiest / steps / (ms * 1e-3) / 1e12
         mhz = peaks.get("sm_max_mhz", 1965.0)
-        peak = 148 * IMAD_LANES_PER_CLK_SM * mhz * 1e6 / 1e12
+        peak = 148 * LANES_PER_CLK_SM * mhz * 1e6 / 1e12
         return {"kernel": name, "bound": "alu", "achieved": round(achieved, 4), "peak": round(peak, 3),
-                "unit": "T IMAD-lane-ops/s", "frac": round(achieved / peak, 4), "traffic": traffic,
-                "peak_source": f"derived: 148 SMs x {IMAD_LANES_PER_CLK_SM} IMAD lanes/clk x {mhz:.0f} MHz "
-                               "(B300_MICROARCH.md fma pipe rt=2/SMSP; MEASURED_PEAKS sm_max_mhz)",
-                "work": f"{imad / steps:.4g} algorithmic IMAD per step = mulmods x {IMAD_PER_MULMOD32} (32-bit) "
-                        f"/ {IMAD_PER_MULMOD64} (64-bit)", "ms_per_step": round(ms, 4)}
+                "unit": "T lane-slots/s (busiest of FMA-heavy / FP64 pipe)", "frac": round(achieved / peak, 4),
+                "traffic": traffic,
+                "peak_source": f"derived: 148 SMs x {LANES_PER_CLK_SM} lanes/clk x {mhz:.0f} MHz "
+                               "(B300_MICROARCH.md pipe rates; MEASURED_PEAKS sm_max_mhz)",
+                "work": f"per step: {fma_slots / steps:.4g} FMA-heavy slots ({SLOTS_MULMOD32}/32-bit, {SLOTS_MULMOD64}/64-bit "
+                        f"Montgomery mulmod) and {fp64_ops / steps:.4g} FP64 ops ({FP64_OPS_MULMOD}/mulmod); "
+                        "mulmods = square-and-multiply count of ModExp",
+                "ms_per_step": round(ms, 4)}
     nbytes = HBM_BYTES_PER_ELEM * n
     if name == "sieve":
         nbytes = stats["sieved_integers"] / steps / 16.0 if stats["sieved_integers"] else 0.0

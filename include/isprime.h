@@ -108,7 +108,9 @@ typedef struct {
     uint64_t kernel_launches;        /* kernels launched by the library (host count) */
     uint64_t mulmods[4];             /* algorithmic modular multiplications counted while
                                         "kernel_timing" is 1: mr1 32-bit, mr1 64-bit,
-                                        mr2 32-bit, mr2 64-bit (square-and-multiply count) */
+                                        mr2 32-bit, mr2 64-bit (square-and-multiply count);
+                                        the 64-bit entries count the Montgomery class only */
+    uint64_t mulmods_fp64[2];        /* same for the FP64 class (odd n < 2^49): mr1, mr2 */
 } isprime_stats;
 
 /* Synchronises the current device, copies the accumulated statistics. */

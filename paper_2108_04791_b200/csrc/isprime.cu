@@ -260,6 +260,7 @@ int ensure_queues(Ctx* c, size_t cap) {
     c->q.p32_idx = reinterpret_cast<uint32_t*>(p); p += cap * 4;
     c->q.p32_val = reinterpret_cast<uint32_t*>(p); p += cap * 4;
     c->q.p64_idx = reinterpret_cast<uint32_t*>(p); p += cap * 4;
+    c->q.cap = (unsigned int)cap;
     c->qcap = cap;
     return ISP_OK;
 }
@@ -618,10 +619,12 @@ int isprime_get_stats(isprime_stats* st) {
     st->queued32 = p.total[0] + p.counts[0];
     st->queued64 = p.total[1] + p.counts[1];
     st->passed32 = p.total[2] + p.counts[2];
-    st->passed64 = p.total[3] + p.counts[3];
+    st->passed64 = p.total[3] + p.counts[3] + p.pback;
     st->chunks = p.chunks;
     st->kernel_launches = g_launches;
     for (int k = 0; k < 4; k++) st->mulmods[k] = p.work[k];
+    st->mulmods_fp64[0] = p.work_f[0];
+    st->mulmods_fp64[1] = p.work_f[1];
     return ISP_OK;
 }
 
@@ -638,6 +641,7 @@ int isprime_reset_stats(void) {
     p.sieved_ints = 0;
     p.chunks = 0;
     for (int k = 0; k < 4; k++) p.work[k] = 0;
+    p.work_f[0] = p.work_f[1] = 0;
     p.valid_lo = p.valid_hi = 0;  // forget the bitmap: the next call sieves again
     CK(cudaMemcpy(c->plan, &p, sizeof(p), cudaMemcpyHostToDevice));
     g_launches = 0;

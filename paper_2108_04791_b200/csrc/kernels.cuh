@@ -47,6 +47,9 @@ struct DevPlan {
     // counting sort of the trial-division survivors by bit length (per chunk)
     unsigned int bins32[33], bins64[65], cur32[33], cur64[65];
     unsigned int sorted32, sorted64;
+    unsigned int pback;                     // FP64-class entries of P64 (stored from the back)
+    unsigned int cur1[3], cur2[3];          // dynamic work cursors of mr1 / mr2 (3 regions)
+    unsigned long long work_f[2];           // FP64-class mulmods: mr1, mr2 (work counting)
 };
 
 // Host -> plan kernel parameters (cost model in picoseconds on a full GPU).
@@ -65,7 +68,8 @@ struct Queues {
     uint32_t* s32_idx; uint32_t* s32_val;             // the same entries ordered by bit length
     uint32_t* s64_idx; unsigned long long* s64_val;
     uint32_t* p32_idx; uint32_t* p32_val;             // base-2 strong probable primes -> mr2
-    uint32_t* p64_idx; unsigned long long* p64_val;
+    uint32_t* p64_idx; unsigned long long* p64_val;   // Montgomery class from the front, FP64 class from the back
+    unsigned int cap;                                  // entries per queue
 };
 
 struct TDParams {
@@ -316,6 +320,9 @@ __global__ void __launch_bounds__(PLAN_THREADS) plan_kernel(const unsigned long 
     for (int b = 0; b < 33; b++) { plan->bins32[b] = 0; plan->cur32[b] = 0; }
     for (int b = 0; b < 65; b++) { plan->bins64[b] = 0; plan->cur64[b] = 0; }
     plan->sorted32 = plan->sorted64 = 0;
+    plan->total[3] += plan->pback;  // FP64-class base-2 passes count with the 64-bit ones
+    plan->pback = 0;
+    for (int r = 0; r < 3; r++) { plan->cur1[r] = 0; plan->cur2[r] = 0; }
     plan->chunks += 1;
 }
 
@@ -762,7 +769,7 @@ struct WarpStage {
 
 template <typename T>
 __device__ __forceinline__ void stage_append(bool pred, uint32_t idx, T val, WarpStage<T>& st, unsigned int& n,
-                                             unsigned int* counter, uint32_t* qidx, T* qval) {
+                                             unsigned int* counter, uint32_t* qidx, T* qval, unsigned int rev_cap = 0) {
     const int lane = threadIdx.x & 31;
     const unsigned int mask = __ballot_sync(0xffffffffu, pred);
     if (pred) {
@@ -776,8 +783,9 @@ __device__ __forceinline__ void stage_append(bool pred, uint32_t idx, T val, War
         unsigned int base = 0;
         if (lane == 0) base = atomicAdd(counter, 32u);
         base = __shfl_sync(0xffffffffu, base, 0);
-        qidx[base + lane] = st.idx[lane];
-        qval[base + lane] = st.val[lane];
+        const unsigned int at = rev_cap ? rev_cap - 1 - (base + lane) : base + lane;
+        qidx[at] = st.idx[lane];
+        qval[at] = st.val[lane];
         __syncwarp();
         if (lane + 32 < n) { st.idx[lane] = st.idx[lane + 32]; st.val[lane] = st.val[lane + 32]; }
         n -= 32;
@@ -786,14 +794,43 @@ __device__ __forceinline__ void stage_append(bool pred, uint32_t idx, T val, War
 }
 
 template <typename T>
-__device__ __forceinline__ void stage_flush(WarpStage<T>& st, unsigned int n, unsigned int* counter, uint32_t* qidx,
-                                            T* qval) {
+__device__ __forceinline__ void stage_flush(WarpStage<T>& st, unsigned int& n, unsigned int* counter, uint32_t* qidx,
+                                            T* qval, unsigned int rev_cap = 0) {
     const int lane = threadIdx.x & 31;
     if (!n) return;
     unsigned int base = 0;
     if (lane == 0) base = atomicAdd(counter, n);
     base = __shfl_sync(0xffffffffu, base, 0);
-    if ((unsigned int)lane < n) { qidx[base + lane] = st.idx[lane]; qval[base + lane] = st.val[lane]; }
+    if ((unsigned int)lane < n) {
+        const unsigned int at = rev_cap ? rev_cap - 1 - (base + lane) : base + lane;
+        qidx[at] = st.idx[lane];
+        qval[at] = st.val[lane];
+    }
+    n = 0;
+    __syncwarp();
+}
+
+// Dynamic work over three regions (the 32-bit Montgomery, FP64 and 64-bit
+// Montgomery classes).  Warps start on region (warp id mod 3) and move on when
+// it is drained, so at any moment an SM holds warps of every class: the
+// FP64 pipe and the FMA-heavy (IMAD) pipe work side by side instead of one
+// class after the other.  Chunks of MR_CHUNK entries per atomicAdd.
+constexpr unsigned int MR_CHUNK = 256;
+
+__device__ __forceinline__ bool next_chunk(const unsigned int (&size)[3], unsigned int* cur, int& r, int& tried,
+                                           unsigned int& start) {
+    const int lane = threadIdx.x & 31;
+    while (tried != 7) {
+        if (!((tried >> r) & 1)) {
+            unsigned int s0 = 0xFFFFFFFFu;
+            if (size[r] && lane == 0) s0 = atomicAdd(&cur[r], MR_CHUNK);
+            s0 = __shfl_sync(0xffffffffu, s0, 0);
+            if (s0 < size[r]) { start = s0; return true; }
+            tried |= 1 << r;
+        }
+        r = r == 2 ? 0 : r + 1;
+    }
+    return false;
 }
 
 __device__ __forceinline__ unsigned long long warp_sum(unsigned long long v) {
@@ -808,58 +845,77 @@ __device__ __forceinline__ unsigned int modexp_squarings(unsigned long long d) {
 __device__ __forceinline__ unsigned int modexp_mults(unsigned long long d) { return __popcll(d) - 1; }
 __device__ __forceinline__ unsigned long long odd_part(unsigned long long n) { return (n - 1) >> (__ffsll((long long)(n - 1)) - 1); }
 
+__device__ __forceinline__ unsigned int fp_class_count(const DevPlan* plan) {
+    if (!plan->sorted64) return 0u;
+    unsigned int c = 0;
+    for (int b = 0; b <= 49; b++) c += plan->bins64[b];  // bit length <= 49 <=> n < 2^49
+    return c;
+}
+
 __global__ void __launch_bounds__(MR_THREADS)
 mr1_kernel(DevPlan* __restrict__ plan, Queues q, int count_work) {
     __shared__ WarpStage<uint32_t> st32[MR_THREADS / 32];
-    __shared__ WarpStage<unsigned long long> st64[MR_THREADS / 32];
-    const unsigned int c32 = plan->counts[0], c64 = plan->counts[1];
+    __shared__ WarpStage<unsigned long long> st64i[MR_THREADS / 32], st64f[MR_THREADS / 32];
+    __shared__ unsigned int s_nf;
+    if (threadIdx.x == 0) s_nf = fp_class_count(plan);
+    __syncthreads();
+    const unsigned int c32 = plan->counts[0], c64 = plan->counts[1], nf = s_nf;
     const uint32_t* q32i = plan->sorted32 ? q.s32_idx : q.q32_idx;
     const uint32_t* q32v = plan->sorted32 ? q.s32_val : q.q32_val;
     const uint32_t* q64i = plan->sorted64 ? q.s64_idx : q.q64_idx;
     const unsigned long long* q64v = plan->sorted64 ? q.s64_val : q.q64_val;
-    unsigned long long w32 = 0, w64 = 0;
+    // regions: 0 = Q32, 1 = FP64 class = sorted Q64 [0, nf), 2 = the rest of Q64
+    const unsigned int size[3] = {c32, nf, c64 - nf};
+    unsigned long long w32 = 0, w64 = 0, wf = 0;
     const unsigned int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
-    const unsigned int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-    const unsigned int nwarps = (gridDim.x * blockDim.x) >> 5;
-    unsigned int ns = 0;
-    for (unsigned int b = warp * 32; b < c32; b += nwarps * 32) {
-        const unsigned int i = b + lane;
-        bool pass = false;
-        uint32_t n = 0, idx = 0;
-        if (i < c32) {
-            n = q32v[i];
-            idx = q32i[i];
-            pass = sprp2_32(n);
-            if (count_work) w32 += modexp_squarings(odd_part(n));
+    const unsigned int gwarp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    int r = (int)(gwarp % 3u), tried = 0;
+    unsigned int start = 0, n32s = 0, n64i = 0, n64f = 0;
+    while (next_chunk(size, plan->cur1, r, tried, start)) {
+        const unsigned int end = min(start + MR_CHUNK, size[r]);
+        for (unsigned int b = start; b < end; b += 32) {
+            const unsigned int i = b + lane;
+            const bool act = i < end;
+            if (r == 0) {
+                bool pass = false;
+                uint32_t n = 0, idx = 0;
+                if (act) {
+                    n = q32v[i];
+                    idx = q32i[i];
+                    pass = sprp2_32(n);
+                    if (count_work) w32 += modexp_squarings(odd_part(n));
+                }
+                stage_append<uint32_t>(pass, idx, n, st32[wib], n32s, &plan->counts[2], q.p32_idx, q.p32_val);
+            } else {
+                const unsigned int k = r == 1 ? i : nf + i;
+                bool pass = false, fp = false;
+                unsigned long long n = 0;
+                uint32_t idx = 0;
+                if (act) {
+                    n = q64v[k];
+                    idx = q64i[k];
+                    // magnitude-class dispatch: below 2^49 on the FP64 pipe, above with
+                    // 64-bit Montgomery (uniform per region when the queue is sorted)
+                    fp = n < FP_LIMIT;
+                    pass = fp ? sprp2_f64(n) : sprp2_64(n);
+                    if (count_work) { if (fp) wf += modexp_squarings(odd_part(n)); else w64 += modexp_squarings(odd_part(n)); }
+                }
+                stage_append<unsigned long long>(pass && !fp, idx, n, st64i[wib], n64i, &plan->counts[3], q.p64_idx, q.p64_val);
+                stage_append<unsigned long long>(pass && fp, idx, n, st64f[wib], n64f, &plan->pback, q.p64_idx, q.p64_val, q.cap);
+            }
         }
-        stage_append<uint32_t>(pass, idx, n, st32[wib], ns, &plan->counts[2], q.p32_idx, q.p32_val);
     }
-    stage_flush<uint32_t>(st32[wib], ns, &plan->counts[2], q.p32_idx, q.p32_val);
-    ns = 0;
-    for (unsigned int b = warp * 32; b < c64; b += nwarps * 32) {
-        const unsigned int i = b + lane;
-        bool pass = false;
-        unsigned long long n = 0;
-        uint32_t idx = 0;
-        if (i < c64) {
-            n = q64v[i];
-            idx = q64i[i];
-        }
-        // magnitude-class dispatch: below 2^49 on the FP64 pipe, above with
-        // 64-bit Montgomery (warp-uniform on the bit-length-sorted queue)
-        if (i < c64) {
-            pass = n < FP_LIMIT ? sprp2_f64(n) : sprp2_64(n);
-            if (count_work) w64 += modexp_squarings(odd_part(n));
-        }
-        stage_append<unsigned long long>(pass, idx, n, st64[wib], ns, &plan->counts[3], q.p64_idx, q.p64_val);
-    }
-    stage_flush<unsigned long long>(st64[wib], ns, &plan->counts[3], q.p64_idx, q.p64_val);
+    stage_flush<uint32_t>(st32[wib], n32s, &plan->counts[2], q.p32_idx, q.p32_val);
+    stage_flush<unsigned long long>(st64i[wib], n64i, &plan->counts[3], q.p64_idx, q.p64_val);
+    stage_flush<unsigned long long>(st64f[wib], n64f, &plan->pback, q.p64_idx, q.p64_val, q.cap);
     if (count_work) {
         w32 = warp_sum(w32);
         w64 = warp_sum(w64);
+        wf = warp_sum(wf);
         if (lane == 0) {
             if (w32) atomicAdd(&plan->work[0], w32);
             if (w64) atomicAdd(&plan->work[1], w64);
+            if (wf) atomicAdd(&plan->work_f[0], wf);
         }
     }
 }
@@ -868,34 +924,48 @@ mr1_kernel(DevPlan* __restrict__ plan, Queues q, int count_work) {
 template <int WIN, bool FULL32, int G64>
 __global__ void __launch_bounds__(MR_THREADS)
 mr2_kernel(DevPlan* __restrict__ plan, Queues q, uint8_t* __restrict__ out, int count_work) {
-    const unsigned int c32 = plan->counts[2], c64 = plan->counts[3];
-    unsigned long long w32 = 0, w64 = 0;
-    const unsigned int stride = gridDim.x * blockDim.x;
-    const unsigned int t0 = blockIdx.x * blockDim.x + threadIdx.x;
-    for (unsigned int i = t0; i < c32; i += stride) {
-        const uint32_t n = q.p32_val[i];
-        const bool prime = FULL32 ? sprp_multi32<6>(n, c_bases32_full) : sprp_multi32<2>(n, c_bases32_red);
-        if (prime) out[q.p32_idx[i]] = 1;
-        if (count_work) {
-            const unsigned long long d = odd_part(n);
-            w32 += (unsigned long long)(FULL32 ? 6 : 2) * (modexp_squarings(d) + modexp_mults(d));
-        }
-    }
-    for (unsigned int i = t0; i < c64; i += stride) {
-        const unsigned long long n = q.p64_val[i];
-        const bool prime = n < FP_LIMIT ? sprp_multi_f64<6, G64, WIN>(n, c_bases64) : sprp_multi64<6, G64, WIN>(n, c_bases64);
-        if (prime) out[q.p64_idx[i]] = 1;
-        if (count_work) {
-            const unsigned long long d = odd_part(n);
-            w64 += 6ull * (modexp_squarings(d) + modexp_mults(d));
+    // regions: 0 = P32, 1 = FP64 class (back of P64), 2 = Montgomery class (front of P64)
+    const unsigned int size[3] = {plan->counts[2], plan->pback, plan->counts[3]};
+    unsigned long long w32 = 0, w64 = 0, wf = 0;
+    const unsigned int lane = threadIdx.x & 31;
+    const unsigned int gwarp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    int r = (int)(gwarp % 3u), tried = 0;
+    unsigned int start = 0;
+    while (next_chunk(size, plan->cur2, r, tried, start)) {
+        const unsigned int end = min(start + MR_CHUNK, size[r]);
+        for (unsigned int b = start; b < end; b += 32) {
+            const unsigned int i = b + lane;
+            if (i >= end) continue;
+            if (r == 0) {
+                const uint32_t n = q.p32_val[i];
+                const bool prime = FULL32 ? sprp_multi32<6>(n, c_bases32_full) : sprp_multi32<2>(n, c_bases32_red);
+                if (prime) out[q.p32_idx[i]] = 1;
+                if (count_work) {
+                    const unsigned long long d = odd_part(n);
+                    w32 += (unsigned long long)(FULL32 ? 6 : 2) * (modexp_squarings(d) + modexp_mults(d));
+                }
+            } else {
+                const unsigned int k = r == 1 ? q.cap - 1 - i : i;
+                const unsigned long long n = q.p64_val[k];
+                const bool fp = n < FP_LIMIT;
+                const bool prime = fp ? sprp_multi_f64<6, G64, WIN>(n, c_bases64) : sprp_multi64<6, G64, WIN>(n, c_bases64);
+                if (prime) out[q.p64_idx[k]] = 1;
+                if (count_work) {
+                    const unsigned long long d = odd_part(n);
+                    const unsigned long long w = 6ull * (modexp_squarings(d) + modexp_mults(d));
+                    if (fp) wf += w; else w64 += w;
+                }
+            }
         }
     }
     if (count_work) {
         w32 = warp_sum(w32);
         w64 = warp_sum(w64);
-        if ((threadIdx.x & 31) == 0) {
+        wf = warp_sum(wf);
+        if (lane == 0) {
             if (w32) atomicAdd(&plan->work[2], w32);
             if (w64) atomicAdd(&plan->work[3], w64);
+            if (wf) atomicAdd(&plan->work_f[1], wf);
         }
     }
 }
