@@ -273,7 +273,9 @@ int sort_grid(int full, uint32_t len) {
 
 // Persistent MR grids never need more blocks than the chunk could queue.
 int mr_grid(int full, uint32_t len) {
-    const uint32_t need = (len + MR_THREADS - 1) / MR_THREADS;
+    // dynamic chunks of MR_CHUNK entries: more warps than len / MR_CHUNK would
+    // only contend on the work cursors
+    const uint32_t need = (len + MR_THREADS * 8 - 1) / (MR_THREADS * 8);
     return (int)(need < (uint32_t)full ? need : (uint32_t)full);
 }
 

@@ -197,20 +197,28 @@ __global__ void __launch_bounds__(PLAN_THREADS) plan_kernel(const unsigned long 
     unsigned long long lmin = ~0ull, lmax = 0;
     unsigned int lin = 0, lcnt = 0;
     if (P.force == 0) {
-        constexpr int PER = PLAN_SAMPLES / PLAN_THREADS;
+        // PLAN_SAMPLES / 8 strata, 8 consecutive elements from a pseudo-random
+        // offset in each: one cache line per stratum, and few enough distinct
+        // 2 MB pages that one SM's TLB walks stay cheap on multi-GB arrays.
+        constexpr int PER = PLAN_SAMPLES / PLAN_THREADS;   // 16 = 2 strata x 8
+        const unsigned long long NS = (S + 7) / 8;          // strata
         unsigned long long v[PER];
 #pragma unroll
-        for (int r = 0; r < PER; r++) {  // independent loads, all in flight together
+        for (int r = 0; r < PER / 8; r++) {
             const unsigned long long k = (unsigned long long)tid + (unsigned long long)r * PLAN_THREADS;
-            v[r] = 0;
-            if (k < S) {
-                const unsigned long long lo = (k * len) / S, hi = ((k + 1) * len) / S;  // stratum [lo, hi)
+            unsigned long long at = 0, avail = 0;
+            if (k < NS) {
+                const unsigned long long lo = (k * len) / NS, hi = ((k + 1) * len) / NS;  // stratum [lo, hi)
                 unsigned int h = (unsigned int)k * 0x9E3779B1u;
                 h ^= h >> 15;
                 h *= 0x2C1B3C6Du;
                 h ^= h >> 12;
-                v[r] = N[lo + (hi > lo ? h % (unsigned int)(hi - lo) : 0u)];
+                const unsigned long long span = hi - lo;
+                at = lo + (span > 8 ? h % (unsigned int)(span - 7) : 0u);
+                avail = span < 8 ? span : 8;
             }
+#pragma unroll
+            for (int e = 0; e < 8; e++) v[8 * r + e] = (unsigned long long)e < avail ? N[at + e] : 0ull;
         }
 #pragma unroll
         for (int r = 0; r < PER; r++) {
@@ -424,54 +432,33 @@ sieve_kernel(const DevPlan* __restrict__ plan, uint32_t* __restrict__ bitmap,
 }
 
 // ------------------------------------------------------------- A2: classify
-// One streaming pass over N, 2048-element tiles per block iteration.
-// Per element v (PAPER.md:11-20 semantics):
+// One streaming pass over N; each warp owns a 256-element warp-tile (lane l:
+// element pairs 2l + 64j, j < 4: every load instruction reads 512 contiguous
+// bytes), a block 8 warp-tiles.  Per element v (PAPER.md:11-20 semantics):
 //   v < 2 -> 0;  v even -> (v == 2);  wlo <= v < whi -> bit of the sieve
 //   (membership instead of division);
 //   v < 2^32: composite if an odd prime p among the first N32 divides it
 //             (v != p), prime if no such p and v < (next prime)^2, else -> Q32;
 //   v >= 2^32: composite if one of the first N64 odd primes divides it, else -> Q64
 // ("shrinking the input array", generalised to N primes).
-// Mixed-magnitude tiles would make a warp run both the 32- and the 64-bit
-// trial-division loops for every element slot, so the tile is first compacted
-// by class in shared memory (block scan), then every thread runs the uniform
-// loops over dense lists.  Survivors leave through one atomicAdd per class per
-// tile; out[] is written for every element from the shared-memory result tile.
-struct ClsSmem {
-    unsigned long long val[CLS_TILE];  // list32 grows up from 0, list64 down from CLS_TILE-1
-    unsigned short pos[CLS_TILE];      // tile-local index; bit 15 = survivor
-    uint8_t res[CLS_TILE];
-    uint32_t warp_tot[CLS_THREADS / 32];
-    uint32_t base32, base64, tot;
+// Mixed magnitudes would make a warp run both trial-division loops for every
+// element slot, so each warp first compacts its candidates by class into
+// warp-private shared-memory lists (ballot / shuffle scan, no block barrier)
+// and runs uniform loops over the dense lists.  A warp with no candidate (a
+// dense sieve window, config C4) stores its results straight from registers.
+// Survivors reserve queue space once per block tile: one __syncthreads_or,
+// then warp 0 scans the 8 warp counts and issues one atomicAdd per class.
+struct ClsWarp {
+    unsigned long long val[256];  // list32 from the front (low 32 bits used), list64 from the back
+    uint8_t pos[256];             // element offset within the warp-tile
+    uint8_t res[256];             // results of the warp-tile, element order
+    uint32_t surv[16];            // survivor bit per list slot: [0..8) list32, [8..16) list64 (by back index)
 };
-
-// Block-wide exclusive scan of a packed (lo16, hi16) count pair; returns the
-// exclusive prefix, *total gets the block total.  Contains __syncthreads.
-__device__ __forceinline__ uint32_t block_scan_pair(uint32_t packed, ClsSmem& sm, uint32_t* total) {
-    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
-    uint32_t incl = packed;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-        const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
-        if (lane >= o) incl += y;
-    }
-    if (lane == 31) sm.warp_tot[wid] = incl;
-    __syncthreads();
-    if (wid == 0) {
-        const uint32_t t = lane < CLS_THREADS / 32 ? sm.warp_tot[lane] : 0u;
-        uint32_t ti = t;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            const uint32_t y = __shfl_up_sync(0xffffffffu, ti, o);
-            if (lane >= o) ti += y;
-        }
-        if (lane < CLS_THREADS / 32) sm.warp_tot[lane] = ti - t;
-        if (lane == CLS_THREADS / 32 - 1) sm.tot = ti;
-    }
-    __syncthreads();
-    *total = sm.tot;
-    return sm.warp_tot[wid] + incl - packed;
-}
+struct ClsSmem {
+    ClsWarp w[CLS_THREADS / 32];
+    uint32_t cnt[CLS_THREADS / 32][2];
+    uint32_t base[CLS_THREADS / 32][2];
+};
 
 template <int N32, int N64>
 __global__ void __launch_bounds__(CLS_THREADS)
@@ -480,33 +467,34 @@ classify_kernel(const unsigned long long* __restrict__ N, uint8_t* __restrict__ 
                 int vec_in, int vec_out) {
     __shared__ ClsSmem sm;
     const unsigned long long wlo = plan->wlo, whi = plan->whi;
-    const int tid = threadIdx.x;
+    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+    ClsWarp& ws = sm.w[wid];
     const uint32_t ntiles = (len + CLS_TILE - 1) / CLS_TILE;
     for (uint32_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-        const uint32_t tbase = tile * CLS_TILE;
-        const bool full = tbase + CLS_TILE <= len;
-        // ---- phase A: load, trivial cases, window gather, class
-        unsigned long long v[2 * CLS_PAIRS];
+        const uint32_t wbase = tile * CLS_TILE + 256u * wid;
+        const bool full = wbase + 256u <= len;
+        // ---- load, trivial cases, window gather, class
+        unsigned long long v[8];
         if (vec_in && full) {
 #pragma unroll
-            for (int j = 0; j < CLS_PAIRS; j++) {
-                const ulonglong2 t = __ldcs(reinterpret_cast<const ulonglong2*>(N + tbase + 2 * tid + 2 * CLS_THREADS * j));
+            for (int j = 0; j < 4; j++) {
+                const ulonglong2 t = __ldcs(reinterpret_cast<const ulonglong2*>(N + wbase + 2 * lane + 64 * j));
                 v[2 * j] = t.x;
                 v[2 * j + 1] = t.y;
             }
         } else {
 #pragma unroll
-            for (int e = 0; e < 2 * CLS_PAIRS; e++) {
-                const uint32_t i = tbase + 2 * tid + 2 * CLS_THREADS * (e >> 1) + (e & 1);
+            for (int e = 0; e < 8; e++) {
+                const uint32_t i = wbase + 2 * lane + 64 * (e >> 1) + (e & 1);
                 v[e] = i < len ? N[i] : 0ull;
             }
         }
-        uint32_t c32 = 0, c64 = 0, clsbits = 0;  // 2 bits per element: 1 -> 32-bit list, 2 -> 64-bit list
-        uint8_t r[2 * CLS_PAIRS];
+        uint32_t c32 = 0, c64 = 0, clsbits = 0;  // 2 bits per element: 1 -> list32, 2 -> list64
+        uint8_t r[8];
 #pragma unroll
-        for (int e = 0; e < 2 * CLS_PAIRS; e++) {
+        for (int e = 0; e < 8; e++) {
             const unsigned long long x = v[e];
-            const uint32_t i = tbase + 2 * tid + 2 * CLS_THREADS * (e >> 1) + (e & 1);
+            const uint32_t i = wbase + 2 * lane + 64 * (e >> 1) + (e & 1);
             uint32_t cls = 0;
             uint8_t rr = 0;
             if (x < 2ull) rr = 0;
@@ -521,86 +509,137 @@ classify_kernel(const unsigned long long* __restrict__ N, uint8_t* __restrict__ 
             c64 += cls == 2;
             clsbits |= cls << (2 * e);
         }
-        if (!__syncthreads_or((int)(c32 | c64))) {
-            // fast path: nothing in this tile needs trial division (e.g. the whole
-            // tile is inside the sieve window) -- results straight from registers
+        // warp scan of the packed (c32, c64) counts
+        const uint32_t packed = c32 | (c64 << 16);
+        uint32_t incl = packed;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= o) incl += y;
+        }
+        const uint32_t wtot = __shfl_sync(0xffffffffu, incl, 31);
+        const uint32_t n32 = wtot & 0xFFFFu, n64 = wtot >> 16;
+        uint32_t s32 = 0, s64 = 0;
+        if (wtot == 0) {
+            // warp fast path: results straight from registers
             if (full && vec_out) {
 #pragma unroll
-                for (int j = 0; j < CLS_PAIRS; j++)
-                    __stcs(reinterpret_cast<unsigned short*>(out + tbase + 2 * tid + 2 * CLS_THREADS * j),
+                for (int j = 0; j < 4; j++)
+                    __stcs(reinterpret_cast<unsigned short*>(out + wbase + 2 * lane + 64 * j),
                            (unsigned short)(r[2 * j] | (r[2 * j + 1] << 8)));
             } else {
 #pragma unroll
-                for (int e = 0; e < 2 * CLS_PAIRS; e++) {
-                    const uint32_t i = tbase + 2 * tid + 2 * CLS_THREADS * (e >> 1) + (e & 1);
+                for (int e = 0; e < 8; e++) {
+                    const uint32_t i = wbase + 2 * lane + 64 * (e >> 1) + (e & 1);
                     if (i < len) out[i] = r[e];
                 }
             }
-            continue;
-        }
+        } else {
 #pragma unroll
-        for (int j = 0; j < CLS_PAIRS; j++)
-            *reinterpret_cast<unsigned short*>(sm.res + 2 * tid + 2 * CLS_THREADS * j) =
-                (unsigned short)(r[2 * j] | (r[2 * j + 1] << 8));
-        {
-            uint32_t tot;
-            const uint32_t ex = block_scan_pair(c32 | (c64 << 16), sm, &tot);
+            for (int j = 0; j < 4; j++)
+                *reinterpret_cast<unsigned short*>(ws.res + 2 * lane + 64 * j) = (unsigned short)(r[2 * j] | (r[2 * j + 1] << 8));
+            const uint32_t ex = incl - packed;
             uint32_t p32 = ex & 0xFFFFu, p64 = ex >> 16;
-            const uint32_t n32 = tot & 0xFFFFu, n64 = tot >> 16;
 #pragma unroll
-            for (int e = 0; e < 2 * CLS_PAIRS; e++) {
+            for (int e = 0; e < 8; e++) {
                 const uint32_t cls = (clsbits >> (2 * e)) & 3u;
-                const unsigned short lp = (unsigned short)(2 * tid + 2 * CLS_THREADS * (e >> 1) + (e & 1));
-                if (cls == 1) { sm.val[p32] = v[e]; sm.pos[p32] = lp; p32++; }
-                else if (cls == 2) { const uint32_t k = CLS_TILE - 1 - p64; sm.val[k] = v[e]; sm.pos[k] = lp; p64++; }
+                const uint8_t lp = (uint8_t)(2 * lane + 64 * (e >> 1) + (e & 1));
+                if (cls == 1) { ws.val[p32] = v[e]; ws.pos[p32] = lp; p32++; }
+                else if (cls == 2) { const uint32_t k = 255u - p64; ws.val[k] = v[e]; ws.pos[k] = lp; p64++; }
+            }
+            __syncwarp();
+            // ---- trial division over the dense lists
+            for (uint32_t k0 = 0; k0 < n32; k0 += 32) {
+                const uint32_t k = k0 + lane;
+                bool surv = false;
+                if (k < n32) {
+                    const uint32_t x = (uint32_t)ws.val[k];
+                    bool comp = false;
+#pragma unroll
+                    for (int t = 0; t < N32; t++) comp |= (x * c_td_inv32[t] <= c_td_lim32[t]) && (x != c_td_p[t]);
+                    if (!comp) {
+                        if (x < td.sq32) ws.res[ws.pos[k]] = 1;
+                        else surv = true;
+                    }
+                }
+                const uint32_t m = __ballot_sync(0xffffffffu, surv);
+                if (lane == 0) ws.surv[k0 >> 5] = m;
+                s32 += __popc(m);
+            }
+            for (uint32_t k0 = 0; k0 < n64; k0 += 32) {
+                const uint32_t k = k0 + lane;  // back index: slot 255 - k
+                bool surv = false;
+                if (k < n64) {
+                    const unsigned long long x = ws.val[255u - k];
+                    bool comp = false;
+#pragma unroll
+                    for (int t = 0; t < N64; t++) comp |= (x * c_td_inv64[t] <= c_td_lim64[t]);
+                    surv = !comp;
+                }
+                const uint32_t m = __ballot_sync(0xffffffffu, surv);
+                if (lane == 0) ws.surv[8 + (k0 >> 5)] = m;
+                s64 += __popc(m);
+            }
+        }
+        // ---- queue reservation: one barrier (two if this block tile has survivors)
+        if (lane == 0) { sm.cnt[wid][0] = s32; sm.cnt[wid][1] = s64; }
+        if (__syncthreads_or((int)(s32 | s64))) {
+            if (wid == 0) {
+                const uint32_t a32 = lane < CLS_THREADS / 32 ? sm.cnt[lane][0] : 0u;
+                const uint32_t a64 = lane < CLS_THREADS / 32 ? sm.cnt[lane][1] : 0u;
+                uint32_t i32 = a32, i64 = a64;
+#pragma unroll
+                for (int o = 1; o < CLS_THREADS / 32; o <<= 1) {
+                    const uint32_t y32 = __shfl_up_sync(0xffffffffu, i32, o);
+                    const uint32_t y64 = __shfl_up_sync(0xffffffffu, i64, o);
+                    if (lane >= o) { i32 += y32; i64 += y64; }
+                }
+                const uint32_t t32 = __shfl_sync(0xffffffffu, i32, CLS_THREADS / 32 - 1);
+                const uint32_t t64 = __shfl_sync(0xffffffffu, i64, CLS_THREADS / 32 - 1);
+                uint32_t g32 = 0, g64 = 0;
+                if (lane == 0) {
+                    g32 = t32 ? atomicAdd(&plan->counts[0], t32) : 0u;
+                    g64 = t64 ? atomicAdd(&plan->counts[1], t64) : 0u;
+                }
+                g32 = __shfl_sync(0xffffffffu, g32, 0);
+                g64 = __shfl_sync(0xffffffffu, g64, 0);
+                if (lane < CLS_THREADS / 32) { sm.base[lane][0] = g32 + i32 - a32; sm.base[lane][1] = g64 + i64 - a64; }
             }
             __syncthreads();
-            // ---- phase B: trial division over the dense lists
-            uint32_t s32 = 0, s64 = 0;
-            for (uint32_t k = tid; k < n32; k += CLS_THREADS) {
-                const uint32_t x = (uint32_t)sm.val[k];
-                bool comp = false;
-#pragma unroll
-                for (int t = 0; t < N32; t++) comp |= (x * c_td_inv32[t] <= c_td_lim32[t]) && (x != c_td_p[t]);
-                if (!comp) {
-                    if (x < td.sq32) sm.res[sm.pos[k]] = 1;
-                    else { sm.pos[k] |= 0x8000u; s32++; }
+            if (s32 | s64) {
+                uint32_t o32 = sm.base[wid][0], o64 = sm.base[wid][1];
+                for (uint32_t k0 = 0; k0 < n32; k0 += 32) {
+                    const uint32_t m = ws.surv[k0 >> 5];
+                    const uint32_t k = k0 + lane;
+                    if ((m >> lane) & 1u) {
+                        const uint32_t at = o32 + __popc(m & ((1u << lane) - 1u));
+                        q.q32_idx[at] = wbase + ws.pos[k];
+                        q.q32_val[at] = (uint32_t)ws.val[k];
+                    }
+                    o32 += __popc(m);
+                }
+                for (uint32_t k0 = 0; k0 < n64; k0 += 32) {
+                    const uint32_t m = ws.surv[8 + (k0 >> 5)];
+                    const uint32_t k = k0 + lane;
+                    if ((m >> lane) & 1u) {
+                        const uint32_t at = o64 + __popc(m & ((1u << lane) - 1u));
+                        q.q64_idx[at] = wbase + ws.pos[255u - k];
+                        q.q64_val[at] = ws.val[255u - k];
+                    }
+                    o64 += __popc(m);
                 }
             }
-            for (int k = CLS_TILE - 1 - tid; k >= CLS_TILE - (int)n64; k -= CLS_THREADS) {
-                const unsigned long long x = sm.val[k];
-                bool comp = false;
-#pragma unroll
-                for (int t = 0; t < N64; t++) comp |= (x * c_td_inv64[t] <= c_td_lim64[t]);
-                if (!comp) { sm.pos[k] |= 0x8000u; s64++; }
-            }
-            // ---- phase C: survivors -> global queues (one atomicAdd per class per tile)
-            uint32_t stot;
-            const uint32_t sex = block_scan_pair(s32 | (s64 << 16), sm, &stot);
-            if (tid == 0) {
-                const uint32_t t32 = stot & 0xFFFFu, t64 = stot >> 16;
-                sm.base32 = t32 ? atomicAdd(&plan->counts[0], t32) : 0u;
-                sm.base64 = t64 ? atomicAdd(&plan->counts[1], t64) : 0u;
-            }
-            __syncthreads();
-            uint32_t o32 = sm.base32 + (sex & 0xFFFFu), o64 = sm.base64 + (sex >> 16);
-            for (uint32_t k = tid; k < n32; k += CLS_THREADS) {
-                const unsigned short ps = sm.pos[k];
-                if (ps & 0x8000u) { q.q32_idx[o32] = tbase + (ps & 0x7FFFu); q.q32_val[o32] = (uint32_t)sm.val[k]; o32++; }
-            }
-            for (int k = CLS_TILE - 1 - tid; k >= CLS_TILE - (int)n64; k -= CLS_THREADS) {
-                const unsigned short ps = sm.pos[k];
-                if (ps & 0x8000u) { q.q64_idx[o64] = tbase + (ps & 0x7FFFu); q.q64_val[o64] = sm.val[k]; o64++; }
+        }
+        // ---- results of a warp that took the list path: shared tile -> out
+        if (wtot != 0) {
+            __syncwarp();
+            if (full && vec_out) {
+                __stcs(reinterpret_cast<uint2*>(out + wbase) + lane, *reinterpret_cast<const uint2*>(ws.res + 8 * lane));
+            } else {
+                for (uint32_t k = lane; k < 256u; k += 32)
+                    if (wbase + k < len) out[wbase + k] = ws.res[k];
             }
         }
-        // ---- phase D: results tile -> out (8 bytes per thread, coalesced)
-        if (vec_out && full) {
-            __stcs(reinterpret_cast<uint2*>(out + tbase) + tid, *reinterpret_cast<const uint2*>(sm.res + 8 * tid));
-        } else {
-            for (uint32_t k = tid; k < CLS_TILE; k += CLS_THREADS)
-                if (tbase + k < len) out[tbase + k] = sm.res[k];
-        }
-        __syncthreads();  // shared tile reused by the next iteration
     }
 }
 
