@@ -25,7 +25,7 @@ namespace {
 struct Options {
     int force_path = 0;      // 0 auto, 1 sieve, 2 mr
     int bases32 = 3;         // 3 -> {2,7,61}; 7 -> full Eq 4 set
-    int td32 = 24;           // odd primes 3..97
+    int td32 = 16;           // odd primes 3..59 (profiles: C2 best at 16)
     int td64 = 24;
     int chunk_log2 = 28;
     int win64 = 2;
