@@ -92,6 +92,87 @@ __constant__ unsigned long long c_bases64[6] = {325ull, 9375ull, 28178ull, 45077
 __constant__ uint32_t c_bases32_full[6] = {325u, 9375u, 28178u, 450775u, 9780504u, 1795265022u};
 __constant__ uint32_t c_bases32_red[2] = {7u, 61u};
 
+// ---- trial division of 64-bit values on the FP64 pipe --------------------
+// The IMAD-based test (v * p^-1 mod 2^64 <= lim) costs one IMAD.WIDE and two
+// IMAD per prime on the FMA-heavy pipe, which the 64-bit witness kernels also
+// saturate.  Instead, residues modulo products M of consecutive odd primes
+// (M < 2^21) are formed in double precision, exactly:
+//   y = x_hi * (2^32 mod M) + x_lo  < 2^53  (one DFMA), y == x (mod M)
+//   q = round(y / M) (one DFMA with the 1.5 * 2^52 addend), r = y - q M + M in (0, 2M)
+// and each prime p | M is tested on the 32-bit r with one IMAD.
+constexpr uint32_t kOddPrimes[32] = {3, 5, 7, 11, 13, 17, 19, 23, 29, 31, 37, 41, 43, 47, 53, 59,
+                                     61, 67, 71, 73, 79, 83, 89, 97, 101, 103, 107, 109, 113, 127, 131, 137};
+constexpr uint64_t kGroupLimit = 1ull << 21;
+
+// index of the first prime of group g when the first `np` odd primes are grouped greedily
+__host__ __device__ constexpr int group_start(int np, int g) {
+    int i = 0;
+    for (int k = 0; k < g && i < np; k++) {
+        uint64_t m = 1;
+        while (i < np && m * kOddPrimes[i] < kGroupLimit) { m *= kOddPrimes[i]; i++; }
+    }
+    return i;
+}
+__host__ __device__ constexpr int group_count(int np) {
+    int g = 0;
+    while (group_start(np, g) < np) g++;
+    return g;
+}
+__host__ __device__ constexpr uint32_t group_modulus(int np, int g) {
+    uint64_t m = 1;
+    for (int i = group_start(np, g); i < group_start(np, g + 1); i++) m *= kOddPrimes[i];
+    return (uint32_t)m;
+}
+__host__ __device__ constexpr uint32_t inv32_c(uint32_t p) {
+    uint32_t x = (p * 3u) ^ 2u;
+    x *= 2u - p * x;
+    x *= 2u - p * x;
+    x *= 2u - p * x;
+    return x;
+}
+
+__device__ __forceinline__ double u32_to_f64(uint32_t v) {
+    return __hiloint2double(0x43300000, (int)v) - 4503599627370496.0;  // exact: (2^52 + v) - 2^52
+}
+
+// primes [I, HI) of a group, tested on the 32-bit residue r (template recursion
+// keeps every constant an immediate)
+template <int I, int HI>
+__device__ __forceinline__ bool td_primes(uint32_t r) {
+    if constexpr (I >= HI) {
+        return false;
+    } else {
+        constexpr uint32_t p = kOddPrimes[I];
+        constexpr uint32_t inv = inv32_c(p);
+        constexpr uint32_t lim = 0xFFFFFFFFu / p;
+        return (r * inv <= lim) | td_primes<I + 1, HI>(r);
+    }
+}
+
+template <int NP, int G>
+__device__ __forceinline__ bool td_groups(double xh, double xl) {
+    if constexpr (G >= group_count(NP)) {
+        return false;
+    } else {
+        constexpr uint32_t M = group_modulus(NP, G);
+        constexpr double Md = (double)M;
+        constexpr double c = (double)(uint32_t)((1ull << 32) % M);
+        constexpr double inv = 1.0 / (double)M;
+        const double y = fma(xh, c, xl);                                        // == x (mod M), < 2^53
+        const double q = fma(y, inv, 6755399441055744.0) - 6755399441055744.0;  // round(y / M)
+        const double r = fma(-q, Md, y) + Md;                                   // in (0, 2M)
+        const uint32_t ri = (uint32_t)__double2loint(r + 4503599627370496.0);
+        return td_primes<group_start(NP, G), group_start(NP, G + 1)>(ri) | td_groups<NP, G + 1>(xh, xl);
+    }
+}
+
+template <int NP>
+__device__ __forceinline__ bool td64_fp(unsigned long long x) {
+    const double xh = u32_to_f64((uint32_t)(x >> 32));
+    const double xl = u32_to_f64((uint32_t)x);
+    return td_groups<NP, 0>(xh, xl);
+}
+
 // ------------------------------------------------------------- init kernels
 // Odd primes below 65536 in increasing order (6541 of them), with
 // ceil(2^32 / p) for the sieve's remainder computation.  One block.
@@ -573,7 +654,7 @@ classify_kernel(const unsigned long long* __restrict__ N, uint8_t* __restrict__ 
                     const unsigned long long x = ws.val[255u - k];
                     bool comp = false;
 #pragma unroll
-                    for (int t = 0; t < N64; t++) comp |= (x * c_td_inv64[t] <= c_td_lim64[t]);
+                    if (N64 > 0) comp = td64_fp<N64>(x);
                     surv = !comp;
                 }
                 const uint32_t m = __ballot_sync(0xffffffffu, surv);

@@ -105,6 +105,63 @@ __device__ __forceinline__ uint64_t redc64(uint64_t lo, uint64_t hi, uint64_t n,
     return hi < mh ? t + n : t;
 }
 
+// General Montgomery product in the same PTX style: four mul.wide for a*b.
+__device__ __forceinline__ uint64_t mmul64_ptx(uint64_t a, uint64_t b, uint64_t n, uint64_t ninv) {
+    uint64_t r;
+    asm("{\n\t"
+        ".reg .u32 a0, a1, b0, b1, n0, n1, i0, i1, p0, p1, c0, c1, e0, e1, h0, h1, t1, t2, t3, m0, m1;\n\t"
+        ".reg .u32 q0, q1, f0, f1, g0, g1, d0, d1, u2, u3, r0, r1, bw, k0, k1;\n\t"
+        ".reg .u64 W;\n\t"
+        "mov.b64 {a0, a1}, %1;\n\t"
+        "mov.b64 {b0, b1}, %2;\n\t"
+        "mov.b64 {n0, n1}, %3;\n\t"
+        "mov.b64 {i0, i1}, %4;\n\t"
+        "mul.wide.u32 W, a0, b0;\n\t"
+        "mov.b64 {p0, p1}, W;\n\t"
+        "mul.wide.u32 W, a0, b1;\n\t"
+        "mov.b64 {c0, c1}, W;\n\t"
+        "mul.wide.u32 W, a1, b0;\n\t"
+        "mov.b64 {e0, e1}, W;\n\t"
+        "mul.wide.u32 W, a1, b1;\n\t"
+        "mov.b64 {h0, h1}, W;\n\t"
+        "add.cc.u32 t1, p1, c0;\n\t"
+        "addc.cc.u32 t2, h0, c1;\n\t"
+        "addc.u32 t3, h1, 0;\n\t"
+        "add.cc.u32 t1, t1, e0;\n\t"
+        "addc.cc.u32 t2, t2, e1;\n\t"
+        "addc.u32 t3, t3, 0;\n\t"
+        "mul.wide.u32 W, p0, i0;\n\t"
+        "mov.b64 {m0, m1}, W;\n\t"
+        "mad.lo.u32 m1, p0, i1, m1;\n\t"
+        "mad.lo.u32 m1, t1, i0, m1;\n\t"
+        "mul.wide.u32 W, m0, n0;\n\t"
+        "mov.b64 {q0, q1}, W;\n\t"
+        "mul.wide.u32 W, m0, n1;\n\t"
+        "mov.b64 {f0, f1}, W;\n\t"
+        "mul.wide.u32 W, m1, n0;\n\t"
+        "mov.b64 {g0, g1}, W;\n\t"
+        "mul.wide.u32 W, m1, n1;\n\t"
+        "mov.b64 {d0, d1}, W;\n\t"
+        "add.cc.u32 q1, q1, f0;\n\t"
+        "addc.cc.u32 u2, d0, f1;\n\t"
+        "addc.u32 u3, d1, 0;\n\t"
+        "add.cc.u32 q1, q1, g0;\n\t"
+        "addc.cc.u32 u2, u2, g1;\n\t"
+        "addc.u32 u3, u3, 0;\n\t"
+        "sub.cc.u32 r0, t2, u2;\n\t"
+        "subc.cc.u32 r1, t3, u3;\n\t"
+        "subc.u32 bw, 0, 0;\n\t"
+        "and.b32 k0, n0, bw;\n\t"
+        "and.b32 k1, n1, bw;\n\t"
+        "add.cc.u32 r0, r0, k0;\n\t"
+        "addc.u32 r1, r1, k1;\n\t"
+        "mov.b64 %0, {r0, r1};\n\t"
+        "}"
+        : "=l"(r)
+        : "l"(a), "l"(b), "l"(n), "l"(ninv));
+    return r;
+}
+
 __device__ __forceinline__ uint64_t mmul64(uint64_t a, uint64_t b, const Mont64& M) {
     return redc64(a * b, __umul64hi(a, b), M.n, M.ninv);
 }

@@ -65,6 +65,31 @@ __global__ void k_step(unsigned long long* out, unsigned long long seed, unsigne
     out[blockIdx.x * blockDim.x + threadIdx.x] = s;
 }
 
+// phase-2-like step: 3 lockstep chains, 2-bit window (2 squarings + 1 multiply by a table entry)
+template <int V>
+__global__ void k_win(unsigned long long* out, unsigned long long seed, unsigned long long dbits) {
+    const unsigned long long n = (seed | 1ull | (1ull << 63)) ^ ((unsigned long long)threadIdx.x << 20);
+    const unsigned long long ninv = isp::inv64(n);
+    isp::Mont64 M; M.n = n; M.ninv = ninv;
+    unsigned long long x[3], t[3][3];
+#pragma unroll
+    for (int c = 0; c < 3; c++) {
+        x[c] = ((threadIdx.x + 1) * 0x9E3779B97F4A7C15ull + c * 0x1234567ull) % n;
+        for (int k = 0; k < 3; k++) t[c][k] = (x[c] * (k + 3)) % n;
+    }
+    for (int i = 0; i < ITERS / 4; i++) {
+        const unsigned int dg = (dbits >> (2 * (i & 31))) & 3u;
+#pragma unroll
+        for (int c = 0; c < 3; c++) {
+            if (V == 0) { x[c] = isp::msqr64(x[c], M); x[c] = isp::msqr64(x[c], M); }
+            else { x[c] = isp::msqr64_ptx(x[c], n, ninv); x[c] = isp::msqr64_ptx(x[c], n, ninv); }
+            unsigned long long m = dg == 1 ? t[c][0] : dg == 2 ? t[c][1] : dg == 3 ? t[c][2] : x[c];
+            x[c] = V == 0 ? isp::mmul64(x[c], m, M) : isp::mmul64_ptx(x[c], m, n, ninv);
+        }
+    }
+    out[blockIdx.x * blockDim.x + threadIdx.x] = x[0] ^ x[1] ^ x[2];
+}
+
 template <typename F>
 float time_ms(F f) {
     cudaEvent_t a, b;
@@ -94,6 +119,14 @@ int main() {
     t[3] = time_ms([&] { k_step<0, true><<<blocks, threads>>>(buf, 0xD1B54A32D192ED03ull, bits); });
     t[4] = time_ms([&] { k_step<1, true><<<blocks, threads>>>(buf, 0xD1B54A32D192ED03ull, bits); });
     t[5] = time_ms([&] { k_step<2, true><<<blocks, threads>>>(buf, 0xD1B54A32D192ED03ull, bits); });
+    float tw0 = time_ms([&] { k_win<0><<<blocks, threads>>>(buf, 0xD1B54A32D192ED03ull, bits); });
+    float tw1 = time_ms([&] { k_win<1><<<blocks, threads>>>(buf, 0xD1B54A32D192ED03ull, bits); });
+    unsigned long long hw[2];
+    k_win<0><<<1, 32>>>(buf, 99, bits); cudaMemcpy(&hw[0], buf + 3, 8, cudaMemcpyDeviceToHost);
+    k_win<1><<<1, 32>>>(buf, 99, bits); cudaMemcpy(&hw[1], buf + 3, 8, cudaMemcpyDeviceToHost);
+    const double wsteps = (double)blocks * threads * 3 * 3 * (ITERS / 4);
+    printf("{\"win_mulmods_per_s\": {\"v0\": %.4e, \"ptx\": %.4e}, \"win_agree\": %s}\n", wsteps / (tw0 * 1e-3),
+           wsteps / (tw1 * 1e-3), hw[0] == hw[1] ? "true" : "false");
     // cross-check: the three squarings agree
     unsigned long long h[3];
     cudaError_t e = cudaDeviceSynchronize();
