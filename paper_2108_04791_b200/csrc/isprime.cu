@@ -22,8 +22,6 @@ using namespace isp;
 
 namespace {
 
-constexpr size_t CLS_DYN_SMEM = LOWBITS_WORDS * 4;  // 32 KB bitmap cache of values < 2^19
-
 struct Options {
     int force_path = 0;      // 0 auto, 1 sieve, 2 mr
     int bases32 = 3;         // 3 -> {2,7,61}; 7 -> full Eq 4 set
@@ -59,7 +57,7 @@ struct Ctx {
     unsigned char* qmem = nullptr;
     size_t qcap = 0;
     Queues q{};
-    int grid_cls = 0, grid_mr1 = 0, grid_mr2 = 0, grid_sieve = 0;
+    int grid_cls = 0, grid_mr1 = 0, grid_mr2 = 0, grid_sieve = 0, grid_sort = 0;
     cudaEvent_t last_done = nullptr;
     void* last_stream = nullptr;
     bool has_last = false;
@@ -77,8 +75,8 @@ struct Ctx {
 std::vector<Ctx*> g_ctx;
 
 // ---- optional per-kernel timing (events on the launching stream)
-enum { K_PLAN, K_SIEVE, K_CLASSIFY, K_MR1, K_MR2, K_POPCOUNT, K_NUM };
-const char* const k_names[K_NUM] = {"plan", "sieve", "classify", "mr1", "mr2", "popcount"};
+enum { K_PLAN, K_SIEVE, K_CLASSIFY, K_SORT, K_MR1, K_MR2, K_POPCOUNT, K_NUM };
+const char* const k_names[K_NUM] = {"plan", "sieve", "classify", "sort", "mr1", "mr2", "popcount"};
 struct KTPending { cudaEvent_t a, b; int kid; };
 std::vector<KTPending> g_kt_pending;
 std::vector<cudaEvent_t> g_ev_pool;
@@ -203,9 +201,9 @@ int init_ctx(Ctx* c) {
     CK(cudaMemset(c->plan, 0, sizeof(DevPlan)));
     CK(cudaFuncSetAttribute(sieve_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SEG_ODD));
     c->grid_sieve = c->sms * occupancy((const void*)sieve_kernel, SIEVE_THREADS, SEG_ODD);
-    CK(cudaFuncSetAttribute(classify_kernel<16, 32>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)CLS_DYN_SMEM));
-    c->grid_cls = c->sms * occupancy((const void*)classify_kernel<16, 32>, CLS_THREADS, CLS_DYN_SMEM);
+    c->grid_cls = c->sms * occupancy((const void*)classify_kernel<24, 24>, CLS_THREADS, 0);
     c->grid_mr1 = c->sms * occupancy((const void*)mr1_kernel, MR_THREADS, 0);
+    c->grid_sort = c->sms * occupancy((const void*)qscatter_kernel, SORT_THREADS, 0);
     c->grid_mr2 = c->sms * occupancy((const void*)mr2_kernel<2, false, 3>, MR_THREADS, 0);
     CK(cudaEventCreateWithFlags(&c->last_done, cudaEventDisableTiming));
     for (int k = 0; k < 2; k++) {
@@ -242,8 +240,8 @@ int ensure_queues(Ctx* c, size_t cap) {
     if (cap <= c->qcap) return ISP_OK;
     if (c->qmem) { CK(cudaFree(c->qmem)); c->qmem = nullptr; c->qcap = 0; }
     cap = (cap + 4095) & ~(size_t)4095;
-    // per entry: q32 4+4, q64 4+8, p32 4+4, p64 4+8 = 40 bytes
-    const size_t bytes = cap * 40;
+    // per entry: q32 4+4, q64 4+8, s32 4+4, s64 4+8, p32 4+4, p64 4+8 = 60 bytes
+    const size_t bytes = cap * 60;
     if (cudaMalloc(&c->qmem, bytes) != cudaSuccess) {
         cudaGetLastError();
         g_err = "queue allocation of " + std::to_string(bytes) + " bytes failed";
@@ -252,6 +250,10 @@ int ensure_queues(Ctx* c, size_t cap) {
     unsigned char* p = c->qmem;
     c->q.q64_val = reinterpret_cast<unsigned long long*>(p); p += cap * 8;
     c->q.p64_val = reinterpret_cast<unsigned long long*>(p); p += cap * 8;
+    c->q.s64_val = reinterpret_cast<unsigned long long*>(p); p += cap * 8;
+    c->q.s32_idx = reinterpret_cast<uint32_t*>(p); p += cap * 4;
+    c->q.s32_val = reinterpret_cast<uint32_t*>(p); p += cap * 4;
+    c->q.s64_idx = reinterpret_cast<uint32_t*>(p); p += cap * 4;
     c->q.q32_idx = reinterpret_cast<uint32_t*>(p); p += cap * 4;
     c->q.q32_val = reinterpret_cast<uint32_t*>(p); p += cap * 4;
     c->q.q64_idx = reinterpret_cast<uint32_t*>(p); p += cap * 4;
@@ -261,6 +263,12 @@ int ensure_queues(Ctx* c, size_t cap) {
     c->q.cap = (unsigned int)cap;
     c->qcap = cap;
     return ISP_OK;
+}
+
+// Sort grids: one 2048-entry tile per block at most, capped at the resident grid.
+int sort_grid(int full, uint32_t len) {
+    const uint32_t need = (len + 2047) / 2048;
+    return (int)(need < (uint32_t)full ? (need ? need : 1) : (uint32_t)full);
 }
 
 // Persistent MR grids never need more blocks than the chunk could queue.
@@ -280,26 +288,15 @@ bool overlaps(const void* a, size_t an, const void* b, size_t bn) {
 // constant-bank operands then sit in the IMAD instructions themselves).
 int td_round(int v) { return v >= 32 ? 32 : v >= 24 ? 24 : v >= 16 ? 16 : v >= 8 ? 8 : 0; }
 
-template <int A, int B>
-void launch_classify_ab(int g, cudaStream_t s, const unsigned long long* N, uint8_t* out, uint32_t len, Ctx* c,
-                        const TDParams& td, int vin, int vout) {
-    static bool attr = false;
-    if (!attr) {
-        cudaFuncSetAttribute(classify_kernel<A, B>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)CLS_DYN_SMEM);
-        attr = true;
-    }
-    classify_kernel<A, B><<<g, CLS_THREADS, CLS_DYN_SMEM, s>>>(N, out, len, c->plan, c->bitmap, c->q, td, vin, vout, 1);
-}
-
 template <int A>
 void launch_classify_b(int n64, int g, cudaStream_t s, const unsigned long long* N, uint8_t* out, uint32_t len,
                        Ctx* c, const TDParams& td, int vin, int vout) {
     switch (n64) {
-        case 32: launch_classify_ab<A, 32>(g, s, N, out, len, c, td, vin, vout); break;
-        case 24: launch_classify_ab<A, 24>(g, s, N, out, len, c, td, vin, vout); break;
-        case 16: launch_classify_ab<A, 16>(g, s, N, out, len, c, td, vin, vout); break;
-        case 8: launch_classify_ab<A, 8>(g, s, N, out, len, c, td, vin, vout); break;
-        default: launch_classify_ab<A, 0>(g, s, N, out, len, c, td, vin, vout); break;
+        case 32: classify_kernel<A, 32><<<g, CLS_THREADS, 0, s>>>(N, out, len, c->plan, c->bitmap, c->q, td, vin, vout); break;
+        case 24: classify_kernel<A, 24><<<g, CLS_THREADS, 0, s>>>(N, out, len, c->plan, c->bitmap, c->q, td, vin, vout); break;
+        case 16: classify_kernel<A, 16><<<g, CLS_THREADS, 0, s>>>(N, out, len, c->plan, c->bitmap, c->q, td, vin, vout); break;
+        case 8: classify_kernel<A, 8><<<g, CLS_THREADS, 0, s>>>(N, out, len, c->plan, c->bitmap, c->q, td, vin, vout); break;
+        default: classify_kernel<A, 0><<<g, CLS_THREADS, 0, s>>>(N, out, len, c->plan, c->bitmap, c->q, td, vin, vout); break;
     }
 }
 
@@ -380,6 +377,14 @@ int device_impl(Ctx* c, const unsigned long long* dN, uint8_t* dout, size_t n, c
             KScope ks(K_CLASSIFY, s);
             launch_classify(td.n32, td.n64, gcls, s, N, out, len, c, td, vin, vout);
             CKL("classify_kernel");
+        }
+        {
+            KScope ks(K_SORT, s);
+            const int gs = sort_grid(c->grid_sort, len);
+            qhist_kernel<<<gs, SORT_THREADS, 0, s>>>(c->plan, c->q);
+            CKL("qhist_kernel");
+            qscatter_kernel<<<gs, SORT_THREADS, 0, s>>>(c->plan, c->q);
+            CKL("qscatter_kernel");
         }
         {
             KScope ks(K_MR1, s);

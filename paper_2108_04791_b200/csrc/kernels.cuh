@@ -44,8 +44,10 @@ struct DevPlan {
     // method), accumulated only when work counting is on:
     // [mr1 32-bit, mr1 64-bit, mr2 32-bit, mr2 64-bit]
     unsigned long long work[4];
+    // counting sort of the trial-division survivors by bit length (per chunk)
+    unsigned int bins32[33], bins64[65], cur32[33], cur64[65];
+    unsigned int sorted32, sorted64;
     unsigned int pback;                     // FP64-class entries of P64 (stored from the back)
-    unsigned int qfback;                    // FP64-class entries of Q64 (stored from the back)
     unsigned int cur1[3], cur2[3];          // dynamic work cursors of mr1 / mr2 (3 regions)
     unsigned long long work_f[2];           // FP64-class mulmods: mr1, mr2 (work counting)
 };
@@ -61,8 +63,10 @@ struct PlanParams {
 };
 
 struct Queues {
-    uint32_t* q32_idx; uint32_t* q32_val;             // classify -> mr1
-    uint32_t* q64_idx; unsigned long long* q64_val;   // Montgomery class from the front, FP64 class from the back
+    uint32_t* q32_idx; uint32_t* q32_val;             // classify -> (sort) -> mr1
+    uint32_t* q64_idx; unsigned long long* q64_val;
+    uint32_t* s32_idx; uint32_t* s32_val;             // the same entries ordered by bit length
+    uint32_t* s64_idx; unsigned long long* s64_val;
     uint32_t* p32_idx; uint32_t* p32_val;             // base-2 strong probable primes -> mr2
     uint32_t* p64_idx; unsigned long long* p64_val;   // Montgomery class from the front, FP64 class from the back
     unsigned int cap;                                  // entries per queue
@@ -402,10 +406,11 @@ __global__ void __launch_bounds__(PLAN_THREADS) plan_kernel(const unsigned long 
     plan->whi = whi;
     plan->sieve_needed = need;
     for (int q = 0; q < 4; q++) { plan->total[q] += plan->counts[q]; plan->counts[q] = 0; }
+    for (int b = 0; b < 33; b++) { plan->bins32[b] = 0; plan->cur32[b] = 0; }
+    for (int b = 0; b < 65; b++) { plan->bins64[b] = 0; plan->cur64[b] = 0; }
+    plan->sorted32 = plan->sorted64 = 0;
     plan->total[3] += plan->pback;  // FP64-class base-2 passes count with the 64-bit ones
     plan->pback = 0;
-    plan->total[1] += plan->qfback;  // FP64-class survivors count with the 64-bit ones
-    plan->qfback = 0;
     for (int r = 0; r < 3; r++) { plan->cur1[r] = 0; plan->cur2[r] = 0; }
     plan->chunks += 1;
 }
@@ -507,9 +512,6 @@ sieve_kernel(const DevPlan* __restrict__ plan, uint32_t* __restrict__ bitmap,
     }
 }
 
-__device__ __forceinline__ unsigned int bitlen32(uint32_t v) { return 32u - __clz(v); }
-__device__ __forceinline__ unsigned int bitlen64u(unsigned long long v) { return 64u - __clzll((long long)v); }
-
 // ------------------------------------------------------------- A2: classify
 // One streaming pass over N; each warp owns a 256-element warp-tile (lane l:
 // element pairs 2l + 64j, j < 4: every load instruction reads 512 contiguous
@@ -531,37 +533,24 @@ struct ClsWarp {
     unsigned long long val[256];  // list32 from the front (low 32 bits used), list64 from the back
     uint8_t pos[256];             // element offset within the warp-tile
     uint8_t res[256];             // results of the warp-tile, element order
-    unsigned short rank[256];     // survivor's rank within its bit-length bin (block tile)
     uint32_t surv[16];            // survivor bit per list slot: [0..8) list32, [8..16) list64 (by back index)
 };
-constexpr unsigned int LOWBITS_VALUES = 1u << 19;               // values cached in shared memory
-constexpr unsigned int LOWBITS_WORDS = LOWBITS_VALUES / 64;     // odd-only: 32 values per word
 struct ClsSmem {
     ClsWarp w[CLS_THREADS / 32];
-    unsigned int bcnt[2][65];     // survivors per bit length (double-buffered by tile parity)
-    unsigned int boff[65];        // queue offset of each bit-length bin in the current tile
+    uint32_t cnt[CLS_THREADS / 32][2];
+    uint32_t base[CLS_THREADS / 32][2];
 };
-// Survivor classes by bit length b of n: b <= 32 -> Q32 (32-bit Montgomery),
-// 33..49 -> FP64 class (back of Q64), 50..64 -> 64-bit Montgomery (front of Q64).
 
 template <int N32, int N64>
 __global__ void __launch_bounds__(CLS_THREADS)
 classify_kernel(const unsigned long long* __restrict__ N, uint8_t* __restrict__ out, uint32_t len,
                 DevPlan* __restrict__ plan, const uint32_t* __restrict__ bitmap, Queues q, TDParams td,
-                int vec_in, int vec_out, int use_lowbits) {
+                int vec_in, int vec_out) {
     __shared__ ClsSmem sm;
-    extern __shared__ uint32_t lowbits[];  // bitmap words of values < LOWBITS_VALUES when the window starts at 0
     const unsigned long long wlo = plan->wlo, whi = plan->whi;
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
     ClsWarp& ws = sm.w[wid];
     const uint32_t ntiles = (len + CLS_TILE - 1) / CLS_TILE;
-    // random lookups of small values hit shared memory instead of L2
-    const bool lowcache = use_lowbits && wlo == 0 && whi >= LOWBITS_VALUES;
-    if (lowcache)
-        for (uint32_t k = tid; k < LOWBITS_WORDS; k += CLS_THREADS) lowbits[k] = __ldg(bitmap + k);
-    for (int b = tid; b < 2 * 65; b += CLS_THREADS) (&sm.bcnt[0][0])[b] = 0;
-    __syncthreads();
-    uint32_t parity = 0;
     for (uint32_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
         const uint32_t wbase = tile * CLS_TILE + 256u * wid;
         const bool full = wbase + 256u <= len;
@@ -593,8 +582,7 @@ classify_kernel(const unsigned long long* __restrict__ N, uint8_t* __restrict__ 
             else if (!(x & 1ull)) rr = (x == 2ull);
             else if (x >= wlo && x < whi) {
                 const unsigned long long b = (x - wlo) >> 1;
-                const uint32_t word = (lowcache && x < LOWBITS_VALUES) ? lowbits[b >> 5] : __ldg(bitmap + (b >> 5));
-                rr = (uint8_t)((word >> (b & 31)) & 1u);
+                rr = (uint8_t)((__ldg(bitmap + (b >> 5)) >> (b & 31)) & 1u);
             } else cls = (x < (1ull << 32)) ? 1u : 2u;
             if (i >= len) cls = 0;
             r[e] = rr;
@@ -674,81 +662,54 @@ classify_kernel(const unsigned long long* __restrict__ N, uint8_t* __restrict__ 
                 s64 += __popc(m);
             }
         }
-        // ---- queue reservation, ordered by bit length within the block tile.
-        // A warp of the witness kernels runs as long as its longest exponent;
-        // neighbouring queue entries of equal bit length keep lanes in step on
-        // mixed magnitudes (config C5) at the cost of shared-memory counters,
-        // with no separate sorting pass.  One barrier when the tile has no
-        // survivor, three otherwise.
-        unsigned int* bcnt = sm.bcnt[parity];
-        if (s32 | s64) {
-            for (uint32_t k0 = 0; k0 < n32; k0 += 32) {
-                const uint32_t k = k0 + lane;
-                if ((ws.surv[k0 >> 5] >> lane) & 1u)
-                    ws.rank[k] = (unsigned short)atomicAdd(&bcnt[bitlen32((uint32_t)ws.val[k])], 1u);
-            }
-            for (uint32_t k0 = 0; k0 < n64; k0 += 32) {
-                const uint32_t k = 255u - (k0 + lane);
-                if ((ws.surv[8 + (k0 >> 5)] >> lane) & 1u)
-                    ws.rank[k] = (unsigned short)atomicAdd(&bcnt[bitlen64u(ws.val[k])], 1u);
-            }
-        }
+        // ---- queue reservation: one barrier (two if this block tile has survivors)
+        if (lane == 0) { sm.cnt[wid][0] = s32; sm.cnt[wid][1] = s64; }
         if (__syncthreads_or((int)(s32 | s64))) {
             if (wid == 0) {
-                // three classes: bins 1..32 (Q32), 33..49 (FP64, back of Q64), 50..64 (front of Q64)
-                const uint32_t c32 = bcnt[1 + lane];
-                const uint32_t cf = lane < 17 ? bcnt[33 + lane] : 0u;
-                const uint32_t ci = lane < 15 ? bcnt[50 + lane] : 0u;
-                uint32_t i32 = c32, i_f = cf, i_i = ci;
+                const uint32_t a32 = lane < CLS_THREADS / 32 ? sm.cnt[lane][0] : 0u;
+                const uint32_t a64 = lane < CLS_THREADS / 32 ? sm.cnt[lane][1] : 0u;
+                uint32_t i32 = a32, i64 = a64;
 #pragma unroll
-                for (int o = 1; o < 32; o <<= 1) {
-                    const uint32_t y0 = __shfl_up_sync(0xffffffffu, i32, o);
-                    const uint32_t y1 = __shfl_up_sync(0xffffffffu, i_f, o);
-                    const uint32_t y2 = __shfl_up_sync(0xffffffffu, i_i, o);
-                    if (lane >= o) { i32 += y0; i_f += y1; i_i += y2; }
+                for (int o = 1; o < CLS_THREADS / 32; o <<= 1) {
+                    const uint32_t y32 = __shfl_up_sync(0xffffffffu, i32, o);
+                    const uint32_t y64 = __shfl_up_sync(0xffffffffu, i64, o);
+                    if (lane >= o) { i32 += y32; i64 += y64; }
                 }
-                const uint32_t t32 = __shfl_sync(0xffffffffu, i32, 31);
-                const uint32_t tf = __shfl_sync(0xffffffffu, i_f, 31);
-                const uint32_t ti = __shfl_sync(0xffffffffu, i_i, 31);
-                uint32_t g32 = 0, gf = 0, gi = 0;
+                const uint32_t t32 = __shfl_sync(0xffffffffu, i32, CLS_THREADS / 32 - 1);
+                const uint32_t t64 = __shfl_sync(0xffffffffu, i64, CLS_THREADS / 32 - 1);
+                uint32_t g32 = 0, g64 = 0;
                 if (lane == 0) {
                     g32 = t32 ? atomicAdd(&plan->counts[0], t32) : 0u;
-                    gf = tf ? atomicAdd(&plan->qfback, tf) : 0u;
-                    gi = ti ? atomicAdd(&plan->counts[1], ti) : 0u;
+                    g64 = t64 ? atomicAdd(&plan->counts[1], t64) : 0u;
                 }
                 g32 = __shfl_sync(0xffffffffu, g32, 0);
-                gf = __shfl_sync(0xffffffffu, gf, 0);
-                gi = __shfl_sync(0xffffffffu, gi, 0);
-                sm.boff[1 + lane] = g32 + i32 - c32;
-                if (lane < 17) sm.boff[33 + lane] = gf + i_f - cf;
-                if (lane < 15) sm.boff[50 + lane] = gi + i_i - ci;
-                // the other parity's counters are no longer read by anyone
-                for (int b = lane; b < 65; b += 32) sm.bcnt[parity ^ 1][b] = 0;
+                g64 = __shfl_sync(0xffffffffu, g64, 0);
+                if (lane < CLS_THREADS / 32) { sm.base[lane][0] = g32 + i32 - a32; sm.base[lane][1] = g64 + i64 - a64; }
             }
             __syncthreads();
             if (s32 | s64) {
+                uint32_t o32 = sm.base[wid][0], o64 = sm.base[wid][1];
                 for (uint32_t k0 = 0; k0 < n32; k0 += 32) {
+                    const uint32_t m = ws.surv[k0 >> 5];
                     const uint32_t k = k0 + lane;
-                    if ((ws.surv[k0 >> 5] >> lane) & 1u) {
-                        const uint32_t v32 = (uint32_t)ws.val[k];
-                        const uint32_t at = sm.boff[bitlen32(v32)] + ws.rank[k];
+                    if ((m >> lane) & 1u) {
+                        const uint32_t at = o32 + __popc(m & ((1u << lane) - 1u));
                         q.q32_idx[at] = wbase + ws.pos[k];
-                        q.q32_val[at] = v32;
+                        q.q32_val[at] = (uint32_t)ws.val[k];
                     }
+                    o32 += __popc(m);
                 }
                 for (uint32_t k0 = 0; k0 < n64; k0 += 32) {
-                    const uint32_t k = 255u - (k0 + lane);
-                    if ((ws.surv[8 + (k0 >> 5)] >> lane) & 1u) {
-                        const unsigned long long v64 = ws.val[k];
-                        const unsigned int bl = bitlen64u(v64);
-                        const uint32_t off = sm.boff[bl] + ws.rank[k];
-                        const uint32_t at = bl <= 49 ? q.cap - 1 - off : off;
-                        q.q64_idx[at] = wbase + ws.pos[k];
-                        q.q64_val[at] = v64;
+                    const uint32_t m = ws.surv[8 + (k0 >> 5)];
+                    const uint32_t k = k0 + lane;
+                    if ((m >> lane) & 1u) {
+                        const uint32_t at = o64 + __popc(m & ((1u << lane) - 1u));
+                        q.q64_idx[at] = wbase + ws.pos[255u - k];
+                        q.q64_val[at] = ws.val[255u - k];
                     }
+                    o64 += __popc(m);
                 }
             }
-            parity ^= 1;
         }
         // ---- results of a warp that took the list path: shared tile -> out
         if (wtot != 0) {
@@ -761,6 +722,142 @@ classify_kernel(const unsigned long long* __restrict__ N, uint8_t* __restrict__ 
             }
         }
     }
+}
+
+// ------------------------------------------------------------- A2b: order by magnitude
+// Counting sort of the survivor queues by bit length (33 keys for Q32, 65 for
+// Q64).  A warp runs the exponent loop as long as its longest element, so on
+// mixed magnitudes (config C5: bit lengths 33..64 in every warp) unsorted
+// queues waste about a quarter of the multiply pipe; sorted, neighbouring
+// lanes carry equal-length exponents.  Skipped (flag stays 0, mr1 reads the
+// unsorted queue) when the expected gain is small (sort_pays).
+constexpr int SORT_THREADS = 256;
+constexpr int SORT_TILE = 2048;
+
+__device__ __forceinline__ unsigned int bitlen32(uint32_t v) { return 32u - __clz(v); }
+__device__ __forceinline__ unsigned int bitlen64u(unsigned long long v) { return 64u - __clzll((long long)v); }
+
+__global__ void __launch_bounds__(SORT_THREADS) qhist_kernel(DevPlan* __restrict__ plan, Queues q) {
+    __shared__ unsigned int h32[33], h64[65];
+    const int tid = threadIdx.x;
+    for (int b = tid; b < 65; b += SORT_THREADS) { h64[b] = 0; if (b < 33) h32[b] = 0; }
+    __syncthreads();
+    const unsigned int c32 = plan->counts[0], c64 = plan->counts[1];
+    const unsigned int stride = gridDim.x * SORT_THREADS;
+    for (unsigned int b0 = blockIdx.x * SORT_THREADS; b0 < c32; b0 += stride) {
+        const unsigned int i = b0 + tid;
+        const unsigned int bin = i < c32 ? bitlen32(q.q32_val[i]) : 0u;
+        const unsigned int peers = __match_any_sync(0xffffffffu, bin);
+        if (i < c32 && (tid & 31) == __ffs(peers) - 1) atomicAdd(&h32[bin], (unsigned int)__popc(peers));
+    }
+    for (unsigned int b0 = blockIdx.x * SORT_THREADS; b0 < c64; b0 += stride) {
+        const unsigned int i = b0 + tid;
+        const unsigned int bin = i < c64 ? bitlen64u(q.q64_val[i]) : 0u;
+        const unsigned int peers = __match_any_sync(0xffffffffu, bin);
+        if (i < c64 && (tid & 31) == __ffs(peers) - 1) atomicAdd(&h64[bin], (unsigned int)__popc(peers));
+    }
+    __syncthreads();
+    for (int b = tid; b < 65; b += SORT_THREADS) {
+        if (h64[b]) atomicAdd(&plan->bins64[b], h64[b]);
+        if (b < 33 && h32[b]) atomicAdd(&plan->bins32[b], h32[b]);
+    }
+}
+
+template <typename T, int NB>
+__device__ __forceinline__ void scatter_sorted(const unsigned int* __restrict__ gbins, unsigned int* gcur, unsigned int count,
+                                               const uint32_t* __restrict__ src_idx, const T* __restrict__ src_val,
+                                               uint32_t* __restrict__ dst_idx, T* __restrict__ dst_val,
+                                               unsigned int* spre, unsigned int* scnt, unsigned int* sbase) {
+    const int tid = threadIdx.x;
+    // exclusive prefix of the global bins (every block computes it)
+    if (tid == 0) {
+        unsigned int acc = 0;
+        for (int b = 0; b < NB; b++) { spre[b] = acc; acc += gbins[b]; }
+    }
+    for (int b = tid; b < NB; b += SORT_THREADS) scnt[b] = 0;
+    __syncthreads();
+    constexpr int PER = SORT_TILE / SORT_THREADS;
+    for (unsigned int t0 = blockIdx.x * SORT_TILE; t0 < count; t0 += gridDim.x * SORT_TILE) {
+        uint32_t idx[PER];
+        T val[PER];
+        unsigned int bin[PER], rank[PER];
+#pragma unroll
+        for (int k = 0; k < PER; k++) {
+            const unsigned int i = t0 + tid + k * SORT_THREADS;
+            bin[k] = NB;  // sentinel: no element
+            if (i < count) {
+                idx[k] = src_idx[i];
+                val[k] = src_val[i];
+                bin[k] = (sizeof(T) == 8) ? bitlen64u((unsigned long long)val[k]) : bitlen32((uint32_t)val[k]);
+            }
+        }
+#pragma unroll
+        for (int k = 0; k < PER; k++) {
+            const unsigned int peers = __match_any_sync(0xffffffffu, bin[k]);
+            const int leader = __ffs(peers) - 1;
+            const int lane = tid & 31;
+            unsigned int base = 0;
+            if (lane == leader && bin[k] < NB) base = atomicAdd(&scnt[bin[k]], (unsigned int)__popc(peers));
+            base = __shfl_sync(0xffffffffu, base, leader);
+            rank[k] = base + __popc(peers & ((1u << lane) - 1u));
+        }
+        __syncthreads();
+        for (int b = tid; b < NB; b += SORT_THREADS)
+            if (scnt[b]) sbase[b] = spre[b] + atomicAdd(&gcur[b], scnt[b]);
+        __syncthreads();
+#pragma unroll
+        for (int k = 0; k < PER; k++) {
+            if (bin[k] < NB) {
+                const unsigned int pos = sbase[bin[k]] + rank[k];
+                dst_idx[pos] = idx[k];
+                dst_val[pos] = val[k];
+            }
+        }
+        __syncthreads();
+        for (int b = tid; b < NB; b += SORT_THREADS) scnt[b] = 0;
+        __syncthreads();
+    }
+}
+
+// Sort only when it pays: a warp of unsorted entries runs about as long as the
+// longest exponent present, so the expected SIMT efficiency is mean/max bit
+// length.  Below 0.92 (config C5: ~0.76) the sort wins; config C3 (~0.98) and
+// C2 (~0.97) skip it.
+__device__ __forceinline__ bool sort_pays(const unsigned int* bins, int nb) {
+    unsigned long long cnt = 0, sum = 0;
+    int mx = 0;
+    for (int b = 0; b < nb; b++) {
+        cnt += bins[b];
+        sum += (unsigned long long)bins[b] * b;
+        if (bins[b]) mx = b;
+    }
+    if (cnt < 4096) return false;
+    if ((double)sum < 0.92 * (double)mx * (double)cnt) return true;
+    // both sides of the FP64 / Montgomery boundary (bit length 49 | 50) present
+    if (nb == 65) {
+        unsigned long long lo = 0;
+        for (int b = 0; b <= 49; b++) lo += bins[b];
+        if (lo > cnt / 64 && lo < cnt - cnt / 64) return true;
+    }
+    return false;
+}
+
+__global__ void __launch_bounds__(SORT_THREADS) qscatter_kernel(DevPlan* __restrict__ plan, Queues q) {
+    __shared__ unsigned int spre[65], scnt[65], sbase[65];
+    __shared__ unsigned int do32, do64;
+    if (threadIdx.x == 0) {
+        do32 = sort_pays(plan->bins32, 33);
+        do64 = sort_pays(plan->bins64, 65);
+        if (blockIdx.x == 0) { plan->sorted32 = do32; plan->sorted64 = do64; }
+    }
+    __syncthreads();
+    if (do32)
+        scatter_sorted<uint32_t, 33>(plan->bins32, plan->cur32, plan->counts[0], q.q32_idx, q.q32_val,
+                                     q.s32_idx, q.s32_val, spre, scnt, sbase);
+    __syncthreads();
+    if (do64)
+        scatter_sorted<unsigned long long, 65>(plan->bins64, plan->cur64, plan->counts[1], q.q64_idx, q.q64_val,
+                                               q.s64_idx, q.s64_val, spre, scnt, sbase);
 }
 
 // ------------------------------------------------------------- A3: MR phase 1
@@ -868,12 +965,27 @@ __device__ __forceinline__ unsigned int modexp_squarings(unsigned long long d) {
 __device__ __forceinline__ unsigned int modexp_mults(unsigned long long d) { return __popcll(d) - 1; }
 __device__ __forceinline__ unsigned long long odd_part(unsigned long long n) { return (n - 1) >> (__ffsll((long long)(n - 1)) - 1); }
 
+__device__ __forceinline__ unsigned int fp_class_count(const DevPlan* plan) {
+    if (!plan->sorted64) return 0u;
+    unsigned int c = 0;
+    for (int b = 0; b <= 49; b++) c += plan->bins64[b];  // bit length <= 49 <=> n < 2^49
+    return c;
+}
+
 __global__ void __launch_bounds__(MR_THREADS)
 mr1_kernel(DevPlan* __restrict__ plan, Queues q, int count_work) {
     __shared__ WarpStage<uint32_t> st32[MR_THREADS / 32];
     __shared__ WarpStage<unsigned long long> st64i[MR_THREADS / 32], st64f[MR_THREADS / 32];
-    // regions: 0 = Q32, 1 = FP64 class (back of Q64), 2 = 64-bit Montgomery class (front of Q64)
-    const unsigned int size[3] = {plan->counts[0], plan->qfback, plan->counts[1]};
+    __shared__ unsigned int s_nf;
+    if (threadIdx.x == 0) s_nf = fp_class_count(plan);
+    __syncthreads();
+    const unsigned int c32 = plan->counts[0], c64 = plan->counts[1], nf = s_nf;
+    const uint32_t* q32i = plan->sorted32 ? q.s32_idx : q.q32_idx;
+    const uint32_t* q32v = plan->sorted32 ? q.s32_val : q.q32_val;
+    const uint32_t* q64i = plan->sorted64 ? q.s64_idx : q.q64_idx;
+    const unsigned long long* q64v = plan->sorted64 ? q.s64_val : q.q64_val;
+    // regions: 0 = Q32, 1 = FP64 class = sorted Q64 [0, nf), 2 = the rest of Q64
+    const unsigned int size[3] = {c32, nf, c64 - nf};
     unsigned long long w32 = 0, w64 = 0, wf = 0;
     const unsigned int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
     const unsigned int gwarp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
@@ -888,22 +1000,22 @@ mr1_kernel(DevPlan* __restrict__ plan, Queues q, int count_work) {
                 bool pass = false;
                 uint32_t n = 0, idx = 0;
                 if (act) {
-                    n = q.q32_val[i];
-                    idx = q.q32_idx[i];
+                    n = q32v[i];
+                    idx = q32i[i];
                     pass = sprp2_32(n);
                     if (count_work) w32 += modexp_squarings(odd_part(n));
                 }
                 stage_append<uint32_t>(pass, idx, n, st32[wib], n32s, &plan->counts[2], q.p32_idx, q.p32_val);
             } else {
-                const unsigned int k = r == 1 ? q.cap - 1 - i : i;
+                const unsigned int k = r == 1 ? i : nf + i;
                 bool pass = false, fp = false;
                 unsigned long long n = 0;
                 uint32_t idx = 0;
                 if (act) {
-                    n = q.q64_val[k];
-                    idx = q.q64_idx[k];
+                    n = q64v[k];
+                    idx = q64i[k];
                     // magnitude-class dispatch: below 2^49 on the FP64 pipe, above with
-                    // 64-bit Montgomery (uniform per region)
+                    // 64-bit Montgomery (uniform per region when the queue is sorted)
                     fp = n < FP_LIMIT;
                     pass = fp ? sprp2_f64(n) : sprp2_64(n);
                     if (count_work) { if (fp) wf += modexp_squarings(odd_part(n)); else w64 += modexp_squarings(odd_part(n)); }
