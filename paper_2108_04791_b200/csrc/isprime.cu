@@ -381,8 +381,6 @@ int device_impl(Ctx* c, const unsigned long long* dN, uint8_t* dout, size_t n, c
         {
             KScope ks(K_SORT, s);
             const int gs = sort_grid(c->grid_sort, len);
-            qhist_kernel<<<gs, SORT_THREADS, 0, s>>>(c->plan, c->q);
-            CKL("qhist_kernel");
             qscatter_kernel<<<gs, SORT_THREADS, 0, s>>>(c->plan, c->q);
             CKL("qscatter_kernel");
         }

@@ -465,9 +465,12 @@ sieve_kernel(const DevPlan* __restrict__ plan, uint32_t* __restrict__ bitmap,
             if (!(m & 1ull)) m += p;
             const unsigned long long pp = (unsigned long long)p * p;
             if (m < pp) m = pp;
-            const unsigned long long k0 = (m - x) >> 1;
-            const uint32_t stride = 32u * p;
-            for (unsigned long long k = k0 + (unsigned long long)lane * p; k < seg_len; k += stride) seg[k] = 0;
+            const unsigned long long k0 = (m - x) >> 1;  // < p + p^2 / 2: may exceed the segment
+            if (k0 < seg_len) {
+                const uint32_t stride = 32u * p;
+#pragma unroll 4
+                for (uint32_t k = (uint32_t)k0 + lane * p; k < seg_len; k += stride) seg[k] = 0;
+            }
         }
         // one prime per thread, larger primes: first index with p >= warp_p
         {
@@ -488,7 +491,11 @@ sieve_kernel(const DevPlan* __restrict__ plan, uint32_t* __restrict__ bitmap,
                 if (!(m & 1ull)) m += p;
                 const unsigned long long pp = (unsigned long long)p * p;
                 if (m < pp) m = pp;
-                for (unsigned long long k = (m - x) >> 1; k < seg_len; k += p) seg[k] = 0;
+                const unsigned long long k0 = (m - x) >> 1;
+                if (k0 < seg_len) {
+#pragma unroll 4
+                    for (uint32_t k = (uint32_t)k0; k < seg_len; k += p) seg[k] = 0;
+                }
             }
         }
         __syncthreads();
@@ -539,6 +546,7 @@ struct ClsSmem {
     ClsWarp w[CLS_THREADS / 32];
     uint32_t cnt[CLS_THREADS / 32][2];
     uint32_t base[CLS_THREADS / 32][2];
+    unsigned int h32[33], h64[65];  // bit-length histogram of this block's survivors (for the sort)
 };
 
 template <int N32, int N64>
@@ -551,6 +559,8 @@ classify_kernel(const unsigned long long* __restrict__ N, uint8_t* __restrict__ 
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
     ClsWarp& ws = sm.w[wid];
     const uint32_t ntiles = (len + CLS_TILE - 1) / CLS_TILE;
+    for (int b = tid; b < 65; b += CLS_THREADS) { sm.h64[b] = 0; if (b < 33) sm.h32[b] = 0; }
+    __syncthreads();
     for (uint32_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
         const uint32_t wbase = tile * CLS_TILE + 256u * wid;
         const bool full = wbase + 256u <= len;
@@ -694,8 +704,10 @@ classify_kernel(const unsigned long long* __restrict__ N, uint8_t* __restrict__ 
                     const uint32_t k = k0 + lane;
                     if ((m >> lane) & 1u) {
                         const uint32_t at = o32 + __popc(m & ((1u << lane) - 1u));
+                        const uint32_t v32 = (uint32_t)ws.val[k];
                         q.q32_idx[at] = wbase + ws.pos[k];
-                        q.q32_val[at] = (uint32_t)ws.val[k];
+                        q.q32_val[at] = v32;
+                        atomicAdd(&sm.h32[32u - __clz(v32)], 1u);
                     }
                     o32 += __popc(m);
                 }
@@ -704,8 +716,10 @@ classify_kernel(const unsigned long long* __restrict__ N, uint8_t* __restrict__ 
                     const uint32_t k = k0 + lane;
                     if ((m >> lane) & 1u) {
                         const uint32_t at = o64 + __popc(m & ((1u << lane) - 1u));
+                        const unsigned long long v64 = ws.val[255u - k];
                         q.q64_idx[at] = wbase + ws.pos[255u - k];
-                        q.q64_val[at] = ws.val[255u - k];
+                        q.q64_val[at] = v64;
+                        atomicAdd(&sm.h64[64u - __clzll((long long)v64)], 1u);
                     }
                     o64 += __popc(m);
                 }
@@ -722,6 +736,11 @@ classify_kernel(const unsigned long long* __restrict__ N, uint8_t* __restrict__ 
             }
         }
     }
+    __syncthreads();
+    for (int b = tid; b < 65; b += CLS_THREADS) {
+        if (sm.h64[b]) atomicAdd(&plan->bins64[b], sm.h64[b]);
+        if (b < 33 && sm.h32[b]) atomicAdd(&plan->bins32[b], sm.h32[b]);
+    }
 }
 
 // ------------------------------------------------------------- A2b: order by magnitude
@@ -736,32 +755,6 @@ constexpr int SORT_TILE = 2048;
 
 __device__ __forceinline__ unsigned int bitlen32(uint32_t v) { return 32u - __clz(v); }
 __device__ __forceinline__ unsigned int bitlen64u(unsigned long long v) { return 64u - __clzll((long long)v); }
-
-__global__ void __launch_bounds__(SORT_THREADS) qhist_kernel(DevPlan* __restrict__ plan, Queues q) {
-    __shared__ unsigned int h32[33], h64[65];
-    const int tid = threadIdx.x;
-    for (int b = tid; b < 65; b += SORT_THREADS) { h64[b] = 0; if (b < 33) h32[b] = 0; }
-    __syncthreads();
-    const unsigned int c32 = plan->counts[0], c64 = plan->counts[1];
-    const unsigned int stride = gridDim.x * SORT_THREADS;
-    for (unsigned int b0 = blockIdx.x * SORT_THREADS; b0 < c32; b0 += stride) {
-        const unsigned int i = b0 + tid;
-        const unsigned int bin = i < c32 ? bitlen32(q.q32_val[i]) : 0u;
-        const unsigned int peers = __match_any_sync(0xffffffffu, bin);
-        if (i < c32 && (tid & 31) == __ffs(peers) - 1) atomicAdd(&h32[bin], (unsigned int)__popc(peers));
-    }
-    for (unsigned int b0 = blockIdx.x * SORT_THREADS; b0 < c64; b0 += stride) {
-        const unsigned int i = b0 + tid;
-        const unsigned int bin = i < c64 ? bitlen64u(q.q64_val[i]) : 0u;
-        const unsigned int peers = __match_any_sync(0xffffffffu, bin);
-        if (i < c64 && (tid & 31) == __ffs(peers) - 1) atomicAdd(&h64[bin], (unsigned int)__popc(peers));
-    }
-    __syncthreads();
-    for (int b = tid; b < 65; b += SORT_THREADS) {
-        if (h64[b]) atomicAdd(&plan->bins64[b], h64[b]);
-        if (b < 33 && h32[b]) atomicAdd(&plan->bins32[b], h32[b]);
-    }
-}
 
 template <typename T, int NB>
 __device__ __forceinline__ void scatter_sorted(const unsigned int* __restrict__ gbins, unsigned int* gcur, unsigned int count,
@@ -782,14 +775,16 @@ __device__ __forceinline__ void scatter_sorted(const unsigned int* __restrict__ 
         T val[PER];
         unsigned int bin[PER], rank[PER];
 #pragma unroll
+        for (int k = 0; k < PER; k++) {  // all loads in flight before any use
+            const unsigned int i = t0 + tid + k * SORT_THREADS;
+            idx[k] = i < count ? src_idx[i] : 0u;
+            val[k] = i < count ? src_val[i] : (T)0;
+        }
+#pragma unroll
         for (int k = 0; k < PER; k++) {
             const unsigned int i = t0 + tid + k * SORT_THREADS;
-            bin[k] = NB;  // sentinel: no element
-            if (i < count) {
-                idx[k] = src_idx[i];
-                val[k] = src_val[i];
-                bin[k] = (sizeof(T) == 8) ? bitlen64u((unsigned long long)val[k]) : bitlen32((uint32_t)val[k]);
-            }
+            bin[k] = i < count ? ((sizeof(T) == 8) ? bitlen64u((unsigned long long)val[k]) : bitlen32((uint32_t)val[k]))
+                               : (unsigned int)NB;  // sentinel: no element
         }
 #pragma unroll
         for (int k = 0; k < PER; k++) {
