@@ -556,6 +556,7 @@ classify_kernel(const unsigned long long* __restrict__ N, uint8_t* __restrict__ 
                 int vec_in, int vec_out) {
     __shared__ ClsSmem sm;
     const unsigned long long wlo = plan->wlo, whi = plan->whi;
+    const unsigned long long span = whi - wlo;  // <= 2^32 (0: no window)
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
     ClsWarp& ws = sm.w[wid];
     const uint32_t ntiles = (len + CLS_TILE - 1) / CLS_TILE;
@@ -580,26 +581,31 @@ classify_kernel(const unsigned long long* __restrict__ N, uint8_t* __restrict__ 
                 v[e] = i < len ? N[i] : 0ull;
             }
         }
-        uint32_t c32 = 0, c64 = 0, clsbits = 0;  // 2 bits per element: 1 -> list32, 2 -> list64
+        // branch-free per element: odd values inside the window read their bit,
+        // even values are prime only when equal to 2, other odd values >= 3
+        // become trial-division candidates (class 1: < 2^32, class 2: >= 2^32)
+        uint32_t clsbits = 0;  // 2 bits per element: 1 -> list32, 2 -> list64
         uint8_t r[8];
 #pragma unroll
         for (int e = 0; e < 8; e++) {
             const unsigned long long x = v[e];
-            const uint32_t i = wbase + 2 * lane + 64 * (e >> 1) + (e & 1);
-            uint32_t cls = 0;
-            uint8_t rr = 0;
-            if (x < 2ull) rr = 0;
-            else if (!(x & 1ull)) rr = (x == 2ull);
-            else if (x >= wlo && x < whi) {
-                const unsigned long long b = (x - wlo) >> 1;
-                rr = (uint8_t)((__ldg(bitmap + (b >> 5)) >> (b & 31)) & 1u);
-            } else cls = (x < (1ull << 32)) ? 1u : 2u;
-            if (i >= len) cls = 0;
-            r[e] = rr;
-            c32 += cls == 1;
-            c64 += cls == 2;
+            const uint32_t xlo = (uint32_t)x, xhi = (uint32_t)(x >> 32);
+            const unsigned long long d = x - wlo;
+            const bool odd = xlo & 1u;
+            const bool inwin = odd && d < span;
+            const uint32_t d32 = (uint32_t)d;
+            const uint32_t word = inwin ? __ldg(bitmap + (d32 >> 6)) : 0u;
+            const uint32_t bit = (word >> ((d32 >> 1) & 31u)) & 1u;
+            const bool two = (xlo == 2u) && (xhi == 0u);
+            r[e] = (uint8_t)(inwin ? bit : (uint32_t)two);
+            uint32_t cls = (odd && !inwin && (xhi != 0u || xlo > 1u)) ? (xhi != 0u ? 2u : 1u) : 0u;
+            if (!full) {
+                const uint32_t i = wbase + 2 * lane + 64 * (e >> 1) + (e & 1);
+                if (i >= len) cls = 0;
+            }
             clsbits |= cls << (2 * e);
         }
+        const uint32_t c32 = __popc(clsbits & 0x5555u), c64 = __popc(clsbits & 0xAAAAu);
         // warp scan of the packed (c32, c64) counts
         const uint32_t packed = c32 | (c64 << 16);
         uint32_t incl = packed;
