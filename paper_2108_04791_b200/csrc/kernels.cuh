@@ -586,16 +586,23 @@ classify_kernel(const unsigned long long* __restrict__ N, uint8_t* __restrict__ 
         // become trial-division candidates (class 1: < 2^32, class 2: >= 2^32)
         uint32_t clsbits = 0;  // 2 bits per element: 1 -> list32, 2 -> list64
         uint8_t r[8];
+        uint32_t word[8];
+        uint32_t inmask = 0;
+#pragma unroll
+        for (int e = 0; e < 8; e++) {  // all eight bitmap reads in flight together
+            const unsigned long long d = v[e] - wlo;
+            const bool inwin = ((uint32_t)v[e] & 1u) && d < span;
+            inmask |= (uint32_t)inwin << e;
+            word[e] = inwin ? __ldg(bitmap + ((uint32_t)d >> 6)) : 0u;
+        }
 #pragma unroll
         for (int e = 0; e < 8; e++) {
             const unsigned long long x = v[e];
             const uint32_t xlo = (uint32_t)x, xhi = (uint32_t)(x >> 32);
-            const unsigned long long d = x - wlo;
             const bool odd = xlo & 1u;
-            const bool inwin = odd && d < span;
-            const uint32_t d32 = (uint32_t)d;
-            const uint32_t word = inwin ? __ldg(bitmap + (d32 >> 6)) : 0u;
-            const uint32_t bit = (word >> ((d32 >> 1) & 31u)) & 1u;
+            const bool inwin = (inmask >> e) & 1u;
+            const uint32_t d32 = xlo - (uint32_t)wlo;
+            const uint32_t bit = (word[e] >> ((d32 >> 1) & 31u)) & 1u;
             const bool two = (xlo == 2u) && (xhi == 0u);
             r[e] = (uint8_t)(inwin ? bit : (uint32_t)two);
             uint32_t cls = (odd && !inwin && (xhi != 0u || xlo > 1u)) ? (xhi != 0u ? 2u : 1u) : 0u;
