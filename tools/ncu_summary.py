@@ -1,0 +1,104 @@
+"""Summarise an ncu --set full report into profiles/.
+
+    python tools/ncu_summary.py gpurun_out/prof_C5.ncu-rep profiles/r1_ncu_C5_v3
+
+Writes <dir>/full_summary.json (the metrics the roofline discussion cites, per
+kernel, averaged over the captured launches) and refreshes
+profiles/ncu_traffic.json (DRAM bytes read + written per launch, keyed by the
+short kernel names bench.py uses).  Reads the report with `ncu -i --page raw`.
+"""
+import csv
+import io
+import json
+import os
+import subprocess
+import sys
+
+KEYS = [
+    "gpu__time_duration.sum",
+    "dram__bytes_read.sum",
+    "dram__bytes_write.sum",
+    "sm__pipe_fmaheavy_cycles_active.avg.pct_of_peak_sustained_elapsed",
+    "sm__pipe_fma_cycles_active.avg.pct_of_peak_sustained_active",
+    "sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active",
+    "sm__pipe_alu_cycles_active.avg.pct_of_peak_sustained_active",
+    "sm__inst_executed_pipe_lsu.avg.pct_of_peak_sustained_active",
+    "sm__inst_executed.avg.per_cycle_active",
+    "smsp__issue_active.avg.pct_of_peak_sustained_active",
+    "sm__warps_active.avg.pct_of_peak_sustained_active",
+    "smsp__thread_inst_executed_per_inst_executed.ratio",
+    "launch__registers_per_thread",
+    "launch__grid_size",
+    "launch__block_size",
+    "gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed",
+    "l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum",
+    "smsp__average_warps_issue_stalled_long_scoreboard_per_issue_active.ratio",
+    "smsp__average_warps_issue_stalled_wait_per_issue_active.ratio",
+    "smsp__average_warps_issue_stalled_math_pipe_throttle_per_issue_active.ratio",
+    "smsp__average_warps_issue_stalled_short_scoreboard_per_issue_active.ratio",
+    "smsp__average_warps_issue_stalled_not_selected_per_issue_active.ratio",
+    "smsp__average_warps_issue_stalled_barrier_per_issue_active.ratio",
+    "sm__cycles_elapsed.avg.per_second",
+]
+
+SHORT = {"mr1_kernel": "mr1", "mr2_kernel": "mr2", "classify_kernel": "classify", "sieve_kernel": "sieve",
+         "qscatter_kernel": "sort", "plan_kernel": "plan", "gather_kernel": "classify"}
+
+SCALE = {"byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12}
+
+
+def short_name(full):
+    base = full.split("(")[0].split("<")[0].replace("void ", "").strip()
+    return SHORT.get(base, base), base
+
+
+def main():
+    rep, outdir = sys.argv[1], sys.argv[2]
+    raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True, check=True).stdout
+    rows = list(csv.reader(io.StringIO(raw)))
+    hdr, units, data = rows[0], rows[1], rows[2:]
+    col = {h: i for i, h in enumerate(hdr)}
+    per = {}
+    for d in data:
+        sname, base = short_name(d[col["Kernel Name"]])
+        ent = per.setdefault(base, {"short": sname, "launches": 0, "sum": {}, "unit": {}})
+        ent["launches"] += 1
+        for k in KEYS:
+            if k not in col:
+                continue
+            try:
+                v = float(d[col[k]].replace(",", ""))
+            except ValueError:
+                continue
+            ent["sum"][k] = ent["sum"].get(k, 0.0) + v
+            ent["unit"][k] = units[col[k]]
+    summary, traffic = {}, {}
+    for base, ent in per.items():
+        n = ent["launches"]
+        s = {"short": ent["short"], "launches_captured": n}
+        for k, v in ent["sum"].items():
+            s[k] = f"{v / n:.6g} {ent['unit'][k]}".strip()
+        rb = ent["sum"].get("dram__bytes_read.sum", 0.0) / n * SCALE.get(ent["unit"].get("dram__bytes_read.sum", "byte"), 1)
+        wb = ent["sum"].get("dram__bytes_write.sum", 0.0) / n * SCALE.get(ent["unit"].get("dram__bytes_write.sum", "byte"), 1)
+        s["dram_bytes_per_launch"] = rb + wb
+        summary[base] = s
+        traffic[ent["short"]] = rb + wb
+    os.makedirs(outdir, exist_ok=True)
+    with open(os.path.join(outdir, "full_summary.json"), "w") as f:
+        json.dump(summary, f, indent=1)
+    tpath = os.path.join(os.path.dirname(os.path.abspath(__file__)), "..", "profiles", "ncu_traffic.json")
+    old = {}
+    if os.path.exists(tpath):
+        old = json.load(open(tpath))
+    old.update({k: v for k, v in traffic.items()})
+    old["_source"] = os.path.relpath(os.path.join(outdir, "full_summary.json"),
+                                     os.path.join(os.path.dirname(tpath)))
+    with open(tpath, "w") as f:
+        json.dump(old, f, indent=1)
+    print(json.dumps({k: {kk: vv for kk, vv in v.items() if kk in ("short", "gpu__time_duration.sum",
+                      "sm__pipe_fmaheavy_cycles_active.avg.pct_of_peak_sustained_elapsed", "dram_bytes_per_launch")}
+                      for k, v in summary.items()}, indent=1))
+
+
+if __name__ == "__main__":
+    main()
