@@ -846,6 +846,11 @@ __device__ __forceinline__ bool sort_pays(const unsigned int* bins, int nb) {
         unsigned long long lo = 0;
         for (int b = 0; b <= 49; b++) lo += bins[b];
         if (lo > cnt / 64 && lo < cnt - cnt / 64) return true;
+        // both sides of 2^63 (bit length 63 | 64): the base-2 ladder fuses its
+        // doubling into the reduction only below 2^63, chosen per warp
+        lo = 0;
+        for (int b = 0; b <= 63; b++) lo += bins[b];
+        if (lo > cnt / 64 && lo < cnt - cnt / 64) return true;
     }
     return false;
 }

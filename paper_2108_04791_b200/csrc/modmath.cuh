@@ -233,6 +233,102 @@ __device__ __forceinline__ uint64_t msqr64_ptx(uint64_t x, uint64_t n, uint64_t 
     return r;
 }
 
+// One step of the base-2 ladder, x <- x^2 * 2^b (b in {0, 1}), as a single
+// reduction: REDC(x^2 << b).  ModMultiply case 3 (the
+// multiplication by a = 2) becomes a one-bit funnel shift of the 128-bit
+// square instead of a separate modular doubling.  Valid for n < 2^63: then
+// x^2 * 2 < 2 n^2 < n R, so the subtraction REDC still lands in (-n, n) and
+// needs the single "+ n on borrow" correction.  sm_100a: 8 IMAD.WIDE + 2 IMAD
+// on the FMA-heavy pipe; the shift is 4 SHF on the ALU pipe, replacing the
+// ~10 ALU instructions of compare / subtract / select of a modular doubling.
+__device__ __forceinline__ uint64_t msqr64_shl_ptx(uint64_t x, uint64_t n, uint64_t ninv, uint32_t b) {
+    uint64_t r;
+    asm("{\n\t"
+        ".reg .u32 x0, x1, n0, n1, i0, i1, p0, p1, c0, c1, h0, h1, t1, t2, t3, m0, m1;\n\t"
+        ".reg .u32 q0, q1, a0, a1, b0, b1, d0, d1, u2, u3, r0, r1, bw, k0, k1;\n\t"
+        ".reg .u64 W;\n\t"
+        "mov.b64 {x0, x1}, %1;\n\t"
+        "mov.b64 {n0, n1}, %2;\n\t"
+        "mov.b64 {i0, i1}, %3;\n\t"
+        "mul.wide.u32 W, x0, x0;\n\t"
+        "mov.b64 {p0, p1}, W;\n\t"
+        "mul.wide.u32 W, x0, x1;\n\t"
+        "mov.b64 {c0, c1}, W;\n\t"
+        "mul.wide.u32 W, x1, x1;\n\t"
+        "mov.b64 {h0, h1}, W;\n\t"
+        "add.cc.u32 t1, p1, c0;\n\t"
+        "addc.cc.u32 t2, h0, c1;\n\t"
+        "addc.u32 t3, h1, 0;\n\t"
+        "add.cc.u32 t1, t1, c0;\n\t"
+        "addc.cc.u32 t2, t2, c1;\n\t"
+        "addc.u32 t3, t3, 0;\n\t"
+        // T <<= b  (T < 2^127 because x < n < 2^63)
+        "shf.l.clamp.b32 t3, t2, t3, %4;\n\t"
+        "shf.l.clamp.b32 t2, t1, t2, %4;\n\t"
+        "shf.l.clamp.b32 t1, p0, t1, %4;\n\t"
+        "shl.b32 p0, p0, %4;\n\t"
+        "mul.wide.u32 W, p0, i0;\n\t"
+        "mov.b64 {m0, m1}, W;\n\t"
+        "mad.lo.u32 m1, p0, i1, m1;\n\t"
+        "mad.lo.u32 m1, t1, i0, m1;\n\t"
+        "mul.wide.u32 W, m0, n0;\n\t"
+        "mov.b64 {q0, q1}, W;\n\t"
+        "mul.wide.u32 W, m0, n1;\n\t"
+        "mov.b64 {a0, a1}, W;\n\t"
+        "mul.wide.u32 W, m1, n0;\n\t"
+        "mov.b64 {b0, b1}, W;\n\t"
+        "mul.wide.u32 W, m1, n1;\n\t"
+        "mov.b64 {d0, d1}, W;\n\t"
+        "add.cc.u32 q1, q1, a0;\n\t"
+        "addc.cc.u32 u2, d0, a1;\n\t"
+        "addc.u32 u3, d1, 0;\n\t"
+        "add.cc.u32 q1, q1, b0;\n\t"
+        "addc.cc.u32 u2, u2, b1;\n\t"
+        "addc.u32 u3, u3, 0;\n\t"
+        "sub.cc.u32 r0, t2, u2;\n\t"
+        "subc.cc.u32 r1, t3, u3;\n\t"
+        "subc.u32 bw, 0, 0;\n\t"
+        "and.b32 k0, n0, bw;\n\t"
+        "and.b32 k1, n1, bw;\n\t"
+        "add.cc.u32 r0, r0, k0;\n\t"
+        "addc.u32 r1, r1, k1;\n\t"
+        "mov.b64 %0, {r0, r1};\n\t"
+        "}"
+        : "=l"(r)
+        : "l"(x), "l"(n), "l"(ninv), "r"(b));
+    return r;
+}
+
+// Conditional modular doubling x <- b ? 2x mod n : x for any odd n < 2^64
+// (ModAdd Property 1 with a = b = x, as one carry chain): s = x +
+// (x & -b) with carry, t = s - n with borrow; t is the answer unless the sum
+// did not carry and t borrowed (then s < n).
+__device__ __forceinline__ uint64_t mdbl64_if_ptx(uint64_t x, uint64_t n, uint32_t b) {
+    uint64_t r;
+    asm("{\n\t"
+        ".reg .u32 x0, x1, n0, n1, mk, a0, a1, s0, s1, t0, t1, c, k0, k1;\n\t"
+        "mov.b64 {x0, x1}, %1;\n\t"
+        "mov.b64 {n0, n1}, %2;\n\t"
+        "neg.s32 mk, %3;\n\t"
+        "and.b32 a0, x0, mk;\n\t"
+        "and.b32 a1, x1, mk;\n\t"
+        "add.cc.u32 s0, x0, a0;\n\t"
+        "addc.cc.u32 s1, x1, a1;\n\t"
+        "addc.u32 c, 0, 0;\n\t"
+        "sub.cc.u32 t0, s0, n0;\n\t"
+        "subc.cc.u32 t1, s1, n1;\n\t"
+        "subc.u32 c, c, 0;\n\t"          // carry - borrow: 0 -> t, -1 -> s (+1 cannot occur)
+        "and.b32 k0, n0, c;\n\t"
+        "and.b32 k1, n1, c;\n\t"
+        "add.cc.u32 t0, t0, k0;\n\t"
+        "addc.u32 t1, t1, k1;\n\t"
+        "mov.b64 %0, {t0, t1};\n\t"
+        "}"
+        : "=l"(r)
+        : "l"(x), "l"(n), "r"(b));
+    return r;
+}
+
 // ModAdd, Property 1: a + b mod n = a - (n - b) when a >= n - b.
 __device__ __forceinline__ uint64_t madd64(uint64_t a, uint64_t b, uint64_t n) {
     uint64_t nb = n - b;

@@ -103,11 +103,25 @@ __device__ __forceinline__ bool sprp2_64(uint64_t n) {
     const int s = __ffsll((long long)d) - 1;
     d >>= s;
     const int top = 63 - __clzll((long long)d);
-    uint64_t x = mdbl64(M.one, n);  // mont(2)
-    for (int b = top - 1; b >= 0; b--) {
-        x = msqr64_ptx(x, M.n, M.ninv);
-        const uint64_t y = mdbl64(x, n);
-        x = ((d >> b) & 1ull) ? y : x;
+    uint64_t x = mdbl64(M.one, n);  // mont(2): the leading bit of d
+    if (top > 0) {
+        // remaining bits of d, most significant first, from the top of dd
+        uint64_t dd = d << (64 - top);
+        // warp-uniform choice (queues are ordered by bit length, so warps
+        // rarely straddle 2^63): fused square-and-double below 2^63
+        if (!__any_sync(__activemask(), (unsigned)(n >> 63))) {
+#pragma unroll 2
+            for (int k = 0; k < top; k++) {
+                x = msqr64_shl_ptx(x, n, M.ninv, (uint32_t)(dd >> 63));
+                dd += dd;
+            }
+        } else {
+#pragma unroll 2
+            for (int k = 0; k < top; k++) {
+                x = mdbl64_if_ptx(msqr64_ptx(x, n, M.ninv), n, (uint32_t)(dd >> 63));
+                dd += dd;
+            }
+        }
     }
     if (x == M.one || x == M.mone) return true;
     for (int r = 1; r < s; r++) {
@@ -158,10 +172,10 @@ __device__ __forceinline__ bool sprp_lockstep64(const Mont64& M, uint64_t R2, ui
 #pragma unroll
         for (int j = 0; j < WIN; j++) {
 #pragma unroll
-            for (int i = 0; i < NB; i++) x[i] = msqr64(x[i], M);
+            for (int i = 0; i < NB; i++) x[i] = msqr64_ptx(x[i], n, M.ninv);
         }
 #pragma unroll
-        for (int i = 0; i < NB; i++) x[i] = mmul64(x[i], sel_table<T>(tab[i], digit, M.one), M);
+        for (int i = 0; i < NB; i++) x[i] = mmul64_ptx(x[i], sel_table<T>(tab[i], digit, M.one), n, M.ninv);
     }
 #pragma unroll
     for (int i = 0; i < NB; i++) {

@@ -106,6 +106,28 @@ def test_all_below_2_20_every_path():
     assert exp.sum() == 82025
 
 
+@pytest.mark.parametrize("count", [3000, 300_000])
+def test_base2_ladder_around_2_63(count):
+    """The base-2 ladder fuses its doubling into the reduction below 2^63 and
+    uses the separate conditional doubling at or above it, chosen per warp.
+    Odd values on both sides of 2^63 -- warps entirely below, entirely above
+    and mixed (interleaved), in short arrays (queue left unsorted) and long
+    ones (queue sorted by bit length) -- plus primes found by the oracle next
+    to 2^62, 2^63 and 2^64, must equal the oracle bit for bit."""
+    rng = np.random.default_rng(63)
+    lo = rng.integers(1 << 62, 1 << 63, size=count, dtype=np.uint64) | np.uint64(1)
+    hi = (rng.integers(0, 1 << 63, size=count, dtype=np.uint64) | np.uint64(1 << 63)) | np.uint64(1)
+    mixed = np.empty(2 * count, dtype=np.uint64)
+    mixed[0::2], mixed[1::2] = lo, hi
+    near = []
+    for c in ((1 << 62), (1 << 63), (1 << 64) - 1):
+        cand = np.array([c - k for k in range(1, 4000, 2)] + [c + k for k in range(1, 4000, 2) if c + k < (1 << 64)],
+                        dtype=np.uint64)
+        near.append(cand[oracle.isprime(cand) == 1])
+    N = np.concatenate([lo, hi, mixed] + near)
+    assert_same(gpu(N), oracle.isprime(N), N)
+
+
 # ------------------------------------------------------------------ configs, reduced sizes (bit-exact)
 @pytest.mark.parametrize("cfg,count", [("C1", 100_000), ("C2", (1 << 20) + 777), ("C3", (1 << 18) + 3),
                                        ("C5", (1 << 20) + 4097)])
