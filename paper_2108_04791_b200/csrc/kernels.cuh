@@ -557,6 +557,9 @@ classify_kernel(const unsigned long long* __restrict__ N, uint8_t* __restrict__ 
     __shared__ ClsSmem sm;
     const unsigned long long wlo = plan->wlo, whi = plan->whi;
     const unsigned long long span = whi - wlo;  // <= 2^32 (0: no window)
+    // 32-bit form of the window test for values below 2^32: (lo - wlo) mod 2^32
+    // <= span - 1 (whi <= 2^32, so values below wlo wrap past the span)
+    const uint32_t wlo32 = (uint32_t)wlo, spanm1 = (uint32_t)(span - 1);
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
     ClsWarp& ws = sm.w[wid];
     const uint32_t ntiles = (len + CLS_TILE - 1) / CLS_TILE;
@@ -581,9 +584,51 @@ classify_kernel(const unsigned long long* __restrict__ N, uint8_t* __restrict__ 
                 v[e] = i < len ? N[i] : 0ull;
             }
         }
+        // ---- window fast path: the whole warp-tile lies below 2^32 and inside
+        // the window (a dense or clustered range, config C4).  Then out[i] =
+        // bit(N[i]) for odd values and (N[i] == 2) for even ones -- about a
+        // third of the general path's instructions, so the pass stays on the
+        // HBM roofline.  Warp-uniform (vote), so no lane diverges.
+        bool fast = false;
+        if (full && vec_out && span != 0) {
+            uint32_t hor = 0;
+#pragma unroll
+            for (int e = 0; e < 8; e++) hor |= (uint32_t)(v[e] >> 32);
+            if (__all_sync(0xffffffffu, hor == 0u)) {
+                uint32_t dd[8];
+                bool in = true;
+#pragma unroll
+                for (int e = 0; e < 8; e++) {
+                    dd[e] = (uint32_t)v[e] - wlo32;
+                    in &= dd[e] <= spanm1;
+                }
+                fast = __all_sync(0xffffffffu, in);
+                if (fast) {
+                    uint32_t w[8];
+#pragma unroll
+                    for (int e = 0; e < 8; e++) w[e] = __ldg(bitmap + (dd[e] >> 6));
+#pragma unroll
+                    for (int j = 0; j < 4; j++) {
+                        uint32_t b2 = 0;
+#pragma unroll
+                        for (int k = 0; k < 2; k++) {
+                            const int e = 2 * j + k;
+                            const uint32_t lo = (uint32_t)v[e];
+                            // bit (dd >> 1) & 31 of the word <-> odd value wlo + dd; even values read 0 (lo & 1)
+                            uint32_t bit = __funnelshift_r(w[e], w[e], dd[e] >> 1) & lo & 1u;
+                            bit = lo == 2u ? 1u : bit;
+                            b2 |= bit << (8 * k);
+                        }
+                        __stcs(reinterpret_cast<unsigned short*>(out + wbase + 2 * lane + 64 * j), (unsigned short)b2);
+                    }
+                }
+            }
+        }
         // branch-free per element: odd values inside the window read their bit,
         // even values are prime only when equal to 2, other odd values >= 3
         // become trial-division candidates (class 1: < 2^32, class 2: >= 2^32)
+        uint32_t s32 = 0, s64 = 0, wtot = 0, n32 = 0, n64 = 0;
+        if (!fast) {
         uint32_t clsbits = 0;  // 2 bits per element: 1 -> list32, 2 -> list64
         uint8_t r[8];
         uint32_t word[8];
@@ -621,9 +666,9 @@ classify_kernel(const unsigned long long* __restrict__ N, uint8_t* __restrict__ 
             const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
             if (lane >= o) incl += y;
         }
-        const uint32_t wtot = __shfl_sync(0xffffffffu, incl, 31);
-        const uint32_t n32 = wtot & 0xFFFFu, n64 = wtot >> 16;
-        uint32_t s32 = 0, s64 = 0;
+        wtot = __shfl_sync(0xffffffffu, incl, 31);
+        n32 = wtot & 0xFFFFu;
+        n64 = wtot >> 16;
         if (wtot == 0) {
             // warp fast path: results straight from registers
             if (full && vec_out) {
@@ -685,6 +730,7 @@ classify_kernel(const unsigned long long* __restrict__ N, uint8_t* __restrict__ 
                 s64 += __popc(m);
             }
         }
+        }  // !fast
         // ---- queue reservation: one barrier (two if this block tile has survivors)
         if (lane == 0) { sm.cnt[wid][0] = s32; sm.cnt[wid][1] = s64; }
         if (__syncthreads_or((int)(s32 | s64))) {
