@@ -403,6 +403,34 @@ __device__ __forceinline__ double fmulmod(double a, double b, const ModF& M) {
     return r < 0.0 ? r + M.n : r;
 }
 
+// Lazy signed product for the witness loops: a, b exact integers with |a| <
+// 2n, |b| < n (n < 2^49).  Returns the signed representative r == a*b (mod n)
+// with |r| < 0.75 n -- no final correction, because the next square does not
+// care about the sign and every later product accepts |.| < n.
+//   h + l = a b exactly (|ab| < 2 n^2 < 2^99, |l| <= ulp(h)/2 <= n 2^-52 * n);
+//   q = round(h * fl(1/n)) in one FMA with the 1.5 * 2^52 addend:
+//       |q - ab/n| <= 1/2 + |l|/n + (h/n) 2^-53 < 3/4;
+//   r = fma(-q, n, h) + l: both steps exact (|h - qn| < n + |l| < 2^50).
+// 7 FP64-pipe instructions for a square-and-double step (fsqr_lazy with f = 2)
+// against 10 FP64 + 4 select/compare instructions for fmulmod + faddmod.
+__device__ __forceinline__ double fmul_lazy(double a, double b, const ModF& M) {
+    const double h = a * b;
+    const double l = fma(a, b, -h);
+    const double q = fma(h, M.ninv, FP_RND) - FP_RND;
+    return fma(-q, M.n, h) + l;
+}
+
+// x^2 * 2^b for the base-2 ladder (ModMultiply case 3 folded in as an exact
+// power-of-two scaling of one factor).  |x| < n, b in {0, 1}.
+__device__ __forceinline__ double fsqr_dbl_lazy(double x, uint32_t b, const ModF& M) {
+    const double f = __hiloint2double(0x3FF00000 + (int)(b << 20), 0);  // 1.0 or 2.0
+    return fmul_lazy(x * f, x, M);
+}
+
+// Signed representative -> congruence tests (|x| < n).
+__device__ __forceinline__ bool f_is_one(double x, const ModF& M) { return x == 1.0 || x == 1.0 - M.n; }
+__device__ __forceinline__ bool f_is_mone(double x, const ModF& M) { return x == -1.0 || x == M.nm1; }
+
 // ModAdd in doubles: a + b < 2n < 2^50 is exact.
 __device__ __forceinline__ double faddmod(double a, double b, const ModF& M) {
     const double s = a + b;

@@ -217,24 +217,29 @@ __device__ __forceinline__ bool sprp_multi64(uint64_t n, const unsigned long lon
 
 // ------------------------------------------------------- FP64 class ----
 // The same two phases on the FP64 pipe for odd n < 2^49 (modmath.cuh, ModF):
-// plain residues (no Montgomery form), so 1 and -1 are 1.0 and n - 1.
+// plain residues (no Montgomery form) kept as signed lazy representatives
+// |x| < n, so 1 is 1.0 or 1 - n and -1 is -1.0 or n - 1.
 __device__ __forceinline__ bool sprp2_f64(unsigned long long n) {
     const ModF M = modf_setup(n);
     unsigned long long d = n - 1;
     const int s = __ffsll((long long)d) - 1;
     d >>= s;
     const int top = 63 - __clzll((long long)d);
+    // signed lazy residues (fmul_lazy): |x| < n throughout, no per-step correction
     double x = 2.0;  // top bit of d
-    for (int b = top - 1; b >= 0; b--) {
-        x = fmulmod(x, x, M);
-        const double y = faddmod(x, x, M);  // * 2 (ModMultiply case 3)
-        x = ((d >> b) & 1ull) ? y : x;
+    if (top > 0) {
+        unsigned long long dd = d << (64 - top);  // remaining bits, MSB first
+#pragma unroll 2
+        for (int k = 0; k < top; k++) {
+            x = fsqr_dbl_lazy(x, (uint32_t)(dd >> 63), M);
+            dd += dd;
+        }
     }
-    if (x == 1.0 || x == M.nm1) return true;
+    if (f_is_one(x, M) || f_is_mone(x, M)) return true;
     for (int r = 1; r < s; r++) {
-        x = fmulmod(x, x, M);
-        if (x == M.nm1) return true;
-        if (x == 1.0) return false;
+        x = fmul_lazy(x, x, M);
+        if (f_is_mone(x, M)) return true;
+        if (f_is_one(x, M)) return false;
     }
     return false;
 }
@@ -262,7 +267,7 @@ __device__ __forceinline__ bool sprp_lockstep_f64(const ModF& M, unsigned long l
         done[i] = pass[i] = (a == 0);
         tab[i][0] = (double)a;
 #pragma unroll
-        for (int k = 1; k < T; k++) tab[i][k] = fmulmod(tab[i][k - 1], tab[i][0], M);
+        for (int k = 1; k < T; k++) tab[i][k] = fmul_lazy(tab[i][k - 1], tab[i][0], M);
     }
     {
         const uint32_t lead = (uint32_t)(d >> (WIN * (nw - 1)));
@@ -274,23 +279,23 @@ __device__ __forceinline__ bool sprp_lockstep_f64(const ModF& M, unsigned long l
 #pragma unroll
         for (int j = 0; j < WIN; j++) {
 #pragma unroll
-            for (int i = 0; i < NB; i++) x[i] = fmulmod(x[i], x[i], M);
+            for (int i = 0; i < NB; i++) x[i] = fmul_lazy(x[i], x[i], M);
         }
 #pragma unroll
-        for (int i = 0; i < NB; i++) x[i] = fmulmod(x[i], sel_table_f<T>(tab[i], digit), M);
+        for (int i = 0; i < NB; i++) x[i] = fmul_lazy(x[i], sel_table_f<T>(tab[i], digit), M);
     }
 #pragma unroll
     for (int i = 0; i < NB; i++) {
-        if (!done[i] && (x[i] == 1.0 || x[i] == M.nm1)) done[i] = pass[i] = true;
+        if (!done[i] && (f_is_one(x[i], M) || f_is_mone(x[i], M))) done[i] = pass[i] = true;
     }
     for (int r = 1; r < s; r++) {
         bool all = true;
 #pragma unroll
         for (int i = 0; i < NB; i++) {
             if (!done[i]) {
-                x[i] = fmulmod(x[i], x[i], M);
-                if (x[i] == M.nm1) done[i] = pass[i] = true;
-                else if (x[i] == 1.0) done[i] = true;
+                x[i] = fmul_lazy(x[i], x[i], M);
+                if (f_is_mone(x[i], M)) done[i] = pass[i] = true;
+                else if (f_is_one(x[i], M)) done[i] = true;
             }
             all &= done[i];
         }
