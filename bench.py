@@ -42,10 +42,11 @@ UNIT = "Gints/s"
 #     (a squaring needs 3 WIDE for a^2 -> 16; the multiply count below does not
 #      separate squarings, so 18 is a conservative, i.e. higher, work figure)
 #   32-bit Montgomery: 1 WIDE + 1 IMAD + 1 HI -> 5 FMA-heavy slots
-#   FP64 (n < 2^49): DMUL, DFMA, DMUL, 2 DADD (rounding), DFMA, DADD, DADD -> 8 FP64 lane-ops
+#   FP64 (n < 2^49), lazy signed residues: DMUL (h), DFMA (l), DFMA + DADD (q), DFMA + DADD (r)
+#     -> 6 FP64 lane-ops (modmath.cuh fmul_lazy)
 SLOTS_MULMOD64 = 18
 SLOTS_MULMOD32 = 5
-FP64_OPS_MULMOD = 8
+FP64_OPS_MULMOD = 6
 LANES_PER_CLK_SM = 64  # FMA-heavy and FP64 pipes: 16 lanes/clk per SMSP x 4 (B300_MICROARCH.md; measured 63.2 / 63.1)
 HBM_BYTES_PER_ELEM = 9      # 8-B value read + 1-B result written
 
@@ -201,19 +202,21 @@ def kernel_profile(isp, torch, dN, dout, n, steps, stream):
     return per_step, st, step_ms
 
 
-def roofline(kern_ms, stats, n, steps, peaks, peaks_kind, clocks):
+def roofline(kern_ms, stats, n, steps, peaks, peaks_kind, clocks, cfg=None):
     """Roofline of the dominant kernel (largest share of the step)."""
     if not kern_ms:
         return None
     name = max(kern_ms, key=kern_ms.get)
     ms = kern_ms[name]
-    traffic = None
-    tpath = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    traffic, ncu = None, None
+    tpath = os.path.join(ROOT, "profiles", "ncu_kernel_metrics.json")
     if os.path.exists(tpath):
         try:
-            traffic = json.load(open(tpath)).get(name)
+            allm = json.load(open(tpath))
+            ncu = allm.get(f"{name}@{cfg}") or allm.get(name)
+            traffic = ncu["dram_bytes_per_launch"] if ncu else None
         except Exception:
-            traffic = None
+            traffic, ncu = None, None
     if name in ("mr1", "mr2"):
         mm, mf = stats["mulmods"], stats["mulmods_fp64"]
         k = 0 if name == "mr1" else 2
@@ -225,7 +228,7 @@ def roofline(kern_ms, stats, n, steps, peaks, peaks_kind, clocks):
         peak = 148 * LANES_PER_CLK_SM * mhz * 1e6 / 1e12
         return {"kernel": name, "bound": "alu", "achieved": round(achieved, 4), "peak": round(peak, 3),
                 "unit": "T lane-slots/s (busiest of FMA-heavy / FP64 pipe)", "frac": round(achieved / peak, 4),
-                "traffic": traffic,
+                "traffic": traffic, "ncu": ncu,
                 "peak_source": f"derived: 148 SMs x {LANES_PER_CLK_SM} lanes/clk x {mhz:.0f} MHz "
                                "(B300_MICROARCH.md pipe rates; MEASURED_PEAKS sm_max_mhz)",
                 "work": f"per step: {fma_slots / steps:.4g} FMA-heavy slots ({SLOTS_MULMOD32}/32-bit, {SLOTS_MULMOD64}/64-bit "
@@ -240,7 +243,7 @@ def roofline(kern_ms, stats, n, steps, peaks, peaks_kind, clocks):
     achieved = nbytes / (ms * 1e-3) / 1e9
     peak = float(peaks.get("hbm_gbs", 6650.0))
     return {"kernel": name, "bound": "hbm", "achieved": round(achieved, 2), "peak": peak, "unit": "GB/s",
-            "frac": round(achieved / peak, 4), "traffic": traffic, "peak_source": f"{peaks_kind} hbm_gbs",
+            "frac": round(achieved / peak, 4), "traffic": traffic, "ncu": ncu, "peak_source": f"{peaks_kind} hbm_gbs",
             "work": f"{nbytes:.4g} algorithmic bytes per step", "ms_per_step": round(ms, 4)}
 
 
@@ -300,7 +303,7 @@ def config_block(cfg, world):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--steps", type=int, default=40)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--config", default="C5", choices=sorted(workloads.CONFIGS))
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
@@ -363,7 +366,7 @@ def main():
     correct = (my_count == counts[cfg]) if rank == 0 else None
 
     kern_ms, st, inst_ms = kernel_profile(isp, torch, dN, dout, n, args.steps, stream)
-    roof = roofline(kern_ms, st, n, args.steps, peaks, peaks_kind, clocks)
+    roof = roofline(kern_ms, st, n, args.steps, peaks, peaks_kind, clocks, cfg)
 
     e2e = None
     if not args.no_e2e:
@@ -421,7 +424,7 @@ def main():
                 isp.isprime_popcount_device(cout, dcount, cn, stream)
                 torch.cuda.synchronize()
                 ckm, cst, _ = kernel_profile(isp, torch, cN, cout, cn, csteps, stream)
-                croof = roofline(ckm, cst, cn, csteps, peaks, peaks_kind, clocks)
+                croof = roofline(ckm, cst, cn, csteps, peaks, peaks_kind, clocks, c)
                 per[c] = {"value": round(cn / (cms * 1e-3) / 1e9, 4), "unit": UNIT, "ms_per_step": round(cms, 4),
                           "n": cn, "correct": int(dcount.item()) == counts[c], "gpu_launches_per_step": cl / csteps,
                           "kernels_ms_per_step": {k: round(v, 4) for k, v in ckm.items()}, "roofline": croof}

@@ -4,8 +4,8 @@
 
 Writes <dir>/full_summary.json (the metrics the roofline discussion cites, per
 kernel, averaged over the captured launches) and refreshes
-profiles/ncu_traffic.json (DRAM bytes read + written per launch, keyed by the
-short kernel names bench.py uses).  Reads the report with `ncu -i --page raw`.
+profiles/ncu_kernel_metrics.json (per short kernel name bench.py uses: DRAM
+bytes read + written per launch and the pipe utilisations of the capture).  Reads the report with `ncu -i --page raw`.
 """
 import csv
 import io
@@ -72,7 +72,7 @@ def main():
                 continue
             ent["sum"][k] = ent["sum"].get(k, 0.0) + v
             ent["unit"][k] = units[col[k]]
-    summary, traffic = {}, {}
+    summary = {}
     for base, ent in per.items():
         n = ent["launches"]
         s = {"short": ent["short"], "launches_captured": n}
@@ -82,17 +82,25 @@ def main():
         wb = ent["sum"].get("dram__bytes_write.sum", 0.0) / n * SCALE.get(ent["unit"].get("dram__bytes_write.sum", "byte"), 1)
         s["dram_bytes_per_launch"] = rb + wb
         summary[base] = s
-        traffic[ent["short"]] = rb + wb
     os.makedirs(outdir, exist_ok=True)
     with open(os.path.join(outdir, "full_summary.json"), "w") as f:
         json.dump(summary, f, indent=1)
-    tpath = os.path.join(os.path.dirname(os.path.abspath(__file__)), "..", "profiles", "ncu_traffic.json")
-    old = {}
-    if os.path.exists(tpath):
-        old = json.load(open(tpath))
-    old.update({k: v for k, v in traffic.items()})
-    old["_source"] = os.path.relpath(os.path.join(outdir, "full_summary.json"),
-                                     os.path.join(os.path.dirname(tpath)))
+    tpath = os.path.join(os.path.dirname(os.path.abspath(__file__)), "..", "profiles", "ncu_kernel_metrics.json")
+    old = json.load(open(tpath)) if os.path.exists(tpath) else {}
+    src = os.path.relpath(os.path.join(outdir, "full_summary.json"), os.path.dirname(tpath))
+    for base, s in summary.items():
+        def pct(k):
+            v = s.get(k)
+            return float(v.split()[0]) if v else None
+        old[s["short"]] = {
+            "dram_bytes_per_launch": s["dram_bytes_per_launch"],
+            "fmaheavy_pipe_pct": pct("sm__pipe_fmaheavy_cycles_active.avg.pct_of_peak_sustained_elapsed"),
+            "fp64_pipe_pct": pct("sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active"),
+            "alu_pipe_pct": pct("sm__pipe_alu_cycles_active.avg.pct_of_peak_sustained_active"),
+            "issue_active_pct": pct("smsp__issue_active.avg.pct_of_peak_sustained_active"),
+            "dram_pct": pct("gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed"),
+            "source": src,
+        }
     with open(tpath, "w") as f:
         json.dump(old, f, indent=1)
     print(json.dumps({k: {kk: vv for kk, vv in v.items() if kk in ("short", "gpu__time_duration.sum",
