@@ -560,6 +560,7 @@ classify_kernel(const unsigned long long* __restrict__ N, uint8_t* __restrict__ 
     // 32-bit form of the window test for values below 2^32: (lo - wlo) mod 2^32
     // <= span - 1 (whi <= 2^32, so values below wlo wrap past the span)
     const uint32_t wlo32 = (uint32_t)wlo, spanm1 = (uint32_t)(span - 1);
+    const uint32_t spanm1w = span ? spanm1 : 0u;  // no window: only dd == 0 passes, i.e. the even value wlo
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
     ClsWarp& ws = sm.w[wid];
     const uint32_t ntiles = (len + CLS_TILE - 1) / CLS_TILE;
@@ -629,35 +630,33 @@ classify_kernel(const unsigned long long* __restrict__ N, uint8_t* __restrict__ 
         // become trial-division candidates (class 1: < 2^32, class 2: >= 2^32)
         uint32_t s32 = 0, s64 = 0, wtot = 0, n32 = 0, n64 = 0;
         if (!fast) {
-        uint32_t clsbits = 0;  // 2 bits per element: 1 -> list32, 2 -> list64
+        // 32-bit arithmetic throughout: the window lies below 2^32, so an element
+        // is inside it iff its high word is 0 and (lo - wlo) mod 2^32 <= span - 1.
+        // Elements past len were loaded as 0 (even): never a candidate.
+        uint32_t m32 = 0, m64 = 0;  // candidate masks by class (bit e)
         uint8_t r[8];
-        uint32_t word[8];
+        uint32_t word[8], dd[8];
         uint32_t inmask = 0;
 #pragma unroll
         for (int e = 0; e < 8; e++) {  // all eight bitmap reads in flight together
-            const unsigned long long d = v[e] - wlo;
-            const bool inwin = ((uint32_t)v[e] & 1u) && d < span;
+            const uint32_t xlo = (uint32_t)v[e], xhi = (uint32_t)(v[e] >> 32);
+            dd[e] = xlo - wlo32;
+            const bool inwin = (xhi == 0u) & (xlo & 1u) & (dd[e] <= spanm1w);
             inmask |= (uint32_t)inwin << e;
-            word[e] = inwin ? __ldg(bitmap + ((uint32_t)d >> 6)) : 0u;
+            word[e] = inwin ? __ldg(bitmap + (dd[e] >> 6)) : 0u;
         }
 #pragma unroll
         for (int e = 0; e < 8; e++) {
-            const unsigned long long x = v[e];
-            const uint32_t xlo = (uint32_t)x, xhi = (uint32_t)(x >> 32);
-            const bool odd = xlo & 1u;
+            const uint32_t xlo = (uint32_t)v[e], xhi = (uint32_t)(v[e] >> 32);
+            const bool small = xhi == 0u;
             const bool inwin = (inmask >> e) & 1u;
-            const uint32_t d32 = xlo - (uint32_t)wlo;
-            const uint32_t bit = (word[e] >> ((d32 >> 1) & 31u)) & 1u;
-            const bool two = (xlo == 2u) && (xhi == 0u);
-            r[e] = (uint8_t)(inwin ? bit : (uint32_t)two);
-            uint32_t cls = (odd && !inwin && (xhi != 0u || xlo > 1u)) ? (xhi != 0u ? 2u : 1u) : 0u;
-            if (!full) {
-                const uint32_t i = wbase + 2 * lane + 64 * (e >> 1) + (e & 1);
-                if (i >= len) cls = 0;
-            }
-            clsbits |= cls << (2 * e);
+            const uint32_t bit = __funnelshift_r(word[e], word[e], dd[e] >> 1) & 1u;  // 0 outside the window
+            r[e] = (uint8_t)((small && xlo == 2u) ? 1u : bit);
+            const bool cand = (xlo & 1u) && !inwin && (!small || xlo > 1u);
+            m32 |= (uint32_t)(cand && small) << e;
+            m64 |= (uint32_t)(cand && !small) << e;
         }
-        const uint32_t c32 = __popc(clsbits & 0x5555u), c64 = __popc(clsbits & 0xAAAAu);
+        const uint32_t c32 = __popc(m32), c64 = __popc(m64);
         // warp scan of the packed (c32, c64) counts
         const uint32_t packed = c32 | (c64 << 16);
         uint32_t incl = packed;
@@ -691,10 +690,9 @@ classify_kernel(const unsigned long long* __restrict__ N, uint8_t* __restrict__ 
             uint32_t p32 = ex & 0xFFFFu, p64 = ex >> 16;
 #pragma unroll
             for (int e = 0; e < 8; e++) {
-                const uint32_t cls = (clsbits >> (2 * e)) & 3u;
                 const uint8_t lp = (uint8_t)(2 * lane + 64 * (e >> 1) + (e & 1));
-                if (cls == 1) { ws.val[p32] = v[e]; ws.pos[p32] = lp; p32++; }
-                else if (cls == 2) { const uint32_t k = 255u - p64; ws.val[k] = v[e]; ws.pos[k] = lp; p64++; }
+                if ((m32 >> e) & 1u) { ws.val[p32] = v[e]; ws.pos[p32] = lp; p32++; }
+                else if ((m64 >> e) & 1u) { const uint32_t k = 255u - p64; ws.val[k] = v[e]; ws.pos[k] = lp; p64++; }
             }
             __syncwarp();
             // ---- trial division over the dense lists
