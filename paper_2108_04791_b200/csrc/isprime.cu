@@ -202,6 +202,7 @@ int init_ctx(Ctx* c) {
     CK(cudaFuncSetAttribute(sieve_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SEG_ODD));
     c->grid_sieve = c->sms * occupancy((const void*)sieve_kernel, SIEVE_THREADS, SEG_ODD);
     c->grid_cls = c->sms * occupancy((const void*)classify_kernel<24, 24>, CLS_THREADS, 0);
+    if (c->grid_cls > MAX_SEG) c->grid_cls = MAX_SEG;  // one queue segment per classify block
     c->grid_mr1 = c->sms * occupancy((const void*)mr1_kernel, MR_THREADS, 0);
     c->grid_sort = c->sms * occupancy((const void*)qscatter_kernel, SORT_THREADS, 0);
     c->grid_mr2 = c->sms * occupancy((const void*)mr2_kernel<2, false, 3>, MR_THREADS, 0);
@@ -265,12 +266,6 @@ int ensure_queues(Ctx* c, size_t cap) {
     return ISP_OK;
 }
 
-// Sort grids: one 2048-entry tile per block at most, capped at the resident grid.
-int sort_grid(int full, uint32_t len) {
-    const uint32_t need = (len + 2047) / 2048;
-    return (int)(need < (uint32_t)full ? (need ? need : 1) : (uint32_t)full);
-}
-
 // Persistent MR grids never need more blocks than the chunk could queue.
 int mr_grid(int full, uint32_t len) {
     // dynamic chunks of MR_CHUNK entries: more warps than len / MR_CHUNK would
@@ -290,24 +285,24 @@ int td_round(int v) { return v >= 32 ? 32 : v >= 24 ? 24 : v >= 16 ? 16 : v >= 8
 
 template <int A>
 void launch_classify_b(int n64, int g, cudaStream_t s, const unsigned long long* N, uint8_t* out, uint32_t len,
-                       Ctx* c, const TDParams& td, int vin, int vout) {
+                       Ctx* c, const TDParams& td, int vin, int vout, uint32_t ss) {
     switch (n64) {
-        case 32: classify_kernel<A, 32><<<g, CLS_THREADS, 0, s>>>(N, out, len, c->plan, c->bitmap, c->q, td, vin, vout); break;
-        case 24: classify_kernel<A, 24><<<g, CLS_THREADS, 0, s>>>(N, out, len, c->plan, c->bitmap, c->q, td, vin, vout); break;
-        case 16: classify_kernel<A, 16><<<g, CLS_THREADS, 0, s>>>(N, out, len, c->plan, c->bitmap, c->q, td, vin, vout); break;
-        case 8: classify_kernel<A, 8><<<g, CLS_THREADS, 0, s>>>(N, out, len, c->plan, c->bitmap, c->q, td, vin, vout); break;
-        default: classify_kernel<A, 0><<<g, CLS_THREADS, 0, s>>>(N, out, len, c->plan, c->bitmap, c->q, td, vin, vout); break;
+        case 32: classify_kernel<A, 32><<<g, CLS_THREADS, 0, s>>>(N, out, len, c->plan, c->bitmap, c->q, td, vin, vout, ss); break;
+        case 24: classify_kernel<A, 24><<<g, CLS_THREADS, 0, s>>>(N, out, len, c->plan, c->bitmap, c->q, td, vin, vout, ss); break;
+        case 16: classify_kernel<A, 16><<<g, CLS_THREADS, 0, s>>>(N, out, len, c->plan, c->bitmap, c->q, td, vin, vout, ss); break;
+        case 8: classify_kernel<A, 8><<<g, CLS_THREADS, 0, s>>>(N, out, len, c->plan, c->bitmap, c->q, td, vin, vout, ss); break;
+        default: classify_kernel<A, 0><<<g, CLS_THREADS, 0, s>>>(N, out, len, c->plan, c->bitmap, c->q, td, vin, vout, ss); break;
     }
 }
 
 void launch_classify(int n32, int n64, int g, cudaStream_t s, const unsigned long long* N, uint8_t* out,
-                     uint32_t len, Ctx* c, const TDParams& td, int vin, int vout) {
+                     uint32_t len, Ctx* c, const TDParams& td, int vin, int vout, uint32_t ss) {
     switch (n32) {
-        case 32: launch_classify_b<32>(n64, g, s, N, out, len, c, td, vin, vout); break;
-        case 24: launch_classify_b<24>(n64, g, s, N, out, len, c, td, vin, vout); break;
-        case 16: launch_classify_b<16>(n64, g, s, N, out, len, c, td, vin, vout); break;
-        case 8: launch_classify_b<8>(n64, g, s, N, out, len, c, td, vin, vout); break;
-        default: launch_classify_b<0>(n64, g, s, N, out, len, c, td, vin, vout); break;
+        case 32: launch_classify_b<32>(n64, g, s, N, out, len, c, td, vin, vout, ss); break;
+        case 24: launch_classify_b<24>(n64, g, s, N, out, len, c, td, vin, vout, ss); break;
+        case 16: launch_classify_b<16>(n64, g, s, N, out, len, c, td, vin, vout, ss); break;
+        case 8: launch_classify_b<8>(n64, g, s, N, out, len, c, td, vin, vout, ss); break;
+        default: launch_classify_b<0>(n64, g, s, N, out, len, c, td, vin, vout, ss); break;
     }
 }
 
@@ -336,7 +331,8 @@ int launch_mr2(Ctx* c, cudaStream_t s, uint8_t* out, int grid) {
 // The whole hot path for dN[0..n) on stream s.  Caller holds g_mu.
 int device_impl(Ctx* c, const unsigned long long* dN, uint8_t* dout, size_t n, cudaStream_t s) {
     const size_t chunk = (size_t)1 << g_opt.chunk_log2;
-    int rc = ensure_queues(c, n < chunk ? n : chunk);
+    // classify's per-block queue segments need up to one tile of slack per block
+    int rc = ensure_queues(c, (n < chunk ? n : chunk) + (size_t)c->grid_cls * CLS_TILE);
     if (rc != ISP_OK) return rc;
     if (c->has_last && c->last_stream != (void*)s) CK(cudaStreamWaitEvent(s, c->last_done, 0));
     PlanParams P;
@@ -371,17 +367,20 @@ int device_impl(Ctx* c, const unsigned long long* dN, uint8_t* dout, size_t n, c
         }
         const uint32_t ntiles = (len + CLS_TILE - 1) / CLS_TILE;
         const int gcls = (int)(ntiles < (uint32_t)c->grid_cls ? ntiles : (uint32_t)c->grid_cls);
+        // block b of classify owns queue entries [b * seg_stride, (b + 1) * seg_stride):
+        // at most ceil(ntiles / gcls) tiles of CLS_TILE elements each
+        const uint32_t seg_stride = ((ntiles + gcls - 1) / gcls) * CLS_TILE;
         const int vin = (((uintptr_t)N & 15) == 0) ? 1 : 0;
         const int vout = (((uintptr_t)out & 7) == 0) ? 1 : 0;
         {
             KScope ks(K_CLASSIFY, s);
-            launch_classify(td.n32, td.n64, gcls, s, N, out, len, c, td, vin, vout);
+            launch_classify(td.n32, td.n64, gcls, s, N, out, len, c, td, vin, vout, seg_stride);
             CKL("classify_kernel");
         }
         {
             KScope ks(K_SORT, s);
-            const int gs = sort_grid(c->grid_sort, len);
-            qscatter_kernel<<<gs, SORT_THREADS, 0, s>>>(c->plan, c->q);
+            const int gs = c->grid_sort < gcls ? c->grid_sort : gcls;
+            qscatter_kernel<<<gs, SORT_THREADS, 0, s>>>(c->plan, c->q, gcls, seg_stride);
             CKL("qscatter_kernel");
         }
         {

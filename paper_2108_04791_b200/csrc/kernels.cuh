@@ -30,6 +30,7 @@ constexpr int CLS_THREADS = 256;
 constexpr int CLS_PAIRS = 4;                          // 2 elements per pair -> 8 per thread
 constexpr int CLS_TILE = CLS_THREADS * 2 * CLS_PAIRS; // 2048 elements per tile
 constexpr int MR_THREADS = 256;
+constexpr int MAX_SEG = 4096;                         // classify blocks (queue segments) per launch
 
 // Device-resident plan and counters (one per device context).
 struct DevPlan {
@@ -50,6 +51,9 @@ struct DevPlan {
     unsigned int pback;                     // FP64-class entries of P64 (stored from the back)
     unsigned int cur1[3], cur2[3];          // dynamic work cursors of mr1 / mr2 (3 regions)
     unsigned long long work_f[2];           // FP64-class mulmods: mr1, mr2 (work counting)
+    // classify writes survivors into per-block segments (no block barrier):
+    // entries used by block b of the last classify launch
+    unsigned int seg32[MAX_SEG], seg64[MAX_SEG];
 };
 
 // Host -> plan kernel parameters (cost model in picoseconds on a full GPU).
@@ -534,8 +538,9 @@ sieve_kernel(const DevPlan* __restrict__ plan, uint32_t* __restrict__ bitmap,
 // warp-private shared-memory lists (ballot / shuffle scan, no block barrier)
 // and runs uniform loops over the dense lists.  A warp with no candidate (a
 // dense sieve window, config C4) stores its results straight from registers.
-// Survivors reserve queue space once per block tile: one __syncthreads_or,
-// then warp 0 scans the 8 warp counts and issues one atomicAdd per class.
+// Survivors go to a private segment of the queues per block (a shared-memory
+// cursor per class, no block barrier and no global atomic on the path); the
+// sort / compaction pass (qscatter_kernel) gathers the segments densely.
 struct ClsWarp {
     unsigned long long val[256];  // list32 from the front (low 32 bits used), list64 from the back
     uint8_t pos[256];             // element offset within the warp-tile
@@ -544,8 +549,7 @@ struct ClsWarp {
 };
 struct ClsSmem {
     ClsWarp w[CLS_THREADS / 32];
-    uint32_t cnt[CLS_THREADS / 32][2];
-    uint32_t base[CLS_THREADS / 32][2];
+    unsigned int cur[2];            // entries used in this block's Q32 / Q64 segment
     unsigned int h32[33], h64[65];  // bit-length histogram of this block's survivors (for the sort)
 };
 
@@ -553,8 +557,9 @@ template <int N32, int N64>
 __global__ void __launch_bounds__(CLS_THREADS)
 classify_kernel(const unsigned long long* __restrict__ N, uint8_t* __restrict__ out, uint32_t len,
                 DevPlan* __restrict__ plan, const uint32_t* __restrict__ bitmap, Queues q, TDParams td,
-                int vec_in, int vec_out) {
+                int vec_in, int vec_out, uint32_t seg_stride) {
     __shared__ ClsSmem sm;
+    const uint32_t segbase = blockIdx.x * seg_stride;
     const unsigned long long wlo = plan->wlo, whi = plan->whi;
     const unsigned long long span = whi - wlo;  // <= 2^32 (0: no window)
     // 32-bit form of the window test for values below 2^32: (lo - wlo) mod 2^32
@@ -565,6 +570,7 @@ classify_kernel(const unsigned long long* __restrict__ N, uint8_t* __restrict__ 
     ClsWarp& ws = sm.w[wid];
     const uint32_t ntiles = (len + CLS_TILE - 1) / CLS_TILE;
     for (int b = tid; b < 65; b += CLS_THREADS) { sm.h64[b] = 0; if (b < 33) sm.h32[b] = 0; }
+    if (tid < 2) sm.cur[tid] = 0;
     __syncthreads();
     for (uint32_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
         const uint32_t wbase = tile * CLS_TILE + 256u * wid;
@@ -729,57 +735,41 @@ classify_kernel(const unsigned long long* __restrict__ N, uint8_t* __restrict__ 
             }
         }
         }  // !fast
-        // ---- queue reservation: one barrier (two if this block tile has survivors)
-        if (lane == 0) { sm.cnt[wid][0] = s32; sm.cnt[wid][1] = s64; }
-        if (__syncthreads_or((int)(s32 | s64))) {
-            if (wid == 0) {
-                const uint32_t a32 = lane < CLS_THREADS / 32 ? sm.cnt[lane][0] : 0u;
-                const uint32_t a64 = lane < CLS_THREADS / 32 ? sm.cnt[lane][1] : 0u;
-                uint32_t i32 = a32, i64 = a64;
-#pragma unroll
-                for (int o = 1; o < CLS_THREADS / 32; o <<= 1) {
-                    const uint32_t y32 = __shfl_up_sync(0xffffffffu, i32, o);
-                    const uint32_t y64 = __shfl_up_sync(0xffffffffu, i64, o);
-                    if (lane >= o) { i32 += y32; i64 += y64; }
-                }
-                const uint32_t t32 = __shfl_sync(0xffffffffu, i32, CLS_THREADS / 32 - 1);
-                const uint32_t t64 = __shfl_sync(0xffffffffu, i64, CLS_THREADS / 32 - 1);
-                uint32_t g32 = 0, g64 = 0;
-                if (lane == 0) {
-                    g32 = t32 ? atomicAdd(&plan->counts[0], t32) : 0u;
-                    g64 = t64 ? atomicAdd(&plan->counts[1], t64) : 0u;
-                }
-                g32 = __shfl_sync(0xffffffffu, g32, 0);
-                g64 = __shfl_sync(0xffffffffu, g64, 0);
-                if (lane < CLS_THREADS / 32) { sm.base[lane][0] = g32 + i32 - a32; sm.base[lane][1] = g64 + i64 - a64; }
+        // ---- queue space from this block's private segment (no block barrier):
+        // block b owns entries [b * seg_stride, (b + 1) * seg_stride) of Q32 and
+        // Q64; seg_stride >= (tiles of the block) * CLS_TILE, so it never fills
+        if (s32 | s64) {  // warp-uniform
+            __syncwarp();    // ws.surv written by lane 0
+            uint32_t o32 = 0, o64 = 0;
+            if (lane == 0) {
+                o32 = s32 ? atomicAdd(&sm.cur[0], s32) : 0u;
+                o64 = s64 ? atomicAdd(&sm.cur[1], s64) : 0u;
             }
-            __syncthreads();
-            if (s32 | s64) {
-                uint32_t o32 = sm.base[wid][0], o64 = sm.base[wid][1];
-                for (uint32_t k0 = 0; k0 < n32; k0 += 32) {
-                    const uint32_t m = ws.surv[k0 >> 5];
-                    const uint32_t k = k0 + lane;
-                    if ((m >> lane) & 1u) {
-                        const uint32_t at = o32 + __popc(m & ((1u << lane) - 1u));
-                        const uint32_t v32 = (uint32_t)ws.val[k];
-                        q.q32_idx[at] = wbase + ws.pos[k];
-                        q.q32_val[at] = v32;
-                        atomicAdd(&sm.h32[32u - __clz(v32)], 1u);
-                    }
-                    o32 += __popc(m);
+            o32 = segbase + __shfl_sync(0xffffffffu, o32, 0);
+            o64 = segbase + __shfl_sync(0xffffffffu, o64, 0);
+            for (uint32_t k0 = 0; k0 < n32; k0 += 32) {
+                const uint32_t m = ws.surv[k0 >> 5];
+                const uint32_t k = k0 + lane;
+                if ((m >> lane) & 1u) {
+                    const uint32_t at = o32 + __popc(m & ((1u << lane) - 1u));
+                    const uint32_t v32 = (uint32_t)ws.val[k];
+                    q.q32_idx[at] = wbase + ws.pos[k];
+                    q.q32_val[at] = v32;
+                    atomicAdd(&sm.h32[32u - __clz(v32)], 1u);
                 }
-                for (uint32_t k0 = 0; k0 < n64; k0 += 32) {
-                    const uint32_t m = ws.surv[8 + (k0 >> 5)];
-                    const uint32_t k = k0 + lane;
-                    if ((m >> lane) & 1u) {
-                        const uint32_t at = o64 + __popc(m & ((1u << lane) - 1u));
-                        const unsigned long long v64 = ws.val[255u - k];
-                        q.q64_idx[at] = wbase + ws.pos[255u - k];
-                        q.q64_val[at] = v64;
-                        atomicAdd(&sm.h64[64u - __clzll((long long)v64)], 1u);
-                    }
-                    o64 += __popc(m);
+                o32 += __popc(m);
+            }
+            for (uint32_t k0 = 0; k0 < n64; k0 += 32) {
+                const uint32_t m = ws.surv[8 + (k0 >> 5)];
+                const uint32_t k = k0 + lane;
+                if ((m >> lane) & 1u) {
+                    const uint32_t at = o64 + __popc(m & ((1u << lane) - 1u));
+                    const unsigned long long v64 = ws.val[255u - k];
+                    q.q64_idx[at] = wbase + ws.pos[255u - k];
+                    q.q64_val[at] = v64;
+                    atomicAdd(&sm.h64[64u - __clzll((long long)v64)], 1u);
                 }
+                o64 += __popc(m);
             }
         }
         // ---- results of a warp that took the list path: shared tile -> out
@@ -791,12 +781,19 @@ classify_kernel(const unsigned long long* __restrict__ N, uint8_t* __restrict__ 
                 for (uint32_t k = lane; k < 256u; k += 32)
                     if (wbase + k < len) out[wbase + k] = ws.res[k];
             }
+            __syncwarp();  // the next warp-tile rewrites this warp's lists
         }
     }
     __syncthreads();
     for (int b = tid; b < 65; b += CLS_THREADS) {
         if (sm.h64[b]) atomicAdd(&plan->bins64[b], sm.h64[b]);
         if (b < 33 && sm.h32[b]) atomicAdd(&plan->bins32[b], sm.h32[b]);
+    }
+    if (tid == 0) {
+        plan->seg32[blockIdx.x] = sm.cur[0];
+        plan->seg64[blockIdx.x] = sm.cur[1];
+        if (sm.cur[0]) atomicAdd(&plan->counts[0], sm.cur[0]);
+        if (sm.cur[1]) atomicAdd(&plan->counts[1], sm.cur[1]);
     }
 }
 
@@ -805,69 +802,114 @@ classify_kernel(const unsigned long long* __restrict__ N, uint8_t* __restrict__ 
 // Q64).  A warp runs the exponent loop as long as its longest element, so on
 // mixed magnitudes (config C5: bit lengths 33..64 in every warp) unsorted
 // queues waste about a quarter of the multiply pipe; sorted, neighbouring
-// lanes carry equal-length exponents.  Skipped (flag stays 0, mr1 reads the
-// unsorted queue) when the expected gain is small (sort_pays).
+// lanes carry equal-length exponents.  When the expected gain is small
+// (sort_pays) the same pass only compacts classify's per-block segments.
 constexpr int SORT_THREADS = 256;
 constexpr int SORT_TILE = 2048;
 
 __device__ __forceinline__ unsigned int bitlen32(uint32_t v) { return 32u - __clz(v); }
 __device__ __forceinline__ unsigned int bitlen64u(unsigned long long v) { return 64u - __clzll((long long)v); }
 
+// Gather the per-block segments of one queue into a dense array: ordered by
+// bit length (counting sort, when `sort`) or in segment order (compaction).
+// Segment g holds segcnt[g] entries at src[g * stride ...].
 template <typename T, int NB>
-__device__ __forceinline__ void scatter_sorted(const unsigned int* __restrict__ gbins, unsigned int* gcur, unsigned int count,
-                                               const uint32_t* __restrict__ src_idx, const T* __restrict__ src_val,
-                                               uint32_t* __restrict__ dst_idx, T* __restrict__ dst_val,
-                                               unsigned int* spre, unsigned int* scnt, unsigned int* sbase) {
-    const int tid = threadIdx.x;
-    // exclusive prefix of the global bins (every block computes it)
-    if (tid == 0) {
-        unsigned int acc = 0;
-        for (int b = 0; b < NB; b++) { spre[b] = acc; acc += gbins[b]; }
+__device__ __forceinline__ void gather_segments(bool sort, const unsigned int* __restrict__ gbins, unsigned int* gcur,
+                                                const unsigned int* __restrict__ segcnt, int nseg, uint32_t stride,
+                                                const uint32_t* __restrict__ src_idx, const T* __restrict__ src_val,
+                                                uint32_t* __restrict__ dst_idx, T* __restrict__ dst_val,
+                                                unsigned int* spre, unsigned int* scnt, unsigned int* sbase,
+                                                unsigned int* spfx, unsigned int* swarp) {
+    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+    if (sort) {
+        // exclusive prefix of the global bins (every block computes it)
+        if (tid == 0) {
+            unsigned int acc = 0;
+            for (int b = 0; b < NB; b++) { spre[b] = acc; acc += gbins[b]; }
+        }
+        for (int b = tid; b < NB; b += SORT_THREADS) scnt[b] = 0;
+    } else {
+        // exclusive prefix of the segment counts: the dense start of each segment
+        constexpr int PERT = MAX_SEG / SORT_THREADS;
+        unsigned int loc[PERT], sum = 0;
+#pragma unroll
+        for (int j = 0; j < PERT; j++) {
+            const int g = tid * PERT + j;
+            loc[j] = g < nseg ? segcnt[g] : 0u;
+            sum += loc[j];
+        }
+        unsigned int incl = sum;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const unsigned int y = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= o) incl += y;
+        }
+        if (lane == 31) swarp[wid] = incl;
+        __syncthreads();
+        unsigned int wofs = 0;
+        for (int w = 0; w < wid; w++) wofs += swarp[w];
+        unsigned int acc = wofs + incl - sum;
+#pragma unroll
+        for (int j = 0; j < PERT; j++) {
+            spfx[tid * PERT + j] = acc;
+            acc += loc[j];
+        }
     }
-    for (int b = tid; b < NB; b += SORT_THREADS) scnt[b] = 0;
     __syncthreads();
     constexpr int PER = SORT_TILE / SORT_THREADS;
-    for (unsigned int t0 = blockIdx.x * SORT_TILE; t0 < count; t0 += gridDim.x * SORT_TILE) {
-        uint32_t idx[PER];
-        T val[PER];
-        unsigned int bin[PER], rank[PER];
+    for (int g = blockIdx.x; g < nseg; g += gridDim.x) {
+        const unsigned int count = segcnt[g];
+        const size_t sb = (size_t)g * stride;
+        for (unsigned int t0 = 0; t0 < count; t0 += SORT_TILE) {
+            uint32_t idx[PER];
+            T val[PER];
 #pragma unroll
-        for (int k = 0; k < PER; k++) {  // all loads in flight before any use
-            const unsigned int i = t0 + tid + k * SORT_THREADS;
-            idx[k] = i < count ? src_idx[i] : 0u;
-            val[k] = i < count ? src_val[i] : (T)0;
-        }
-#pragma unroll
-        for (int k = 0; k < PER; k++) {
-            const unsigned int i = t0 + tid + k * SORT_THREADS;
-            bin[k] = i < count ? ((sizeof(T) == 8) ? bitlen64u((unsigned long long)val[k]) : bitlen32((uint32_t)val[k]))
-                               : (unsigned int)NB;  // sentinel: no element
-        }
-#pragma unroll
-        for (int k = 0; k < PER; k++) {
-            const unsigned int peers = __match_any_sync(0xffffffffu, bin[k]);
-            const int leader = __ffs(peers) - 1;
-            const int lane = tid & 31;
-            unsigned int base = 0;
-            if (lane == leader && bin[k] < NB) base = atomicAdd(&scnt[bin[k]], (unsigned int)__popc(peers));
-            base = __shfl_sync(0xffffffffu, base, leader);
-            rank[k] = base + __popc(peers & ((1u << lane) - 1u));
-        }
-        __syncthreads();
-        for (int b = tid; b < NB; b += SORT_THREADS)
-            if (scnt[b]) sbase[b] = spre[b] + atomicAdd(&gcur[b], scnt[b]);
-        __syncthreads();
-#pragma unroll
-        for (int k = 0; k < PER; k++) {
-            if (bin[k] < NB) {
-                const unsigned int pos = sbase[bin[k]] + rank[k];
-                dst_idx[pos] = idx[k];
-                dst_val[pos] = val[k];
+            for (int k = 0; k < PER; k++) {  // all loads in flight before any use
+                const unsigned int i = t0 + tid + k * SORT_THREADS;
+                idx[k] = i < count ? src_idx[sb + i] : 0u;
+                val[k] = i < count ? src_val[sb + i] : (T)0;
             }
+            if (!sort) {
+                const unsigned int d0 = spfx[g];
+#pragma unroll
+                for (int k = 0; k < PER; k++) {
+                    const unsigned int i = t0 + tid + k * SORT_THREADS;
+                    if (i < count) { dst_idx[d0 + i] = idx[k]; dst_val[d0 + i] = val[k]; }
+                }
+                continue;
+            }
+            unsigned int bin[PER], rank[PER];
+#pragma unroll
+            for (int k = 0; k < PER; k++) {
+                const unsigned int i = t0 + tid + k * SORT_THREADS;
+                bin[k] = i < count ? ((sizeof(T) == 8) ? bitlen64u((unsigned long long)val[k]) : bitlen32((uint32_t)val[k]))
+                                   : (unsigned int)NB;  // sentinel: no element
+            }
+#pragma unroll
+            for (int k = 0; k < PER; k++) {
+                const unsigned int peers = __match_any_sync(0xffffffffu, bin[k]);
+                const int leader = __ffs(peers) - 1;
+                unsigned int base = 0;
+                if (lane == leader && bin[k] < NB) base = atomicAdd(&scnt[bin[k]], (unsigned int)__popc(peers));
+                base = __shfl_sync(0xffffffffu, base, leader);
+                rank[k] = base + __popc(peers & ((1u << lane) - 1u));
+            }
+            __syncthreads();
+            for (int b = tid; b < NB; b += SORT_THREADS)
+                if (scnt[b]) sbase[b] = spre[b] + atomicAdd(&gcur[b], scnt[b]);
+            __syncthreads();
+#pragma unroll
+            for (int k = 0; k < PER; k++) {
+                if (bin[k] < NB) {
+                    const unsigned int pos = sbase[bin[k]] + rank[k];
+                    dst_idx[pos] = idx[k];
+                    dst_val[pos] = val[k];
+                }
+            }
+            __syncthreads();
+            for (int b = tid; b < NB; b += SORT_THREADS) scnt[b] = 0;
+            __syncthreads();
         }
-        __syncthreads();
-        for (int b = tid; b < NB; b += SORT_THREADS) scnt[b] = 0;
-        __syncthreads();
     }
 }
 
@@ -899,22 +941,27 @@ __device__ __forceinline__ bool sort_pays(const unsigned int* bins, int nb) {
     return false;
 }
 
-__global__ void __launch_bounds__(SORT_THREADS) qscatter_kernel(DevPlan* __restrict__ plan, Queues q) {
-    __shared__ unsigned int spre[65], scnt[65], sbase[65];
+__global__ void __launch_bounds__(SORT_THREADS) qscatter_kernel(DevPlan* __restrict__ plan, Queues q, int nseg,
+                                                                uint32_t seg_stride) {
+    __shared__ unsigned int spre[65], scnt[65], sbase[65], swarp[SORT_THREADS / 32];
+    __shared__ unsigned int spfx[MAX_SEG];
     __shared__ unsigned int do32, do64;
+    const unsigned int c32 = plan->counts[0], c64 = plan->counts[1];
+    if (c32 == 0 && c64 == 0) return;  // nothing queued (a dense sieve window)
     if (threadIdx.x == 0) {
         do32 = sort_pays(plan->bins32, 33);
         do64 = sort_pays(plan->bins64, 65);
         if (blockIdx.x == 0) { plan->sorted32 = do32; plan->sorted64 = do64; }
     }
     __syncthreads();
-    if (do32)
-        scatter_sorted<uint32_t, 33>(plan->bins32, plan->cur32, plan->counts[0], q.q32_idx, q.q32_val,
-                                     q.s32_idx, q.s32_val, spre, scnt, sbase);
+    if (c32)
+        gather_segments<uint32_t, 33>(do32, plan->bins32, plan->cur32, plan->seg32, nseg, seg_stride, q.q32_idx,
+                                      q.q32_val, q.s32_idx, q.s32_val, spre, scnt, sbase, spfx, swarp);
     __syncthreads();
-    if (do64)
-        scatter_sorted<unsigned long long, 65>(plan->bins64, plan->cur64, plan->counts[1], q.q64_idx, q.q64_val,
-                                               q.s64_idx, q.s64_val, spre, scnt, sbase);
+    if (c64)
+        gather_segments<unsigned long long, 65>(do64, plan->bins64, plan->cur64, plan->seg64, nseg, seg_stride,
+                                                q.q64_idx, q.q64_val, q.s64_idx, q.s64_val, spre, scnt, sbase, spfx,
+                                                swarp);
 }
 
 // ------------------------------------------------------------- A3: MR phase 1
@@ -1037,10 +1084,11 @@ mr1_kernel(DevPlan* __restrict__ plan, Queues q, int count_work) {
     if (threadIdx.x == 0) s_nf = fp_class_count(plan);
     __syncthreads();
     const unsigned int c32 = plan->counts[0], c64 = plan->counts[1], nf = s_nf;
-    const uint32_t* q32i = plan->sorted32 ? q.s32_idx : q.q32_idx;
-    const uint32_t* q32v = plan->sorted32 ? q.s32_val : q.q32_val;
-    const uint32_t* q64i = plan->sorted64 ? q.s64_idx : q.q64_idx;
-    const unsigned long long* q64v = plan->sorted64 ? q.s64_val : q.q64_val;
+    // dense copies written by qscatter_kernel (ordered by bit length when sorted*)
+    const uint32_t* q32i = q.s32_idx;
+    const uint32_t* q32v = q.s32_val;
+    const uint32_t* q64i = q.s64_idx;
+    const unsigned long long* q64v = q.s64_val;
     // regions: 0 = Q32, 1 = FP64 class = sorted Q64 [0, nf), 2 = the rest of Q64
     const unsigned int size[3] = {c32, nf, c64 - nf};
     unsigned long long w32 = 0, w64 = 0, wf = 0;
