@@ -503,20 +503,21 @@ sieve_kernel(const DevPlan* __restrict__ plan, uint32_t* __restrict__ bitmap,
             }
         }
         __syncthreads();
-        // pack: word w of the segment = bytes [32w, 32w+32); 32 words per warp pass
+        // pack: word w of the segment = bytes [32w, 32w+32), one word per thread.
+        // Bytes are 0 / 1, so four of them gather into a nibble with one multiply:
+        // (b0 + b1 2^8 + b2 2^16 + b3 2^24) * (1 + 2^7 + 2^14 + 2^21) has b_k at
+        // bit 21 + k and no carry into bits 21..24.
         {
             const uint32_t nwords = seg_len >> 5;  // seg_len is a multiple of 32
             uint32_t* dstw = bitmap + ((sgi * SEG_ODD) >> 5);
-            for (uint32_t w0 = (uint32_t)wid * 32u; w0 < nwords; w0 += NWARPS * 32u) {
-                uint32_t mine = 0;
-#pragma unroll 8
-                for (int j = 0; j < 32; j++) {
-                    const uint32_t w = w0 + j;
-                    const uint8_t b = (w < nwords) ? seg[w * 32u + lane] : 0;
-                    const uint32_t word = __ballot_sync(0xffffffffu, b != 0);
-                    if (lane == j) mine = word;
-                }
-                if (w0 + lane < nwords) dstw[w0 + lane] = mine;
+            for (uint32_t w = tid; w < nwords; w += SIEVE_THREADS) {
+                const uint4* src = reinterpret_cast<const uint4*>(seg + 32u * w);
+                const uint4 a = src[0], b = src[1];
+                const uint32_t q[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
+                uint32_t word = 0;
+#pragma unroll
+                for (int k = 0; k < 8; k++) word |= (((q[k] * 0x204081u) >> 21) & 0xFu) << (4 * k);
+                dstw[w] = word;
             }
         }
         __syncthreads();
