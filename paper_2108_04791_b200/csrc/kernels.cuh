@@ -1150,6 +1150,10 @@ mr1_kernel(DevPlan* __restrict__ plan, Queues q, int count_work) {
 template <int WIN, bool FULL32, int G64>
 __global__ void __launch_bounds__(MR_THREADS)
 mr2_kernel(DevPlan* __restrict__ plan, Queues q, uint8_t* __restrict__ out, int count_work) {
+    // window tables of the lockstep bases in shared memory (transposed per thread)
+    constexpr bool SM = G64 * (1 << WIN) <= 12;
+    __shared__ unsigned long long s_tab[SM ? G64 * (1 << WIN) * MR_THREADS : 1];
+    unsigned long long* st = s_tab + threadIdx.x;
     // regions: 0 = P32, 1 = FP64 class (back of P64), 2 = Montgomery class (front of P64)
     const unsigned int size[3] = {plan->counts[2], plan->pback, plan->counts[3]};
     unsigned long long w32 = 0, w64 = 0, wf = 0;
@@ -1174,7 +1178,8 @@ mr2_kernel(DevPlan* __restrict__ plan, Queues q, uint8_t* __restrict__ out, int 
                 const unsigned int k = r == 1 ? q.cap - 1 - i : i;
                 const unsigned long long n = q.p64_val[k];
                 const bool fp = n < FP_LIMIT;
-                const bool prime = fp ? sprp_multi_f64<6, G64, WIN>(n, c_bases64) : sprp_multi64<6, G64, WIN>(n, c_bases64);
+                const bool prime = fp ? sprp_multi_f64<6, G64, WIN, SM, MR_THREADS>(n, c_bases64, reinterpret_cast<double*>(st))
+                                      : sprp_multi64<6, G64, WIN, SM, MR_THREADS>(n, c_bases64, st);
                 if (prime) out[q.p64_idx[k]] = 1;
                 if (count_work) {
                     const unsigned long long d = odd_part(n);

@@ -422,9 +422,8 @@ __device__ __forceinline__ double fmul_lazy(double a, double b, const ModF& M) {
 
 // x^2 * 2^b for the base-2 ladder (ModMultiply case 3 folded in as an exact
 // power-of-two scaling of one factor).  |x| < n, b in {0, 1}.
-__device__ __forceinline__ double fsqr_dbl_lazy(double x, uint32_t b, const ModF& M) {
-    const double f = __hiloint2double(0x3FF00000 + (int)(b << 20), 0);  // 1.0 or 2.0
-    return fmul_lazy(x * f, x, M);
+__device__ __forceinline__ double fsqr_dbl_lazy(double x, bool b, const ModF& M) {
+    return fmul_lazy(x * (b ? 2.0 : 1.0), x, M);
 }
 
 // Signed representative -> congruence tests (|x| < n).

@@ -144,9 +144,13 @@ __device__ __forceinline__ uint64_t sel_table(const uint64_t (&tab)[T], uint32_t
 // Phase 2: NB bases in lockstep with a fixed WIN-bit window, for a modulus
 // whose Montgomery context (M, R2, d, s) is already set up.  Returns true iff
 // n passes every base.  Bases are reduced mod n.
-template <int NB, int WIN>
+// SM: the window table lives in shared memory, transposed so that lane t's
+// entry (base i, digit k) is st[(i (T + 1) + k) * TS] with st = table + t:
+// one LDS per base and window (conflict-free across the warp) replaces the
+// 2T selects of sel_table.  TS = threads per block.
+template <int NB, int WIN, bool SM = false, int TS = 256>
 __device__ __forceinline__ bool sprp_lockstep64(const Mont64& M, uint64_t R2, uint64_t d, int s,
-                                                const unsigned long long* bases) {
+                                                const unsigned long long* bases, unsigned long long* st = nullptr) {
     constexpr int T = (1 << WIN) - 1;
     const uint64_t n = M.n;
     const int nbits = 64 - __clzll((long long)d);
@@ -161,21 +165,29 @@ __device__ __forceinline__ bool sprp_lockstep64(const Mont64& M, uint64_t R2, ui
         tab[i][0] = mmul64(a, R2, M);
 #pragma unroll
         for (int k = 1; k < T; k++) tab[i][k] = mmul64(tab[i][k - 1], tab[i][0], M);
+        if (SM) {
+            st[(i * (T + 1)) * TS] = M.one;
+#pragma unroll
+            for (int k = 0; k < T; k++) st[(i * (T + 1) + k + 1) * TS] = tab[i][k];
+        }
     }
     {
         const uint32_t lead = (uint32_t)(d >> (WIN * (nw - 1)));  // nonzero
 #pragma unroll
-        for (int i = 0; i < NB; i++) x[i] = sel_table<T>(tab[i], lead, M.one);
+        for (int i = 0; i < NB; i++) x[i] = SM ? st[(i * (T + 1) + lead) * TS] : sel_table<T>(tab[i], lead, M.one);
     }
     for (int w = nw - 2; w >= 0; w--) {
         const uint32_t digit = (uint32_t)(d >> (WIN * w)) & (uint32_t)T;
+        uint64_t mt[NB];
+#pragma unroll
+        for (int i = 0; i < NB; i++) mt[i] = SM ? st[(i * (T + 1) + digit) * TS] : sel_table<T>(tab[i], digit, M.one);
 #pragma unroll
         for (int j = 0; j < WIN; j++) {
 #pragma unroll
             for (int i = 0; i < NB; i++) x[i] = msqr64_ptx(x[i], n, M.ninv);
         }
 #pragma unroll
-        for (int i = 0; i < NB; i++) x[i] = mmul64_ptx(x[i], sel_table<T>(tab[i], digit, M.one), n, M.ninv);
+        for (int i = 0; i < NB; i++) x[i] = mmul64_ptx(x[i], mt[i], n, M.ninv);
     }
 #pragma unroll
     for (int i = 0; i < NB; i++) {
@@ -202,8 +214,9 @@ __device__ __forceinline__ bool sprp_lockstep64(const Mont64& M, uint64_t R2, ui
 
 // All NB bases of `bases`, G at a time in lockstep (G | NB), stopping at the
 // first group with a witness.  One Montgomery setup per n.
-template <int NB, int G, int WIN>
-__device__ __forceinline__ bool sprp_multi64(uint64_t n, const unsigned long long* bases) {
+template <int NB, int G, int WIN, bool SM = false, int TS = 256>
+__device__ __forceinline__ bool sprp_multi64(uint64_t n, const unsigned long long* bases,
+                                             unsigned long long* st = nullptr) {
     const Mont64 M = mont64_setup(n);
     const uint64_t R2 = mont64_r2(M);
     uint64_t d = n - 1;
@@ -211,7 +224,7 @@ __device__ __forceinline__ bool sprp_multi64(uint64_t n, const unsigned long lon
     d >>= s;
 #pragma unroll 1
     for (int g = 0; g < NB; g += G)
-        if (!sprp_lockstep64<G, WIN>(M, R2, d, s, bases + g)) return false;
+        if (!sprp_lockstep64<G, WIN, SM, TS>(M, R2, d, s, bases + g, st)) return false;
     return true;
 }
 
@@ -231,7 +244,7 @@ __device__ __forceinline__ bool sprp2_f64(unsigned long long n) {
         unsigned long long dd = d << (64 - top);  // remaining bits, MSB first
 #pragma unroll 2
         for (int k = 0; k < top; k++) {
-            x = fsqr_dbl_lazy(x, (uint32_t)(dd >> 63), M);
+            x = fsqr_dbl_lazy(x, (long long)dd < 0, M);
             dd += dd;
         }
     }
@@ -252,9 +265,9 @@ __device__ __forceinline__ double sel_table_f(const double (&tab)[T], uint32_t d
     return m;
 }
 
-template <int NB, int WIN>
+template <int NB, int WIN, bool SM = false, int TS = 256>
 __device__ __forceinline__ bool sprp_lockstep_f64(const ModF& M, unsigned long long n, unsigned long long d, int s,
-                                                  const unsigned long long* bases) {
+                                                  const unsigned long long* bases, double* st = nullptr) {
     constexpr int T = (1 << WIN) - 1;
     const int nbits = 64 - __clzll((long long)d);
     const int nw = (nbits + WIN - 1) / WIN;
@@ -268,21 +281,29 @@ __device__ __forceinline__ bool sprp_lockstep_f64(const ModF& M, unsigned long l
         tab[i][0] = (double)a;
 #pragma unroll
         for (int k = 1; k < T; k++) tab[i][k] = fmul_lazy(tab[i][k - 1], tab[i][0], M);
+        if (SM) {
+            st[(i * (T + 1)) * TS] = 1.0;
+#pragma unroll
+            for (int k = 0; k < T; k++) st[(i * (T + 1) + k + 1) * TS] = tab[i][k];
+        }
     }
     {
         const uint32_t lead = (uint32_t)(d >> (WIN * (nw - 1)));
 #pragma unroll
-        for (int i = 0; i < NB; i++) x[i] = sel_table_f<T>(tab[i], lead);
+        for (int i = 0; i < NB; i++) x[i] = SM ? st[(i * (T + 1) + lead) * TS] : sel_table_f<T>(tab[i], lead);
     }
     for (int w = nw - 2; w >= 0; w--) {
         const uint32_t digit = (uint32_t)(d >> (WIN * w)) & (uint32_t)T;
+        double mt[NB];
+#pragma unroll
+        for (int i = 0; i < NB; i++) mt[i] = SM ? st[(i * (T + 1) + digit) * TS] : sel_table_f<T>(tab[i], digit);
 #pragma unroll
         for (int j = 0; j < WIN; j++) {
 #pragma unroll
             for (int i = 0; i < NB; i++) x[i] = fmul_lazy(x[i], x[i], M);
         }
 #pragma unroll
-        for (int i = 0; i < NB; i++) x[i] = fmul_lazy(x[i], sel_table_f<T>(tab[i], digit), M);
+        for (int i = 0; i < NB; i++) x[i] = fmul_lazy(x[i], mt[i], M);
     }
 #pragma unroll
     for (int i = 0; i < NB; i++) {
@@ -307,15 +328,16 @@ __device__ __forceinline__ bool sprp_lockstep_f64(const ModF& M, unsigned long l
     return ok;
 }
 
-template <int NB, int G, int WIN>
-__device__ __forceinline__ bool sprp_multi_f64(unsigned long long n, const unsigned long long* bases) {
+template <int NB, int G, int WIN, bool SM = false, int TS = 256>
+__device__ __forceinline__ bool sprp_multi_f64(unsigned long long n, const unsigned long long* bases,
+                                               double* st = nullptr) {
     const ModF M = modf_setup(n);
     unsigned long long d = n - 1;
     const int s = __ffsll((long long)d) - 1;
     d >>= s;
 #pragma unroll 1
     for (int g = 0; g < NB; g += G)
-        if (!sprp_lockstep_f64<G, WIN>(M, n, d, s, bases + g)) return false;
+        if (!sprp_lockstep_f64<G, WIN, SM, TS>(M, n, d, s, bases + g, st)) return false;
     return true;
 }
 
