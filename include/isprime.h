@@ -86,7 +86,8 @@ void isprime_shutdown(void);
  *                    below 2^32 before Miller-Rabin (0..ISP_MAX_TD)
  * "td_primes64"      same for values >= 2^32
  * "chunk_log2"       device chunk size (elements) = 2^value, 16..31
- * "win64"            exponent window width for the 64-bit multi-base phase (1..3)
+ * "win64"            exponent window width for the 64-bit multi-base phase (1..3,
+ *                    default 3; the window tables live in shared memory)
  * "sieve_cache"      0 (default): every call sieves its own window; 1: a call may
  *                    reuse the bitmap an earlier call on this device produced
  * "mr2_group"        3 or 6: 64-bit phase-2 bases run in lockstep groups of this size

@@ -28,7 +28,7 @@ struct Options {
     int td32 = 16;           // odd primes 3..59 (profiles: C2 best at 16)
     int td64 = 32;
     int chunk_log2 = 28;
-    int win64 = 2;
+    int win64 = 3;           // phase-2 window bits (tables in shared memory; 3 measured best)
     int warp_p = 2048;
     long long sieve_fs_per_int = 700;     // femtoseconds per integer of window (measured: C4 0.68 ps)
     long long sieve_fixed_ns = 8000;

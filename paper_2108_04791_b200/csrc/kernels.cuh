@@ -1151,7 +1151,7 @@ template <int WIN, bool FULL32, int G64>
 __global__ void __launch_bounds__(MR_THREADS)
 mr2_kernel(DevPlan* __restrict__ plan, Queues q, uint8_t* __restrict__ out, int count_work) {
     // window tables of the lockstep bases in shared memory (transposed per thread)
-    constexpr bool SM = G64 * (1 << WIN) <= 12;
+    constexpr bool SM = G64 * (1 << WIN) <= 24;  // <= 48 KB of static shared memory
     __shared__ unsigned long long s_tab[SM ? G64 * (1 << WIN) * MR_THREADS : 1];
     unsigned long long* st = s_tab + threadIdx.x;
     // regions: 0 = P32, 1 = FP64 class (back of P64), 2 = Montgomery class (front of P64)
