@@ -91,6 +91,10 @@ void isprime_shutdown(void);
  * "sieve_cache"      0 (default): every call sieves its own window; 1: a call may
  *                    reuse the bitmap an earlier call on this device produced
  * "mr2_group"        3 or 6: 64-bit phase-2 bases run in lockstep groups of this size
+ * "small_max"        arrays with n <= small_max (default 131072) and force_path 0
+ *                    take one fused launch (trial division + Miller-Rabin per
+ *                    element) instead of the plan / sieve / queue pipeline;
+ *                    0 disables it.  Never changes a bit of out.
  * "kernel_timing"    1: bracket every launch with CUDA events on its stream and
  *                    accumulate per-kernel device time (isprime_get_kernel_times)
  * Returns ISP_OK or ISP_EINVAL. */

@@ -36,7 +36,8 @@ struct Options {
     unsigned long long sieve_max = 1ull << 32;
     int kernel_timing = 0;
     int sieve_cache = 0;
-    int mr2_group = 3;       // 64-bit phase-2 bases run G at a time in lockstep (3 or 6)     // 1: a call may reuse the bitmap sieved by an earlier call
+    int mr2_group = 3;       // 64-bit phase-2 bases run G at a time in lockstep (3 or 6)
+    long long small_max = 1 << 17;  // n <= small_max (and force_path auto): one fused launch     // 1: a call may reuse the bitmap sieved by an earlier call
 };
 
 Options g_opt;
@@ -75,8 +76,8 @@ struct Ctx {
 std::vector<Ctx*> g_ctx;
 
 // ---- optional per-kernel timing (events on the launching stream)
-enum { K_PLAN, K_SIEVE, K_CLASSIFY, K_SORT, K_MR1, K_MR2, K_POPCOUNT, K_NUM };
-const char* const k_names[K_NUM] = {"plan", "sieve", "classify", "sort", "mr1", "mr2", "popcount"};
+enum { K_PLAN, K_SIEVE, K_CLASSIFY, K_SORT, K_MR1, K_MR2, K_POPCOUNT, K_SMALL, K_NUM };
+const char* const k_names[K_NUM] = {"plan", "sieve", "classify", "sort", "mr1", "mr2", "popcount", "small"};
 struct KTPending { cudaEvent_t a, b; int kid; };
 std::vector<KTPending> g_kt_pending;
 std::vector<cudaEvent_t> g_ev_pool;
@@ -349,6 +350,20 @@ int device_impl(Ctx* c, const unsigned long long* dN, uint8_t* dout, size_t n, c
         const unsigned long long sq = pn * pn;
         td.sq32 = sq > 0xFFFFFFFFull ? 0xFFFFFFFFu : (uint32_t)sq;
     }
+    if ((long long)n <= g_opt.small_max && g_opt.force_path == 0) {
+        // short array: one fused launch (small_kernel), latency instead of pipeline stages
+        const uint32_t len = (uint32_t)n;
+        {
+            KScope ks(K_SMALL, s);
+            if (g_opt.bases32 == 7) small_kernel<true><<<(len + 255) / 256, 256, 0, s>>>(dN, dout, len, td);
+            else small_kernel<false><<<(len + 255) / 256, 256, 0, s>>>(dN, dout, len, td);
+            CKL("small_kernel");
+        }
+        CK(cudaEventRecord(c->last_done, s));
+        c->has_last = true;
+        c->last_stream = (void*)s;
+        return ISP_OK;
+    }
     for (size_t base = 0; base < n; base += chunk) {
         const uint32_t len = (uint32_t)((n - base) < chunk ? (n - base) : chunk);
         const unsigned long long* N = dN + base;
@@ -578,6 +593,7 @@ int isprime_set_option(const char* key, long long v) {
     else if (!strcmp(key, "kernel_timing")) { if (v < 0 || v > 1) return ISP_EINVAL; g_opt.kernel_timing = (int)v; }
     else if (!strcmp(key, "mr2_group")) { if (v != 3 && v != 6) return ISP_EINVAL; g_opt.mr2_group = (int)v; }
     else if (!strcmp(key, "sieve_cache")) { if (v < 0 || v > 1) return ISP_EINVAL; g_opt.sieve_cache = (int)v; }
+    else if (!strcmp(key, "small_max")) { if (v < 0) return ISP_EINVAL; g_opt.small_max = v; }
     else return ISP_EINVAL;
     return ISP_OK;
 }
@@ -599,6 +615,7 @@ long long isprime_get_option(const char* key) {
     if (!strcmp(key, "kernel_timing")) return g_opt.kernel_timing;
     if (!strcmp(key, "sieve_cache")) return g_opt.sieve_cache;
     if (!strcmp(key, "mr2_group")) return g_opt.mr2_group;
+    if (!strcmp(key, "small_max")) return g_opt.small_max;
     return -1;
 }
 

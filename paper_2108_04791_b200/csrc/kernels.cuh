@@ -1201,6 +1201,40 @@ mr2_kernel(DevPlan* __restrict__ plan, Queues q, uint8_t* __restrict__ out, int 
     }
 }
 
+// ------------------------------------------------------------- short arrays
+// Scalars and short arrays (the paper's per-call latency regime, PAPER.md:349-372
+// and Tables 4/6/7): one fused launch, one element per thread, no plan, sieve
+// or queues.  Per element the same exact steps as the pipeline -- trivial
+// cases, trial division by the first N32 odd primes (< 2^32), then the strong
+// tests of Eq 4 ({2, 7, 61} below 2^32 unless FULL32) in the
+// magnitude class's arithmetic -- so the result is the same bit for bit; lanes
+// diverge, which only matters when n is large (the host sends those down the
+// pipeline).
+template <bool FULL32>
+__global__ void __launch_bounds__(256) small_kernel(const unsigned long long* __restrict__ N, uint8_t* __restrict__ out,
+                                                    uint32_t len, TDParams td) {
+    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= len) return;
+    const unsigned long long v = N[i];
+    uint8_t r;
+    if (v < 2ull) r = 0;
+    else if (!(v & 1ull)) r = (v == 2ull);
+    else if (v < (1ull << 32)) {
+        const uint32_t x = (uint32_t)v;
+        bool comp = false;
+        for (int t = 0; t < td.n32; t++) comp |= (x * c_td_inv32[t] <= c_td_lim32[t]) && (x != c_td_p[t]);
+        if (comp) r = 0;
+        else if (x < td.sq32) r = 1;
+        else if (!sprp2_32(x)) r = 0;
+        else r = FULL32 ? sprp_multi32<6>(x, c_bases32_full) : sprp_multi32<2>(x, c_bases32_red);
+    } else if (v < FP_LIMIT) {
+        r = sprp2_f64(v) && sprp_multi_f64<6, 3, 2>(v, c_bases64);
+    } else {
+        r = sprp2_64(v) && sprp_multi64<6, 3, 2>(v, c_bases64);
+    }
+    out[i] = r;
+}
+
 // ------------------------------------------------------------- harness
 __global__ void popcount_kernel(const uint8_t* __restrict__ out, unsigned long long n,
                                 unsigned long long* __restrict__ count) {

@@ -51,7 +51,7 @@ def assert_same(got, exp, N=None):
 @pytest.fixture(autouse=True)
 def _default_options():
     saved = {k: isp.get_option(k) for k in ("force_path", "bases32", "td_primes32", "td_primes64",
-                                             "chunk_log2", "win64", "warp_p")}
+                                             "chunk_log2", "win64", "warp_p", "small_max")}
     yield
     for k, v in saved.items():
         isp.set_option(k, v)
@@ -81,9 +81,11 @@ def test_chernick_and_pseudoprimes():
                     80581, 85489, 88357, 90751, 3215031751, 2152302898747, 3474749660383,
                     341550071728321, 3825123056546413051], dtype=np.uint64)
     N = np.concatenate([cs, sp2])
-    got = gpu(N)
-    assert got.sum() == 0
-    assert_same(got, oracle.isprime(N), N)
+    for small_max in (0, 1 << 17):  # pipeline and short-array path
+        isp.set_option("small_max", small_max)
+        got = gpu(N)
+        assert got.sum() == 0
+        assert_same(got, oracle.isprime(N), N)
 
 
 def test_boundary_primes_and_neighbours():
@@ -94,7 +96,10 @@ def test_boundary_primes_and_neighbours():
         hi = min(2**64, c + 3000)
         vals.extend(range(lo, hi))
     N = np.array(vals, dtype=np.uint64)
-    assert_same(gpu(N), oracle.isprime(N), N)
+    exp = oracle.isprime(N)
+    for small_max in (0, 1 << 17):  # pipeline and short-array path
+        isp.set_option("small_max", small_max)
+        assert_same(gpu(N), exp, N)
 
 
 def test_all_below_2_20_every_path():
@@ -104,6 +109,25 @@ def test_all_below_2_20_every_path():
         isp.set_option("force_path", fp)
         assert_same(gpu(N), exp, N)
     assert exp.sum() == 82025
+
+
+@pytest.mark.parametrize("small_max", [0, 1 << 17])
+def test_short_array_path_vs_pipeline(small_max):
+    """Short arrays (n <= small_max) take one fused launch (small_kernel);
+    longer ones the plan / sieve / classify / Miller-Rabin pipeline.  The pin
+    lists and seeded prefixes of every magnitude class through both must equal
+    the oracle."""
+    isp.set_option("small_max", small_max)
+    vals = np.array([int(r[0]) for r in _rows("special_values.txt")], dtype=np.uint64)
+    cs = np.array(workloads.chernick_numbers(), dtype=np.uint64)
+    near = np.concatenate([np.arange(max(0, c - 500), c + 500, dtype=np.uint64)
+                           for c in (2**32, 2**49, 2**63)] + [np.arange(2**64 - 1000, 2**64 - 1, dtype=np.uint64)])
+    for N in (vals, cs, near, workloads.generate("C1", count=100_000), workloads.generate("C5", count=100_000),
+              workloads.generate("C3", count=30_000), workloads.generate("C2", count=50_000)):
+        exp = oracle.isprime(N)
+        assert_same(gpu(N), exp, N)
+        for n in (1, 31, 257):
+            assert_same(gpu(N[:n]), exp[:n], N[:n])
 
 
 @pytest.mark.parametrize("count", [3000, 300_000])
@@ -125,6 +149,7 @@ def test_base2_ladder_around_2_63(count):
                         dtype=np.uint64)
         near.append(cand[oracle.isprime(cand) == 1])
     N = np.concatenate([lo, hi, mixed] + near)
+    isp.set_option("small_max", 0)  # through the pipeline's witness kernels
     assert_same(gpu(N), oracle.isprime(N), N)
 
 
@@ -233,7 +258,9 @@ def test_options_do_not_change_results():
 
 
 # ------------------------------------------------------------------ boundary edge cases
-def test_edge_sizes_and_alignment():
+@pytest.mark.parametrize("small_max", [0, 1 << 17])
+def test_edge_sizes_and_alignment(small_max):
+    isp.set_option("small_max", small_max)
     N = workloads.generate("C5", count=70_001)
     exp = oracle.isprime(N)
     for n in (0, 1, 2, 3, 7, 8, 31, 2047, 2048, 2049, 4097, 70_001):
