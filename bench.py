@@ -293,6 +293,35 @@ def run_reference(args, rank, world):
     print(json.dumps(line), flush=True)
 
 
+def scalar_latency(isp, torch, dev, stream):
+    """Per-call latency for one scalar (the paper's Tables 4, 6 and 7 time a
+    single 64-bit prime): the device call on a
+    resident value (CUDA events) and the host C-ABI isprime() call on a
+    one-element host array (wall clock, H2D + D2H included).  Median of 200."""
+    vals = {"2^64-59 (prime)": (1 << 64) - 59, "2^52-47 (prime)": (1 << 52) - 47, "2^31-1 (prime)": (1 << 31) - 1}
+    res = {}
+    for name, v in vals.items():
+        host = np.array([v], dtype=np.uint64)
+        dN = torch.from_numpy(host.view(np.int64)).to(dev)
+        dout = torch.empty(1, dtype=torch.uint8, device=dev)
+        ts, tw = [], []
+        for k in range(220):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            isp.isprime_device(dN, dout, 1, stream)
+            e1.record(stream)
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            out = isp.isprime(host)
+            t1 = time.perf_counter()
+            if k >= 20:
+                ts.append(e0.elapsed_time(e1) * 1e3)
+                tw.append((t1 - t0) * 1e6)
+        assert int(out[0]) == 1 and int(dout.item()) == 1
+        res[name] = {"device_us": round(float(np.median(ts)), 2), "host_api_us": round(float(np.median(tw)), 2)}
+    return res
+
+
 def config_block(cfg, world):
     n = workloads.CONFIGS[cfg][1]
     return {"workload": f"{cfg}: {workloads.CONFIGS[cfg][2]} (BASELINE.json configs[{int(cfg[1]) - 1}])",
@@ -431,6 +460,7 @@ def main():
                 del cN, cout
                 torch.cuda.empty_cache()
             line["per_config"] = per
+        line["scalar_latency"] = scalar_latency(isp, torch, dev, stream)
     if rank == 0:
         print(json.dumps(line), flush=True)
     if dist:
