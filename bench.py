@@ -293,6 +293,31 @@ def run_reference(args, rank, world):
     print(json.dumps(line), flush=True)
 
 
+def witness_bpsw(isp, torch, dev, stream, args, counts):
+    """Option witness = 1 (Baillie-PSW: a strong Lucas test replaces the six
+    remaining Eq 4 bases for n >= 2^49 -- the paper's proposed next step,
+    PAPER.md:425-426).  Same workloads, same timing; the headline above is the
+    paper's Eq 4 method."""
+    res = {}
+    isp.set_option("witness", 1)
+    try:
+        for c in ("C5", "C3"):
+            cn = workloads.CONFIGS[c][1]
+            cN, _ = make_input(c, 0, torch, dev)
+            cout = torch.empty(cn, dtype=torch.uint8, device=dev)
+            cms, _ = time_steps(isp, torch, cN, cout, cn, args.steps, args.warmup, stream, None)
+            dcount = torch.zeros(1, dtype=torch.int64, device=dev)
+            isp.isprime_popcount_device(cout, dcount, cn, stream)
+            torch.cuda.synchronize()
+            res[c] = {"value": round(cn / (cms * 1e-3) / 1e9, 4), "unit": UNIT, "ms_per_step": round(cms, 4),
+                      "correct": int(dcount.item()) == counts[c]}
+            del cN, cout
+            torch.cuda.empty_cache()
+    finally:
+        isp.set_option("witness", 0)
+    return res
+
+
 def scalar_latency(isp, torch, dev, stream):
     """Per-call latency for one scalar (the paper's Tables 4, 6 and 7 time a
     single 64-bit prime): the device call on a
@@ -461,6 +486,7 @@ def main():
                 torch.cuda.empty_cache()
             line["per_config"] = per
         line["scalar_latency"] = scalar_latency(isp, torch, dev, stream)
+        line["witness_bpsw"] = witness_bpsw(isp, torch, dev, stream, args, counts)
     if rank == 0:
         print(json.dumps(line), flush=True)
     if dist:

@@ -91,6 +91,11 @@ void isprime_shutdown(void);
  * "sieve_cache"      0 (default): every call sieves its own window; 1: a call may
  *                    reuse the bitmap an earlier call on this device produced
  * "mr2_group"        3 or 6: 64-bit phase-2 bases run in lockstep groups of this size
+ * "witness"          0 (default): the Eq 4 bases after base 2 for every
+ *                    class; 1: Baillie-PSW for n >= 2^49 -- a strong Lucas test
+ *                    (Selfridge parameters) after the base-2 strong test, the
+ *                    paper's proposed next step; exact below
+ *                    2^64 like Eq 4, so it never changes a bit of out
  * "small_max"        arrays with n <= small_max (default 131072) and force_path 0
  *                    take one fused launch (trial division + Miller-Rabin per
  *                    element) instead of the plan / sieve / queue pipeline;

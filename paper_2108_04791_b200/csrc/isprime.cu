@@ -37,7 +37,8 @@ struct Options {
     int kernel_timing = 0;
     int sieve_cache = 0;
     int mr2_group = 3;       // 64-bit phase-2 bases run G at a time in lockstep (3 or 6)
-    long long small_max = 1 << 17;  // n <= small_max (and force_path auto): one fused launch     // 1: a call may reuse the bitmap sieved by an earlier call
+    long long small_max = 1 << 17;  // n <= small_max (and force_path auto): one fused launch
+    int witness = 0;         // 0: Eq 4 bases; 1: Baillie-PSW for n >= 2^49     // 1: a call may reuse the bitmap sieved by an earlier call
 };
 
 Options g_opt;
@@ -317,6 +318,12 @@ int launch_mr2(Ctx* c, cudaStream_t s, uint8_t* out, int grid) {
     const bool full = g_opt.bases32 == 7;
     const int cw = g_opt.kernel_timing;
     const int g = g_opt.mr2_group == 6 ? 6 : 3;
+    if (g_opt.witness == 1) {  // Baillie-PSW for the 64-bit Montgomery class
+        if (full) mr2_kernel<3, true, 3, true><<<grid, MR_THREADS, 0, s>>>(c->plan, c->q, out, cw);
+        else mr2_kernel<3, false, 3, true><<<grid, MR_THREADS, 0, s>>>(c->plan, c->q, out, cw);
+        CKL("mr2_kernel");
+        return ISP_OK;
+    }
     switch (g_opt.win64 * 10 + g) {
         case 13: launch_mr2_w<1, 3>(c, s, out, grid, full, cw); break;
         case 16: launch_mr2_w<1, 6>(c, s, out, grid, full, cw); break;
@@ -594,6 +601,7 @@ int isprime_set_option(const char* key, long long v) {
     else if (!strcmp(key, "mr2_group")) { if (v != 3 && v != 6) return ISP_EINVAL; g_opt.mr2_group = (int)v; }
     else if (!strcmp(key, "sieve_cache")) { if (v < 0 || v > 1) return ISP_EINVAL; g_opt.sieve_cache = (int)v; }
     else if (!strcmp(key, "small_max")) { if (v < 0) return ISP_EINVAL; g_opt.small_max = v; }
+    else if (!strcmp(key, "witness")) { if (v < 0 || v > 1) return ISP_EINVAL; g_opt.witness = (int)v; }
     else return ISP_EINVAL;
     return ISP_OK;
 }
@@ -616,6 +624,7 @@ long long isprime_get_option(const char* key) {
     if (!strcmp(key, "sieve_cache")) return g_opt.sieve_cache;
     if (!strcmp(key, "mr2_group")) return g_opt.mr2_group;
     if (!strcmp(key, "small_max")) return g_opt.small_max;
+    if (!strcmp(key, "witness")) return g_opt.witness;
     return -1;
 }
 

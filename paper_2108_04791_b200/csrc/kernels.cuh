@@ -1147,7 +1147,7 @@ mr1_kernel(DevPlan* __restrict__ plan, Queues q, int count_work) {
 }
 
 // ------------------------------------------------------------- A4: MR phase 2
-template <int WIN, bool FULL32, int G64>
+template <int WIN, bool FULL32, int G64, bool LUCAS = false>
 __global__ void __launch_bounds__(MR_THREADS)
 mr2_kernel(DevPlan* __restrict__ plan, Queues q, uint8_t* __restrict__ out, int count_work) {
     // window tables of the lockstep bases in shared memory (transposed per thread)
@@ -1178,8 +1178,9 @@ mr2_kernel(DevPlan* __restrict__ plan, Queues q, uint8_t* __restrict__ out, int 
                 const unsigned int k = r == 1 ? q.cap - 1 - i : i;
                 const unsigned long long n = q.p64_val[k];
                 const bool fp = n < FP_LIMIT;
+                // LUCAS: Baillie-PSW for the Montgomery class (strong Lucas after the base-2 phase)
                 const bool prime = fp ? sprp_multi_f64<6, G64, WIN, SM, MR_THREADS>(n, c_bases64, reinterpret_cast<double*>(st))
-                                      : sprp_multi64<6, G64, WIN, SM, MR_THREADS>(n, c_bases64, st);
+                                      : (LUCAS ? slprp64(n) : sprp_multi64<6, G64, WIN, SM, MR_THREADS>(n, c_bases64, st));
                 if (prime) out[q.p64_idx[k]] = 1;
                 if (count_work) {
                     const unsigned long long d = odd_part(n);

@@ -335,6 +335,11 @@ __device__ __forceinline__ uint64_t madd64(uint64_t a, uint64_t b, uint64_t n) {
     return a >= nb ? a - nb : a + b;
 }
 
+// a - b mod n for a, b < n.
+__device__ __forceinline__ uint64_t msub64(uint64_t a, uint64_t b, uint64_t n) {
+    return a >= b ? a - b : a + (n - b);
+}
+
 // ModMultiply case 3: 2b mod n = b - (n - b).
 __device__ __forceinline__ uint64_t mdbl64(uint64_t b, uint64_t n) { return madd64(b, b, n); }
 

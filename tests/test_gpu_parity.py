@@ -130,6 +130,36 @@ def test_short_array_path_vs_pipeline(small_max):
             assert_same(gpu(N[:n]), exp[:n], N[:n])
 
 
+def test_bpsw_witness_option():
+    """Option witness = 1 replaces the six remaining Eq 4 bases of the 64-bit
+    Montgomery class by a strong Lucas test (Baillie-PSW, the paper's proposed
+    next step).  The Chernick numbers include 251 strong
+    base-2 pseudoprimes, which only the Lucas part can
+    reject; with them the pins, boundary neighbours and seeded 64-bit data must
+    equal the oracle, and the full C3 count must hold."""
+    saved = isp.get_option("witness")
+    try:
+        isp.set_option("witness", 1)
+        isp.set_option("small_max", 0)
+        cs = np.array(workloads.chernick_numbers(), dtype=np.uint64)
+        vals = np.array([int(r[0]) for r in _rows("special_values.txt")], dtype=np.uint64)
+        near = np.concatenate([np.arange(c - 3000, c + 3000, dtype=np.uint64) for c in (2**49, 2**56, 2**63)]
+                              + [np.arange(2**64 - 6000, 2**64 - 1, dtype=np.uint64)])
+        sq = np.array([p * p for p in (4294967291, 4294967279, 65521 * 65519, 2147483647)], dtype=np.uint64)
+        for N in (cs, np.tile(vals, 64), near, sq, workloads.generate("C3", count=(1 << 18) + 3),
+                  workloads.generate("C5", count=(1 << 20) + 4097)):
+            assert_same(gpu(N), oracle.isprime(N), N)
+        N = workloads.generate("C3")
+        dN = torch.from_numpy(N.view(np.int64)).to(DEV)
+        dout = torch.empty(N.shape[0], dtype=torch.uint8, device=DEV)
+        dcount = torch.zeros(1, dtype=torch.int64, device=DEV)
+        isp.isprime_count_device(dN, dout, dcount)
+        torch.cuda.synchronize()
+        assert int(dcount.item()) == _counts()["C3"]
+    finally:
+        isp.set_option("witness", saved)
+
+
 @pytest.mark.parametrize("count", [3000, 300_000])
 def test_base2_ladder_around_2_63(count):
     """The base-2 ladder fuses its doubling into the reduction below 2^63 and
@@ -249,7 +279,8 @@ def test_options_do_not_change_results():
                         workloads.generate("C1", count=50_000)])
     exp = oracle.isprime(N)
     for key, vals in (("td_primes32", (0, 1, 5, 128)), ("td_primes64", (0, 3, 128)), ("win64", (1, 2, 3)),
-                      ("force_path", (0, 1, 2)), ("chunk_log2", (16, 17, 28)), ("warp_p", (17, 600, 65536))):
+                      ("force_path", (0, 1, 2)), ("chunk_log2", (16, 17, 28)), ("warp_p", (17, 600, 65536)),
+                      ("witness", (1, 0))):
         saved = isp.get_option(key)
         for v in vals:
             isp.set_option(key, v)
