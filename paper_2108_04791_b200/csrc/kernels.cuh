@@ -153,19 +153,41 @@ __device__ __forceinline__ bool td_primes(uint32_t r) {
     }
 }
 
+// Per-group doubles that are not short immediates (1/M and M + 2^52) live in
+// the constant bank, so the DFMA / DADD take them as operands instead of two
+// register moves each per candidate.
+constexpr int kMaxGroups = 12;
+struct TDGroupConst {
+    double inv[4][kMaxGroups];  // [NP / 8 - 1][g]: fl(1 / M)
+    double mb[4][kMaxGroups];   // M + 2^52
+};
+__host__ __device__ constexpr TDGroupConst make_td_group_const() {
+    TDGroupConst t{};
+    for (int k = 0; k < 4; k++) {
+        const int np = 8 * (k + 1);
+        for (int g = 0; g < kMaxGroups; g++) {
+            const bool used = g < group_count(np);
+            t.inv[k][g] = used ? 1.0 / (double)group_modulus(np, g) : 0.0;
+            t.mb[k][g] = used ? (double)group_modulus(np, g) + 4503599627370496.0 : 0.0;
+        }
+    }
+    return t;
+}
+__constant__ TDGroupConst c_tdg = make_td_group_const();
+
 template <int NP, int G>
 __device__ __forceinline__ bool td_groups(double xh, double xl) {
     if constexpr (G >= group_count(NP)) {
         return false;
     } else {
+        static_assert(NP % 8 == 0 && NP <= 32 && group_count(NP) <= kMaxGroups, "trial-division group table");
         constexpr uint32_t M = group_modulus(NP, G);
         constexpr double Md = (double)M;
         constexpr double c = (double)(uint32_t)((1ull << 32) % M);
-        constexpr double inv = 1.0 / (double)M;
-        const double y = fma(xh, c, xl);                                        // == x (mod M), < 2^53
-        const double q = fma(y, inv, 6755399441055744.0) - 6755399441055744.0;  // round(y / M)
-        const double r = fma(-q, Md, y) + Md;                                   // in (0, 2M)
-        const uint32_t ri = (uint32_t)__double2loint(r + 4503599627370496.0);
+        const double y = fma(xh, c, xl);                                                  // == x (mod M), < 2^53
+        const double q = fma(y, c_tdg.inv[NP / 8 - 1][G], 6755399441055744.0) - 6755399441055744.0;  // round(y / M)
+        // r = y - q M + M in (0, 2M); adding 2^52 in the same DADD leaves r in the low word
+        const uint32_t ri = (uint32_t)__double2loint(fma(-q, Md, y) + c_tdg.mb[NP / 8 - 1][G]);
         return td_primes<group_start(NP, G), group_start(NP, G + 1)>(ri) | td_groups<NP, G + 1>(xh, xl);
     }
 }
@@ -644,24 +666,26 @@ classify_kernel(const unsigned long long* __restrict__ N, uint8_t* __restrict__ 
         uint8_t r[8];
         uint32_t word[8], dd[8];
         uint32_t inmask = 0;
+        // flags as 0/1 integers combined with bitwise operators: no short-circuit
+        // branches and few live predicates
 #pragma unroll
         for (int e = 0; e < 8; e++) {  // all eight bitmap reads in flight together
             const uint32_t xlo = (uint32_t)v[e], xhi = (uint32_t)(v[e] >> 32);
             dd[e] = xlo - wlo32;
-            const bool inwin = (xhi == 0u) & (xlo & 1u) & (dd[e] <= spanm1w);
-            inmask |= (uint32_t)inwin << e;
-            word[e] = inwin ? __ldg(bitmap + (dd[e] >> 6)) : 0u;
+            const uint32_t in = (uint32_t)(xhi == 0u) & xlo & (uint32_t)(dd[e] <= spanm1w) & 1u;
+            inmask |= in << e;
+            word[e] = in ? __ldg(bitmap + (dd[e] >> 6)) : 0u;
         }
 #pragma unroll
         for (int e = 0; e < 8; e++) {
             const uint32_t xlo = (uint32_t)v[e], xhi = (uint32_t)(v[e] >> 32);
-            const bool small = xhi == 0u;
-            const bool inwin = (inmask >> e) & 1u;
+            const uint32_t big = (uint32_t)(xhi != 0u);
             const uint32_t bit = __funnelshift_r(word[e], word[e], dd[e] >> 1) & 1u;  // 0 outside the window
-            r[e] = (uint8_t)((small && xlo == 2u) ? 1u : bit);
-            const bool cand = (xlo & 1u) && !inwin && (!small || xlo > 1u);
-            m32 |= (uint32_t)(cand && small) << e;
-            m64 |= (uint32_t)(cand && !small) << e;
+            r[e] = (uint8_t)(bit | ((uint32_t)(xlo == 2u) & (big ^ 1u)));
+            // candidate: odd, outside the window, not 1
+            const uint32_t cand = xlo & ~(inmask >> e) & (big | (uint32_t)(xlo != 1u)) & 1u;
+            m64 |= (cand & big) << e;
+            m32 |= (cand & (big ^ 1u)) << e;
         }
         const uint32_t c32 = __popc(m32), c64 = __popc(m64);
         // warp scan of the packed (c32, c64) counts
