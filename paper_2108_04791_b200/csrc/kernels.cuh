@@ -135,6 +135,23 @@ __host__ __device__ constexpr uint32_t inv32_c(uint32_t p) {
     return x;
 }
 
+// bit (x >> 1) & 31 of word x >> 6: odd x < 256 is prime
+__host__ __device__ constexpr bool small_odd_prime_c(uint32_t x) {
+    if (x < 3) return false;
+    for (uint32_t d = 3; d * d <= x; d += 2) if (x % d == 0) return false;
+    return true;
+}
+struct SmallPrimeMask { uint32_t w[4]; };
+__host__ __device__ constexpr SmallPrimeMask make_small_prime_mask() {
+    SmallPrimeMask m{};
+    for (uint32_t x = 3; x < 256; x += 2) if (small_odd_prime_c(x)) m.w[x >> 6] |= 1u << ((x >> 1) & 31u);
+    return m;
+}
+constexpr SmallPrimeMask kSmallPrimeMaskStruct = make_small_prime_mask();
+__device__ __constant__ uint32_t kSmallOddPrimeMask[4] = {kSmallPrimeMaskStruct.w[0], kSmallPrimeMaskStruct.w[1],
+                                                           kSmallPrimeMaskStruct.w[2], kSmallPrimeMaskStruct.w[3]};
+static_assert(kOddPrimes[31] < 256, "small prime mask covers the trial-division primes");
+
 __device__ __forceinline__ double u32_to_f64(uint32_t v) {
     return __hiloint2double(0x43300000, (int)v) - 4503599627370496.0;  // exact: (2^52 + v) - 2^52
 }
@@ -732,9 +749,13 @@ classify_kernel(const unsigned long long* __restrict__ N, uint8_t* __restrict__ 
                 bool surv = false;
                 if (k < n32) {
                     const uint32_t x = (uint32_t)ws.val[k];
-                    bool comp = false;
-#pragma unroll
-                    for (int t = 0; t < N32; t++) comp |= (x * c_td_inv32[t] <= c_td_lim32[t]) && (x != c_td_p[t]);
+                    // compile-time primes (immediate operands, 2 instructions each);
+                    // x itself among them is prime, read from a bit mask instead
+                    bool comp = td_primes<0, N32>(x);
+                    if constexpr (N32 > 0) {
+                        constexpr uint32_t kLast = kOddPrimes[N32 - 1];
+                        if (x <= kLast) comp = !((kSmallOddPrimeMask[x >> 6] >> ((x >> 1) & 31u)) & 1u);
+                    }
                     if (!comp) {
                         if (x < td.sq32) ws.res[ws.pos[k]] = 1;
                         else surv = true;
