@@ -383,8 +383,11 @@ int device_impl(Ctx* c, const unsigned long long* dN, uint8_t* dout, size_t n, c
         }
         {
             KScope ks(K_SIEVE, s);
+            // first base prime >= warp_p (the warp-cooperative / per-thread split)
+            int first_large = FIRST_CROSS_PRIME_IDX;
+            while (first_large < c->nbp && c->hbp[first_large].x < (uint32_t)g_opt.warp_p) first_large++;
             sieve_kernel<<<c->grid_sieve, SIEVE_THREADS, SEG_ODD, s>>>(c->plan, c->bitmap, c->bp, c->nbp, c->patt,
-                                                                         (uint32_t)g_opt.warp_p);
+                                                                         first_large);
             CKL("sieve_kernel");
         }
         const uint32_t ntiles = (len + CLS_TILE - 1) / CLS_TILE;

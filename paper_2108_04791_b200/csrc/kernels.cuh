@@ -463,13 +463,13 @@ __global__ void __launch_bounds__(PLAN_THREADS) plan_kernel(const unsigned long 
 // whi <= 2^32).  Byte k of a segment stands for v = seg_lo + 2k + 1.  Bytes are
 // initialised from the {3,5,7,11,13} pre-sieve pattern, primes 17 <= p with
 // p^2 < seg_hi cross off their odd multiples from max(p^2, first in segment):
-// warp-cooperatively (lane l takes every 32nd multiple) for p < warp_p, one
-// prime per thread above.  Byte stores of 0 need no atomics.  The segment is
-// packed to bits with warp ballots and stored coalesced.
+// warp-cooperatively (lane l takes every 32nd multiple) for p < warp_p (index
+// < first_large, found by the host), one prime per thread above.  Byte stores
+// of 0 need no atomics.  The segment is packed to bitmap words per thread.
 __global__ void __launch_bounds__(SIEVE_THREADS, 2)
 sieve_kernel(const DevPlan* __restrict__ plan, uint32_t* __restrict__ bitmap,
              const uint2* __restrict__ bp, int nbp, const uint8_t* __restrict__ patt,
-             uint32_t warp_p) {
+             int first_large) {
     extern __shared__ __align__(16) uint8_t seg[];
     if (!plan->sieve_needed) return;
     const unsigned long long wlo = plan->wlo, whi = plan->whi;
@@ -495,12 +495,10 @@ sieve_kernel(const DevPlan* __restrict__ plan, uint32_t* __restrict__ bitmap,
             seg[0] = 0; seg[1] = 1; seg[2] = 1; seg[3] = 1; seg[5] = 1; seg[6] = 1;
         }
         const uint32_t x = (uint32_t)(seg_lo + 1);  // first odd value, < 2^32
-        // warp-cooperative crossing, small primes
-        int i = FIRST_CROSS_PRIME_IDX + wid;
-        for (; i < nbp; i += NWARPS) {
-            const uint2 pc = bp[i];
+        // first index of a multiple of p in the segment (its odd multiple >= max(p^2, x)),
+        // or 0xFFFFFFFF when there is none
+        auto first_k = [&](uint2 pc) -> uint32_t {
             const uint32_t p = pc.x;
-            if (p >= warp_p || (unsigned long long)p * p >= seg_hi) break;
             uint32_t q = __umulhi(x, pc.y);
             int32_t rr = (int32_t)(x - q * p);
             if (rr < 0) rr += (int32_t)p;
@@ -509,36 +507,40 @@ sieve_kernel(const DevPlan* __restrict__ plan, uint32_t* __restrict__ bitmap,
             const unsigned long long pp = (unsigned long long)p * p;
             if (m < pp) m = pp;
             const unsigned long long k0 = (m - x) >> 1;  // < p + p^2 / 2: may exceed the segment
-            if (k0 < seg_len) {
-                const uint32_t stride = 32u * p;
-#pragma unroll 4
-                for (uint32_t k = (uint32_t)k0 + lane * p; k < seg_len; k += stride) seg[k] = 0;
+            return k0 < seg_len ? (uint32_t)k0 : 0xFFFFFFFFu;
+        };
+        // small primes (p < warp_p): the lanes of a warp set up 32 primes at
+        // once (warp w takes primes w, w + 16, w + 32, ...), then cross each of
+        // them off warp-cooperatively (lane l takes every 32nd multiple)
+        for (int i0 = FIRST_CROSS_PRIME_IDX + wid; i0 < first_large; i0 += 32 * NWARPS) {
+            const int i = i0 + NWARPS * lane;
+            uint32_t p = 0, k0 = 0xFFFFFFFFu;
+            if (i < first_large) {
+                const uint2 pc = bp[i];
+                if ((unsigned long long)pc.x * pc.x < seg_hi) { p = pc.x; k0 = first_k(pc); }
             }
+            uint32_t work = __ballot_sync(0xffffffffu, k0 != 0xFFFFFFFFu);
+            const bool more = __any_sync(0xffffffffu, p != 0);
+            while (work) {
+                const int j = __ffs(work) - 1;
+                work &= work - 1;
+                const uint32_t pj = __shfl_sync(0xffffffffu, p, j);
+                const uint32_t kj = __shfl_sync(0xffffffffu, k0, j);
+                const uint32_t stride = 32u * pj;
+#pragma unroll 4
+                for (uint32_t k = kj + lane * pj; k < seg_len; k += stride) seg[k] = 0;
+            }
+            if (!more) break;  // p^2 >= seg_hi from here on
         }
-        // one prime per thread, larger primes: first index with p >= warp_p
-        {
-            // binary search for the first prime >= warp_p (uniform)
-            int lo = FIRST_CROSS_PRIME_IDX, hi = nbp;
-            while (lo < hi) {
-                const int mid = (lo + hi) >> 1;
-                if (bp[mid].x < warp_p) lo = mid + 1; else hi = mid;
-            }
-            for (int j = lo + tid; j < nbp; j += SIEVE_THREADS) {
-                const uint2 pc = bp[j];
-                const uint32_t p = pc.x;
-                if ((unsigned long long)p * p >= seg_hi) break;
-                uint32_t q = __umulhi(x, pc.y);
-                int32_t rr = (int32_t)(x - q * p);
-                if (rr < 0) rr += (int32_t)p;
-                unsigned long long m = (unsigned long long)x + (rr ? (p - (uint32_t)rr) : 0u);
-                if (!(m & 1ull)) m += p;
-                const unsigned long long pp = (unsigned long long)p * p;
-                if (m < pp) m = pp;
-                const unsigned long long k0 = (m - x) >> 1;
-                if (k0 < seg_len) {
+        // larger primes: one per thread
+        for (int j = first_large + tid; j < nbp; j += SIEVE_THREADS) {
+            const uint2 pc = bp[j];
+            const uint32_t p = pc.x;
+            if ((unsigned long long)p * p >= seg_hi) break;
+            const uint32_t k0 = first_k(pc);
+            if (k0 != 0xFFFFFFFFu) {
 #pragma unroll 4
-                    for (uint32_t k = (uint32_t)k0; k < seg_len; k += p) seg[k] = 0;
-                }
+                for (uint32_t k = k0; k < seg_len; k += p) seg[k] = 0;
             }
         }
         __syncthreads();
