@@ -100,6 +100,9 @@ void isprime_shutdown(void);
  *                    take one fused launch (trial division + Miller-Rabin per
  *                    element) instead of the plan / sieve / queue pipeline;
  *                    0 disables it.  Never changes a bit of out.
+ * "warp_max"         within the short-array path, n <= warp_max (default 4096)
+ *                    runs one warp per element with one Eq 4 base per lane
+ *                    (latency of one exponentiation instead of seven)
  * "kernel_timing"    1: bracket every launch with CUDA events on its stream and
  *                    accumulate per-kernel device time (isprime_get_kernel_times)
  * Returns ISP_OK or ISP_EINVAL. */

@@ -38,6 +38,7 @@ struct Options {
     int sieve_cache = 0;
     int mr2_group = 3;       // 64-bit phase-2 bases run G at a time in lockstep (3 or 6)
     long long small_max = 1 << 17;  // n <= small_max (and force_path auto): one fused launch
+    long long warp_max = 4096;      // n <= warp_max: one warp per element (one base per lane)
     int witness = 0;         // 0: Eq 4 bases; 1: Baillie-PSW for n >= 2^49     // 1: a call may reuse the bitmap sieved by an earlier call
 };
 
@@ -362,8 +363,15 @@ int device_impl(Ctx* c, const unsigned long long* dN, uint8_t* dout, size_t n, c
         const uint32_t len = (uint32_t)n;
         {
             KScope ks(K_SMALL, s);
-            if (g_opt.bases32 == 7) small_kernel<true><<<(len + 255) / 256, 256, 0, s>>>(dN, dout, len, td);
-            else small_kernel<false><<<(len + 255) / 256, 256, 0, s>>>(dN, dout, len, td);
+            if ((long long)len <= g_opt.warp_max) {  // one warp per element, one base per lane
+                const unsigned blocks = (unsigned)(((size_t)len * 32 + 255) / 256);
+                if (g_opt.bases32 == 7) small_warp_kernel<true><<<blocks, 256, 0, s>>>(dN, dout, len, td);
+                else small_warp_kernel<false><<<blocks, 256, 0, s>>>(dN, dout, len, td);
+            } else if (g_opt.bases32 == 7) {
+                small_kernel<true><<<(len + 255) / 256, 256, 0, s>>>(dN, dout, len, td);
+            } else {
+                small_kernel<false><<<(len + 255) / 256, 256, 0, s>>>(dN, dout, len, td);
+            }
             CKL("small_kernel");
         }
         CK(cudaEventRecord(c->last_done, s));
@@ -604,6 +612,7 @@ int isprime_set_option(const char* key, long long v) {
     else if (!strcmp(key, "mr2_group")) { if (v != 3 && v != 6) return ISP_EINVAL; g_opt.mr2_group = (int)v; }
     else if (!strcmp(key, "sieve_cache")) { if (v < 0 || v > 1) return ISP_EINVAL; g_opt.sieve_cache = (int)v; }
     else if (!strcmp(key, "small_max")) { if (v < 0) return ISP_EINVAL; g_opt.small_max = v; }
+    else if (!strcmp(key, "warp_max")) { if (v < 0 || v > (1 << 26)) return ISP_EINVAL; g_opt.warp_max = v; }
     else if (!strcmp(key, "witness")) { if (v < 0 || v > 1) return ISP_EINVAL; g_opt.witness = (int)v; }
     else return ISP_EINVAL;
     return ISP_OK;
@@ -627,6 +636,7 @@ long long isprime_get_option(const char* key) {
     if (!strcmp(key, "sieve_cache")) return g_opt.sieve_cache;
     if (!strcmp(key, "mr2_group")) return g_opt.mr2_group;
     if (!strcmp(key, "small_max")) return g_opt.small_max;
+    if (!strcmp(key, "warp_max")) return g_opt.warp_max;
     if (!strcmp(key, "witness")) return g_opt.witness;
     return -1;
 }

@@ -1283,6 +1283,47 @@ __global__ void __launch_bounds__(256) small_kernel(const unsigned long long* __
     out[i] = r;
 }
 
+// Scalars and very short arrays: one warp per element, one Eq 4 base per lane
+// (SURVEY.md 8(f) f3).  The strong tests of the bases are independent, so the
+// latency of an element is one modular exponentiation instead of seven in a
+// row; every lane runs the same generic test (base 2 included), so the warp
+// never splits.  Same trivial cases and trial division as small_kernel.
+__constant__ unsigned long long c_bases7[7] = {2ull, 325ull, 9375ull, 28178ull, 450775ull, 9780504ull, 1795265022ull};
+__constant__ uint32_t c_bases32_3[3] = {2u, 7u, 61u};
+
+template <bool FULL32>
+__global__ void __launch_bounds__(256) small_warp_kernel(const unsigned long long* __restrict__ N,
+                                                         uint8_t* __restrict__ out, uint32_t len, TDParams td) {
+    const uint32_t w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (w >= len) return;  // warp-uniform
+    const unsigned long long v = N[w];
+    int r = -1;            // -1: undecided
+    if (v < 2ull) r = 0;
+    else if (!(v & 1ull)) r = (v == 2ull);
+    else if (v < (1ull << 32)) {
+        const uint32_t x = (uint32_t)v;
+        bool comp = false;
+        for (int t = 0; t < td.n32; t++) comp |= (x * c_td_inv32[t] <= c_td_lim32[t]) && (x != c_td_p[t]);
+        if (comp) r = 0;
+        else if (x < td.sq32) r = 1;
+    }
+    if (r < 0) {
+        bool pass = true;
+        if (v < (1ull << 32)) {
+            const int nb = FULL32 ? 7 : 3;
+            if (lane < nb) {
+                const uint32_t b = FULL32 ? (uint32_t)c_bases7[lane] : c_bases32_3[lane];
+                pass = sprp_multi32<1>((uint32_t)v, &b);
+            }
+        } else if (lane < 7) {
+            pass = v < FP_LIMIT ? sprp_multi_f64<1, 1, 2>(v, c_bases7 + lane) : sprp_multi64<1, 1, 2>(v, c_bases7 + lane);
+        }
+        r = __all_sync(0xffffffffu, pass) ? 1 : 0;
+    }
+    if (lane == 0) out[w] = (uint8_t)r;
+}
+
 // ------------------------------------------------------------- harness
 __global__ void popcount_kernel(const uint8_t* __restrict__ out, unsigned long long n,
                                 unsigned long long* __restrict__ count) {

@@ -51,7 +51,7 @@ def assert_same(got, exp, N=None):
 @pytest.fixture(autouse=True)
 def _default_options():
     saved = {k: isp.get_option(k) for k in ("force_path", "bases32", "td_primes32", "td_primes64",
-                                             "chunk_log2", "win64", "warp_p", "small_max")}
+                                             "chunk_log2", "win64", "warp_p", "small_max", "warp_max")}
     yield
     for k, v in saved.items():
         isp.set_option(k, v)
@@ -111,13 +111,15 @@ def test_all_below_2_20_every_path():
     assert exp.sum() == 82025
 
 
-@pytest.mark.parametrize("small_max", [0, 1 << 17])
-def test_short_array_path_vs_pipeline(small_max):
-    """Short arrays (n <= small_max) take one fused launch (small_kernel);
-    longer ones the plan / sieve / classify / Miller-Rabin pipeline.  The pin
-    lists and seeded prefixes of every magnitude class through both must equal
-    the oracle."""
+@pytest.mark.parametrize("small_max,warp_max", [(0, 4096), (1 << 17, 0), (1 << 17, 4096), (1 << 17, 1 << 17)])
+def test_short_array_path_vs_pipeline(small_max, warp_max):
+    """Short arrays (n <= small_max) take one fused launch -- one warp per
+    element with one base per lane up to warp_max elements (small_warp_kernel),
+    one thread per element above (small_kernel); longer ones the plan / sieve /
+    classify / Miller-Rabin pipeline.  The pin lists and seeded prefixes of
+    every magnitude class through each must equal the oracle."""
     isp.set_option("small_max", small_max)
+    isp.set_option("warp_max", warp_max)
     vals = np.array([int(r[0]) for r in _rows("special_values.txt")], dtype=np.uint64)
     cs = np.array(workloads.chernick_numbers(), dtype=np.uint64)
     near = np.concatenate([np.arange(max(0, c - 500), c + 500, dtype=np.uint64)
