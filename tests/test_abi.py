@@ -71,6 +71,13 @@ def test_options_validate():
     isp.set_option("win64", 3)
     assert isp.get_option("win64") == 3
     isp.set_option("win64", old)
+    for key, bad, good in (("witness", 2, 1), ("small_max", -1, 0), ("warp_max", -1, 64)):
+        saved = isp.get_option(key)
+        with pytest.raises(isp.IsPrimeError):
+            isp.set_option(key, bad)
+        isp.set_option(key, good)
+        assert isp.get_option(key) == good
+        isp.set_option(key, saved)
 
 
 def test_no_cpu_fallback_without_device():
