@@ -1086,18 +1086,27 @@ __device__ __forceinline__ void stage_flush(WarpStage<T>& st, unsigned int& n, u
 // Montgomery classes).  Warps start on region (warp id mod 3) and move on when
 // it is drained, so at any moment an SM holds warps of every class: the
 // FP64 pipe and the FMA-heavy (IMAD) pipe work side by side instead of one
-// class after the other.  Chunks of MR_CHUNK entries per atomicAdd.
+// class after the other.  Chunks of MR_CHUNK entries per atomicAdd while
+// plenty of work remains, then single rounds of 32 (guided self-scheduling):
+// a warp that claims a 256-entry chunk near the end would otherwise run alone
+// for eight rounds while the rest of the GPU idles.
 constexpr unsigned int MR_CHUNK = 256;
+constexpr unsigned int MR_CHUNK_TAIL = 32;
 
 __device__ __forceinline__ bool next_chunk(const unsigned int (&size)[3], unsigned int* cur, int& r, int& tried,
-                                           unsigned int& start) {
+                                           unsigned int& start, unsigned int& end, unsigned int tail) {
     const int lane = threadIdx.x & 31;
     while (tried != 7) {
         if (!((tried >> r) & 1)) {
-            unsigned int s0 = 0xFFFFFFFFu;
-            if (size[r] && lane == 0) s0 = atomicAdd(&cur[r], MR_CHUNK);
+            unsigned int s0 = 0xFFFFFFFFu, ch = MR_CHUNK;
+            if (size[r] && lane == 0) {
+                const unsigned int seen = *reinterpret_cast<volatile unsigned int*>(&cur[r]);  // racy estimate
+                ch = seen + tail < size[r] ? MR_CHUNK : MR_CHUNK_TAIL;
+                s0 = atomicAdd(&cur[r], ch);
+            }
             s0 = __shfl_sync(0xffffffffu, s0, 0);
-            if (s0 < size[r]) { start = s0; return true; }
+            ch = __shfl_sync(0xffffffffu, ch, 0);
+            if (s0 < size[r]) { start = s0; end = min(s0 + ch, size[r]); return true; }
             tried |= 1 << r;
         }
         r = r == 2 ? 0 : r + 1;
@@ -1144,8 +1153,9 @@ mr1_kernel(DevPlan* __restrict__ plan, Queues q, int count_work) {
     const unsigned int gwarp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     int r = (int)(gwarp % 3u), tried = 0;
     unsigned int start = 0, n32s = 0, n64i = 0, n64f = 0;
-    while (next_chunk(size, plan->cur1, r, tried, start)) {
-        const unsigned int end = min(start + MR_CHUNK, size[r]);
+    // base-2 rounds are short: whole chunks to the end (tail 0)
+    unsigned int end = 0;
+    while (next_chunk(size, plan->cur1, r, tried, start, end, 0u)) {
         for (unsigned int b = start; b < end; b += 32) {
             const unsigned int i = b + lane;
             const bool act = i < end;
@@ -1208,8 +1218,10 @@ mr2_kernel(DevPlan* __restrict__ plan, Queues q, uint8_t* __restrict__ out, int 
     const unsigned int gwarp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     int r = (int)(gwarp % 3u), tried = 0;
     unsigned int start = 0;
-    while (next_chunk(size, plan->cur2, r, tried, start)) {
-        const unsigned int end = min(start + MR_CHUNK, size[r]);
+    // tail: about one 256-entry chunk per warp of the grid left
+    const unsigned int tail = gridDim.x * (MR_THREADS / 32) * MR_CHUNK;
+    unsigned int end = 0;
+    while (next_chunk(size, plan->cur2, r, tried, start, end, tail)) {
         for (unsigned int b = start; b < end; b += 32) {
             const unsigned int i = b + lane;
             if (i >= end) continue;
