@@ -205,6 +205,33 @@ def test_c4_shard_window_bit_exact():
     assert_same(gpu(N), oracle.dense_range(lo, N.shape[0]), N)
 
 
+@pytest.mark.parametrize("witness", [0, 1])
+def test_random_all_magnitudes_bit_exact(witness):
+    """2^22 values drawn three ways -- uniform over all of [0, 2^64), uniform
+    bit length 1..64, and odd values just above/below powers of two -- through
+    the full pipeline, every element compared with the oracle (beyond the
+    seeded BASELINE.json configurations)."""
+    isp.set_option("small_max", 0)
+    saved = isp.get_option("witness")
+    try:
+        isp.set_option("witness", witness)
+        rng = np.random.default_rng(2108 + witness)
+        n = 1 << 20
+        uni = rng.integers(0, 2**64 - 1, size=n, dtype=np.uint64, endpoint=True)
+        bl = rng.integers(1, 65, size=n)
+        lo = rng.integers(0, 2**63, size=n, dtype=np.uint64)
+        logu = np.array([(1 << (b - 1)) | (int(x) & ((1 << (b - 1)) - 1)) for b, x in zip(bl.tolist(), lo.tolist())],
+                        dtype=np.uint64)
+        k = rng.integers(1, 64, size=n)
+        off = rng.integers(0, 1 << 12, size=n)
+        edge = np.array([((1 << int(a)) + int(o)) | 1 if (i & 1) else max(3, ((1 << int(a)) - int(o)) | 1)
+                         for i, (a, o) in enumerate(zip(k.tolist(), off.tolist()))], dtype=np.uint64)
+        N = np.concatenate([uni, logu, edge, rng.permutation(np.concatenate([uni[: n // 2], logu[: n // 2]]))])
+        assert_same(gpu(N), oracle.isprime(N), N)
+    finally:
+        isp.set_option("witness", saved)
+
+
 # ------------------------------------------------------------------ full sizes (count + sampled elements)
 def _counts():
     return {r[0]: int(r[2]) for r in _rows("config_counts.txt")}
