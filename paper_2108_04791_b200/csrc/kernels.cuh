@@ -95,6 +95,12 @@ __constant__ unsigned long long c_td_lim64[MAX_TD];
 __constant__ unsigned long long c_bases64[6] = {325ull, 9375ull, 28178ull, 450775ull, 9780504ull, 1795265022ull};
 __constant__ uint32_t c_bases32_full[6] = {325u, 9375u, 28178u, 450775u, 9780504u, 1795265022u};
 __constant__ uint32_t c_bases32_red[2] = {7u, 61u};
+__constant__ unsigned long long c_bases32_red64[2] = {7ull, 61ull};
+// 32-bit class of the witness kernels on the FP64 pipe (lazy signed residues,
+// modmath.cuh fmul_lazy) instead of 32-bit Montgomery on the IMAD / ALU pipes
+#ifndef CLS32_FP64
+#define CLS32_FP64 1
+#endif
 
 // ---- trial division of 64-bit values on the FP64 pipe --------------------
 // The IMAD-based test (v * p^-1 mod 2^64 <= lim) costs one IMAD.WIDE and two
@@ -1165,7 +1171,7 @@ mr1_kernel(DevPlan* __restrict__ plan, Queues q, int count_work) {
                 if (act) {
                     n = q32v[i];
                     idx = q32i[i];
-                    pass = sprp2_32(n);
+                    pass = CLS32_FP64 ? sprp2_f64(n) : sprp2_32(n);
                     if (count_work) w32 += modexp_squarings(odd_part(n));
                 }
                 stage_append<uint32_t>(pass, idx, n, st32[wib], n32s, &plan->counts[2], q.p32_idx, q.p32_val);
@@ -1227,7 +1233,12 @@ mr2_kernel(DevPlan* __restrict__ plan, Queues q, uint8_t* __restrict__ out, int 
             if (i >= end) continue;
             if (r == 0) {
                 const uint32_t n = q.p32_val[i];
-                const bool prime = FULL32 ? sprp_multi32<6>(n, c_bases32_full) : sprp_multi32<2>(n, c_bases32_red);
+                bool prime;
+                if (CLS32_FP64)  // the 32-bit class on the FP64 pipe (exact below 2^49)
+                    prime = FULL32 ? sprp_multi_f64<6, 3, WIN, SM, MR_THREADS>(n, c_bases64, reinterpret_cast<double*>(st))
+                                   : sprp_multi_f64<2, 2, WIN, SM, MR_THREADS>(n, c_bases32_red64, reinterpret_cast<double*>(st));
+                else
+                    prime = FULL32 ? sprp_multi32<6>(n, c_bases32_full) : sprp_multi32<2>(n, c_bases32_red);
                 if (prime) out[q.p32_idx[i]] = 1;
                 if (count_work) {
                     const unsigned long long d = odd_part(n);
