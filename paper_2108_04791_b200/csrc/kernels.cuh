@@ -940,14 +940,7 @@ __device__ __forceinline__ void gather_segments(bool sort, const unsigned int* _
                                    : (unsigned int)NB;  // sentinel: no element
             }
 #pragma unroll
-            for (int k = 0; k < PER; k++) {
-                const unsigned int peers = __match_any_sync(0xffffffffu, bin[k]);
-                const int leader = __ffs(peers) - 1;
-                unsigned int base = 0;
-                if (lane == leader && bin[k] < NB) base = atomicAdd(&scnt[bin[k]], (unsigned int)__popc(peers));
-                base = __shfl_sync(0xffffffffu, base, leader);
-                rank[k] = base + __popc(peers & ((1u << lane) - 1u));
-            }
+            for (int k = 0; k < PER; k++) rank[k] = bin[k] < NB ? atomicAdd(&scnt[bin[k]], 1u) : 0u;
             __syncthreads();
             for (int b = tid; b < NB; b += SORT_THREADS)
                 if (scnt[b]) sbase[b] = spre[b] + atomicAdd(&gcur[b], scnt[b]);
