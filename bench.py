@@ -236,9 +236,11 @@ def roofline(kern_ms, stats, n, steps, peaks, peaks_kind, clocks, cfg=None):
                         "mulmods = square-and-multiply count of ModExp",
                 "ms_per_step": round(ms, 4)}
     nbytes = HBM_BYTES_PER_ELEM * n
-    if name == "sieve":
+    if name == "dense":   # fused sieve + gather of a dense range: reads N, writes out
+        nbytes = HBM_BYTES_PER_ELEM * n
+    elif name == "sieve":
         nbytes = stats["sieved_integers"] / steps / 16.0 if stats["sieved_integers"] else 0.0
-    elif name != "classify":
+    elif name not in ("classify", "dense"):
         nbytes = n
     achieved = nbytes / (ms * 1e-3) / 1e9
     peak = float(peaks.get("hbm_gbs", 6650.0))

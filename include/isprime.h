@@ -85,7 +85,8 @@ void isprime_shutdown(void);
  * "td_primes32"      number of odd primes (from 3) trial-divided into values
  *                    below 2^32 before Miller-Rabin (0..ISP_MAX_TD)
  * "td_primes64"      same for values >= 2^32
- * "chunk_log2"       device chunk size (elements) = 2^value, 16..31
+ * "chunk_log2"       device chunk size (elements) = 2^value, 16..31 (default 30;
+ *                    halved while the queues of a chunk do not fit in memory)
  * "win64"            exponent window width for the 64-bit multi-base phase (1..3,
  *                    default 3; the window tables live in shared memory)
  * "sieve_cache"      0 (default): every call sieves its own window; 1: a call may

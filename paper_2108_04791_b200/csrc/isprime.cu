@@ -27,7 +27,7 @@ struct Options {
     int bases32 = 3;         // 3 -> {2,7,61}; 7 -> full Eq 4 set
     int td32 = 16;           // odd primes 3..59 (profiles: C2 best at 16)
     int td64 = 32;
-    int chunk_log2 = 28;
+    int chunk_log2 = 30;     // device chunk: 2^30 elements need <= 64 GB of queues (of 180 GB); halved on ENOMEM
     int win64 = 3;           // phase-2 window bits (tables in shared memory; 3 measured best)
     int warp_p = 2048;
     long long sieve_fs_per_int = 700;     // femtoseconds per integer of window (measured: C4 0.68 ps)
@@ -78,8 +78,8 @@ struct Ctx {
 std::vector<Ctx*> g_ctx;
 
 // ---- optional per-kernel timing (events on the launching stream)
-enum { K_PLAN, K_SIEVE, K_CLASSIFY, K_SORT, K_MR1, K_MR2, K_POPCOUNT, K_SMALL, K_NUM };
-const char* const k_names[K_NUM] = {"plan", "sieve", "classify", "sort", "mr1", "mr2", "popcount", "small"};
+enum { K_PLAN, K_SIEVE, K_CLASSIFY, K_SORT, K_MR1, K_MR2, K_POPCOUNT, K_SMALL, K_DENSE, K_NUM };
+const char* const k_names[K_NUM] = {"plan", "sieve", "classify", "sort", "mr1", "mr2", "popcount", "small", "dense"};
 struct KTPending { cudaEvent_t a, b; int kid; };
 std::vector<KTPending> g_kt_pending;
 std::vector<cudaEvent_t> g_ev_pool;
@@ -203,6 +203,7 @@ int init_ctx(Ctx* c) {
     CK(cudaMalloc(&c->plan, sizeof(DevPlan)));
     CK(cudaMemset(c->plan, 0, sizeof(DevPlan)));
     CK(cudaFuncSetAttribute(sieve_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SEG_ODD));
+    CK(cudaFuncSetAttribute(dense_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * SEG_ODD));
     c->grid_sieve = c->sms * occupancy((const void*)sieve_kernel, SIEVE_THREADS, SEG_ODD);
     c->grid_cls = c->sms * occupancy((const void*)classify_kernel<24, 24>, CLS_THREADS, 0);
     if (c->grid_cls > MAX_SEG) c->grid_cls = MAX_SEG;  // one queue segment per classify block
@@ -339,9 +340,15 @@ int launch_mr2(Ctx* c, cudaStream_t s, uint8_t* out, int grid) {
 
 // The whole hot path for dN[0..n) on stream s.  Caller holds g_mu.
 int device_impl(Ctx* c, const unsigned long long* dN, uint8_t* dout, size_t n, cudaStream_t s) {
-    const size_t chunk = (size_t)1 << g_opt.chunk_log2;
-    // classify's per-block queue segments need up to one tile of slack per block
-    int rc = ensure_queues(c, (n < chunk ? n : chunk) + (size_t)c->grid_cls * CLS_TILE);
+    size_t chunk = (size_t)1 << g_opt.chunk_log2;
+    // classify's per-block queue segments need up to one tile of slack per block;
+    // when the device cannot hold the queues of a full chunk, halve the chunk
+    int rc;
+    for (;;) {
+        rc = ensure_queues(c, (n < chunk ? n : chunk) + (size_t)c->grid_cls * CLS_TILE);
+        if (rc != ISP_ENOMEM || chunk <= ((size_t)1 << 24) || n <= ((size_t)1 << 24)) break;
+        chunk >>= 1;
+    }
     if (rc != ISP_OK) return rc;
     if (c->has_last && c->last_stream != (void*)s) CK(cudaStreamWaitEvent(s, c->last_done, 0));
     PlanParams P;
@@ -397,6 +404,16 @@ int device_impl(Ctx* c, const unsigned long long* dN, uint8_t* dout, size_t n, c
             sieve_kernel<<<c->grid_sieve, SIEVE_THREADS, SEG_ODD, s>>>(c->plan, c->bitmap, c->bp, c->nbp, c->patt,
                                                                          first_large);
             CKL("sieve_kernel");
+        }
+        {
+            KScope ks(K_DENSE, s);
+            int first_large = FIRST_CROSS_PRIME_IDX;
+            while (first_large < c->nbp && c->hbp[first_large].x < (uint32_t)g_opt.warp_p) first_large++;
+            // 16-byte loads of element pairs need N 16-B aligned and out 2-B aligned
+            const int vec = ((((uintptr_t)N & 15) == 0) && (((uintptr_t)out & 1) == 0)) ? 1 : 0;
+            dense_kernel<<<c->sms, DENSE_THREADS, 2 * SEG_ODD, s>>>(c->plan, N, out, len, c->bp, c->nbp, c->patt,
+                                                                      first_large, vec);
+            CKL("dense_kernel");
         }
         const uint32_t ntiles = (len + CLS_TILE - 1) / CLS_TILE;
         const int gcls = (int)(ntiles < (uint32_t)c->grid_cls ? ntiles : (uint32_t)c->grid_cls);

@@ -199,6 +199,30 @@ def test_c4_prefix_bit_exact():
     assert_same(gpu(N), oracle.dense_range(0, n), N)
 
 
+def test_dense_range_path_and_fallback():
+    """Chunks the plan samples as a dense range N[i] = N0 + i below 2^32 are
+    sieved and classified in one pass (dense_kernel, no global bitmap).  Odd
+    and even starting points, ragged lengths, multiple chunks, a range ending
+    at 2^32, and ranges with a few foreign elements the sampling cannot see
+    (the kernel detects them and the classify pass redoes the chunk without
+    the window) must all equal the oracle."""
+    cases = [(0, (1 << 21) + 5), (1_000_001, (1 << 20) + 999), ((1 << 32) - (1 << 21) - 3, (1 << 21) + 3),
+             (123_456_788, 3 << 20)]
+    for lo, n in cases:
+        N = np.arange(lo, lo + n, dtype=np.uint64)
+        exp = oracle.dense_range(lo, n)
+        assert_same(gpu(N), exp, N)
+        isp.set_option("chunk_log2", 20)  # several chunks, each its own dense window
+        assert_same(gpu(N), exp, N)
+        isp.set_option("chunk_log2", 28)
+    rng = np.random.default_rng(4)
+    N = np.arange(7_000_000, 7_000_000 + (1 << 21), dtype=np.uint64)
+    hit = rng.choice(N.shape[0], size=37, replace=False)
+    N[hit] = rng.integers(0, 2**64 - 1, size=37, dtype=np.uint64, endpoint=True)
+    N[hit[:5]] = np.array([2, 1, 0, (1 << 64) - 59, 4294967291], dtype=np.uint64)
+    assert_same(gpu(N), oracle.isprime(N), N)
+
+
 def test_c4_shard_window_bit_exact():
     lo = (1 << 32) - (1 << 22) - 99
     N = np.arange(lo, 1 << 32, dtype=np.uint64)

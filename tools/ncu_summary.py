@@ -42,7 +42,8 @@ KEYS = [
 ]
 
 SHORT = {"mr1_kernel": "mr1", "mr2_kernel": "mr2", "classify_kernel": "classify", "sieve_kernel": "sieve",
-         "qscatter_kernel": "sort", "plan_kernel": "plan", "gather_kernel": "classify"}
+         "qscatter_kernel": "sort", "plan_kernel": "plan", "dense_kernel": "dense", "small_kernel": "small",
+         "small_warp_kernel": "small"}
 
 SCALE = {"byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12}
 
