@@ -18,5 +18,5 @@ python tools/explore.py C5 > gpurun_out/ncu_plain_c5.json 2>&1 && \
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:"plan_kernel|sieve_kernel|classify_kernel|qscatter|mr1_kernel|mr2_kernel" -s 18 -c 6 -o gpurun_out/prof_C5 python tools/explore.py C5 > gpurun_out/ncu_full_c5.log 2>&1
 echo "full C5 rc=$?" >> gpurun_out/prof_status.txt
 python tools/explore.py C4 > gpurun_out/ncu_plain_c4.json 2>&1 && \
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:"classify_kernel|sieve_kernel" -s 40 -c 2 -o gpurun_out/prof_C4 python tools/explore.py C4 > gpurun_out/ncu_full_c4.log 2>&1
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:"dense_kernel|classify_kernel|sieve_kernel" -s 9 -c 3 -o gpurun_out/prof_C4 python tools/explore.py C4 > gpurun_out/ncu_full_c4.log 2>&1
 echo "full C4 rc=$?" >> gpurun_out/prof_status.txt
