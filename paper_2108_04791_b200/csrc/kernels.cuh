@@ -656,6 +656,7 @@ dense_kernel(DevPlan* __restrict__ plan, const unsigned long long* __restrict__ 
     unsigned long long nseg;
     seg_layout(span_odd, gridDim.x, SL, nseg);
     const bool producer = threadIdx.x < DENSE_PRODUCERS;
+    const bool odd0 = n0 & 1ull;  // parity of n0 + i for even i (the vector path's pairs)
     const int ctid = (int)threadIdx.x - DENSE_PRODUCERS;  // consumer thread index
     constexpr int NC = DENSE_THREADS - DENSE_PRODUCERS;
     bool fail = false;
@@ -704,7 +705,12 @@ dense_kernel(DevPlan* __restrict__ plan, const unsigned long long* __restrict__ 
                 for (int j = 0; j < U; j++) {
                     const unsigned long long i = bb + 2ull * (ctid + NC * j);
                     if (i < a1) {
-                        const uint32_t r = one(i, t[j].x) | (one(i + 1, t[j].y) << 8);
+                        // pair (i, i + 1) holds n0 + i and n0 + i + 1: one odd value, whose byte
+                        // index is (n0 + i - seg_lo) >> 1 either way, and one even (prime iff 2)
+                        const unsigned long long e0 = n0 + i;
+                        fail |= (t[j].x != e0) | (t[j].y != e0 + 1);
+                        const uint32_t byte = seg[(uint32_t)(e0 - seg_lo) >> 1];
+                        const uint32_t r = odd0 ? byte : ((uint32_t)(e0 == 2ull) | (byte << 8));
                         __stcs(reinterpret_cast<unsigned short*>(out + i), (unsigned short)r);
                     }
                 }
