@@ -1434,26 +1434,53 @@ mr2_kernel(DevPlan* __restrict__ plan, Queues q, uint8_t* __restrict__ out, int 
 template <bool FULL32>
 __global__ void __launch_bounds__(256) small_kernel(const unsigned long long* __restrict__ N, uint8_t* __restrict__ out,
                                                     uint32_t len, TDParams td) {
+    // phase A: trivial cases and trial division per element; the undecided
+    // ones are compacted into a block-local list, so phase B (the strong tests)
+    // runs on dense warps instead of the few lanes trial division left alive
+    __shared__ unsigned long long s_v[256];
+    __shared__ uint32_t s_i[256];
+    __shared__ unsigned int s_n[2];  // FP64-pipe classes from the front, 64-bit Montgomery from the back
+    if (threadIdx.x < 2) s_n[threadIdx.x] = 0;
+    __syncthreads();
     const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= len) return;
-    const unsigned long long v = N[i];
-    uint8_t r;
-    if (v < 2ull) r = 0;
-    else if (!(v & 1ull)) r = (v == 2ull);
-    else if (v < (1ull << 32)) {
-        const uint32_t x = (uint32_t)v;
-        bool comp = false;
-        for (int t = 0; t < td.n32; t++) comp |= (x * c_td_inv32[t] <= c_td_lim32[t]) && (x != c_td_p[t]);
-        if (comp) r = 0;
-        else if (x < td.sq32) r = 1;
-        else if (!sprp2_32(x)) r = 0;
-        else r = FULL32 ? sprp_multi32<6>(x, c_bases32_full) : sprp_multi32<2>(x, c_bases32_red);
-    } else if (v < FP_LIMIT) {
-        r = sprp2_f64(v) && sprp_multi_f64<6, 3, 2>(v, c_bases64);
-    } else {
-        r = sprp2_64(v) && sprp_multi64<6, 3, 2>(v, c_bases64);
+    if (i < len) {
+        const unsigned long long v = N[i];
+        int r = -1;
+        if (v < 2ull) r = 0;
+        else if (!(v & 1ull)) r = (v == 2ull);
+        else if (v < (1ull << 32)) {
+            const uint32_t x = (uint32_t)v;
+            bool comp = false;
+            for (int t = 0; t < td.n32; t++) comp |= (x * c_td_inv32[t] <= c_td_lim32[t]) && (x != c_td_p[t]);
+            if (comp) r = 0;
+            else if (x < td.sq32) r = 1;
+        }
+        if (r >= 0) out[i] = (uint8_t)r;
+        else {
+            const bool fp = v < FP_LIMIT;
+            const unsigned int k = atomicAdd(&s_n[fp ? 0 : 1], 1u);
+            const unsigned int at = fp ? k : 255u - k;
+            s_v[at] = v;
+            s_i[at] = i;
+        }
     }
-    out[i] = r;
+    __syncthreads();
+    // slots: [0, nf) FP64-pipe entries, then from the next warp boundary the
+    // Montgomery entries, so warps are uniform in arithmetic
+    const unsigned int nf = s_n[0], nm = s_n[1], m0 = (nf + 31u) & ~31u;
+    for (unsigned int t = threadIdx.x; t < m0 + nm; t += blockDim.x) {
+        if (t >= nf && t < m0) continue;
+        const unsigned int at = t < nf ? t : 255u - (t - m0);
+        const unsigned long long v = s_v[at];
+        bool r;
+        if (v < FP_LIMIT) {  // 32-bit and FP64 classes on the FP64 pipe (lazy residues)
+            r = sprp2_f64(v) && (v < (1ull << 32) && !FULL32 ? sprp_multi_f64<2, 2, 2>(v, c_bases32_red64)
+                                                             : sprp_multi_f64<6, 3, 2>(v, c_bases64));
+        } else {
+            r = sprp2_64(v) && sprp_multi64<6, 3, 2>(v, c_bases64);
+        }
+        out[s_i[at]] = (uint8_t)r;
+    }
 }
 
 // Scalars and very short arrays: one warp per element, one Eq 4 base per lane
