@@ -901,11 +901,17 @@ classify_kernel(const unsigned long long* __restrict__ N, uint8_t* __restrict__ 
                 *reinterpret_cast<unsigned short*>(ws.res + 2 * lane + 64 * j) = (unsigned short)(r[2 * j] | (r[2 * j + 1] << 8));
             const uint32_t ex = incl - packed;
             uint32_t p32 = ex & 0xFFFFu, p64 = ex >> 16;
+            // one predicated store pair per candidate, no nested branches:
+            // list32 grows from the front, list64 from the back
+            p64 = 255u - p64;
 #pragma unroll
             for (int e = 0; e < 8; e++) {
                 const uint8_t lp = (uint8_t)(2 * lane + 64 * (e >> 1) + (e & 1));
-                if ((m32 >> e) & 1u) { ws.val[p32] = v[e]; ws.pos[p32] = lp; p32++; }
-                else if ((m64 >> e) & 1u) { const uint32_t k = 255u - p64; ws.val[k] = v[e]; ws.pos[k] = lp; p64++; }
+                const uint32_t c32 = (m32 >> e) & 1u, c64 = (m64 >> e) & 1u;
+                const uint32_t k = c32 ? p32 : p64;
+                if (c32 | c64) { ws.val[k] = v[e]; ws.pos[k] = lp; }
+                p32 += c32;
+                p64 -= c64;
             }
             __syncwarp();
             // ---- trial division over the dense lists
