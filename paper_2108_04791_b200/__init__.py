@@ -21,7 +21,8 @@ import numpy as np
 from . import _build
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libisprime.so")
+# ISPRIME_LIB: load another build of the same library (A/B timing of kernel variants)
+LIB_PATH = os.environ.get("ISPRIME_LIB") or os.path.join(_HERE, "libisprime.so")
 
 ISP_OK, ISP_EINVAL, ISP_ENOMEM, ISP_ECUDA, ISP_ENODEV = 0, -1, -2, -3, -4
 

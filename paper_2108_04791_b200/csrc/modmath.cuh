@@ -329,6 +329,138 @@ __device__ __forceinline__ uint64_t mdbl64_if_ptx(uint64_t x, uint64_t n, uint32
     return r;
 }
 
+// ---- lazy additive REDC (n < 2^62) ----------------------------------------
+// With nn = -n^-1 mod 2^64 and m = T mod 2^64 * nn mod 2^64, T + m n is a
+// multiple of R = 2^64 and (T + m n) / R == T R^-1 (mod n).  For inputs below
+// 2n and n < R / 4, T < 4 n^2 and (T + m n) / R < 4 n^2 / R + n < 2n: the
+// result is again below 2n with no final correction, so a ladder keeps lazy
+// representatives in [0, 2n) and reduces once (mcanon64) before comparing.
+// The column sum is three carry chains (T + m0n0 + m1n1, + m0n1, + m1n0):
+// 10 ALU operations against 13 for the subtraction form's sum, borrow and
+// conditional add.  Same 8 IMAD.WIDE + 2 IMAD on the FMA-heavy pipe.
+#define ISP_LZ_REDC_SUM                                  \
+    "mul.wide.u32 W, p0, i0;\n\t"                        \
+    "mov.b64 {m0, m1}, W;\n\t"                           \
+    "mad.lo.u32 m1, p0, i1, m1;\n\t"                     \
+    "mad.lo.u32 m1, t1, i0, m1;\n\t"                     \
+    "mul.wide.u32 W, m0, n0;\n\t"                        \
+    "mov.b64 {q0, q1}, W;\n\t"                           \
+    "mul.wide.u32 W, m0, n1;\n\t"                        \
+    "mov.b64 {a0, a1}, W;\n\t"                           \
+    "mul.wide.u32 W, m1, n0;\n\t"                        \
+    "mov.b64 {b0, b1}, W;\n\t"                           \
+    "mul.wide.u32 W, m1, n1;\n\t"                        \
+    "mov.b64 {d0, d1}, W;\n\t"                           \
+    "add.cc.u32 z, p0, q0;\n\t"                          \
+    "addc.cc.u32 z, t1, q1;\n\t"                         \
+    "addc.cc.u32 r0, t2, d0;\n\t"                        \
+    "addc.u32 r1, t3, d1;\n\t"                           \
+    "add.cc.u32 z, z, a0;\n\t"                           \
+    "addc.cc.u32 r0, r0, a1;\n\t"                        \
+    "addc.u32 r1, r1, 0;\n\t"                            \
+    "add.cc.u32 z, z, b0;\n\t"                           \
+    "addc.cc.u32 r0, r0, b1;\n\t"                        \
+    "addc.u32 r1, r1, 0;\n\t"                            \
+    "mov.b64 %0, {r0, r1};\n\t"
+
+#define ISP_LZ_REGS                                                                  \
+    ".reg .u32 x0, x1, n0, n1, i0, i1, p0, p1, c0, c1, h0, h1, t1, t2, t3, m0, m1;\n\t" \
+    ".reg .u32 q0, q1, a0, a1, b0, b1, d0, d1, r0, r1, z;\n\t"                         \
+    ".reg .u64 W;\n\t"
+
+// x^2 R^-1 mod n, lazily: x < 2n, n < 2^62 -> result < 2n.  nn = -n^-1 mod 2^64.
+__device__ __forceinline__ uint64_t msqr64_lz_ptx(uint64_t x, uint64_t n, uint64_t nn) {
+    uint64_t r;
+    asm("{\n\t" ISP_LZ_REGS
+        "mov.b64 {x0, x1}, %1;\n\t"
+        "mov.b64 {n0, n1}, %2;\n\t"
+        "mov.b64 {i0, i1}, %3;\n\t"
+        "mul.wide.u32 W, x0, x0;\n\t"
+        "mov.b64 {p0, p1}, W;\n\t"
+        "mul.wide.u32 W, x0, x1;\n\t"
+        "mov.b64 {c0, c1}, W;\n\t"
+        "mul.wide.u32 W, x1, x1;\n\t"
+        "mov.b64 {h0, h1}, W;\n\t"
+        "add.cc.u32 t1, p1, c0;\n\t"
+        "addc.cc.u32 t2, h0, c1;\n\t"
+        "addc.u32 t3, h1, 0;\n\t"
+        "add.cc.u32 t1, t1, c0;\n\t"
+        "addc.cc.u32 t2, t2, c1;\n\t"
+        "addc.u32 t3, t3, 0;\n\t"
+        ISP_LZ_REDC_SUM
+        "}"
+        : "=l"(r)
+        : "l"(x), "l"(n), "l"(nn));
+    return r;
+}
+
+// x^2 2^b R^-1 mod n, lazily (b in {0, 1}): x < 2n, n <= 2^61 -> result < 2n
+// (T = 2 x^2 < 8 n^2 <= n R).  The base-2 ladder step of msqr64_shl_ptx
+// without its final correction.
+__device__ __forceinline__ uint64_t msqr64_shl_lz_ptx(uint64_t x, uint64_t n, uint64_t nn, uint32_t b) {
+    uint64_t r;
+    asm("{\n\t" ISP_LZ_REGS
+        "mov.b64 {x0, x1}, %1;\n\t"
+        "mov.b64 {n0, n1}, %2;\n\t"
+        "mov.b64 {i0, i1}, %3;\n\t"
+        "mul.wide.u32 W, x0, x0;\n\t"
+        "mov.b64 {p0, p1}, W;\n\t"
+        "mul.wide.u32 W, x0, x1;\n\t"
+        "mov.b64 {c0, c1}, W;\n\t"
+        "mul.wide.u32 W, x1, x1;\n\t"
+        "mov.b64 {h0, h1}, W;\n\t"
+        "add.cc.u32 t1, p1, c0;\n\t"
+        "addc.cc.u32 t2, h0, c1;\n\t"
+        "addc.u32 t3, h1, 0;\n\t"
+        "add.cc.u32 t1, t1, c0;\n\t"
+        "addc.cc.u32 t2, t2, c1;\n\t"
+        "addc.u32 t3, t3, 0;\n\t"
+        "shf.l.clamp.b32 t3, t2, t3, %4;\n\t"
+        "shf.l.clamp.b32 t2, t1, t2, %4;\n\t"
+        "shf.l.clamp.b32 t1, p0, t1, %4;\n\t"
+        "shl.b32 p0, p0, %4;\n\t"
+        ISP_LZ_REDC_SUM
+        "}"
+        : "=l"(r)
+        : "l"(x), "l"(n), "l"(nn), "r"(b));
+    return r;
+}
+
+// a b R^-1 mod n, lazily: a, b < 2n, n < 2^62 -> result < 2n.
+__device__ __forceinline__ uint64_t mmul64_lz_ptx(uint64_t a, uint64_t b, uint64_t n, uint64_t nn) {
+    uint64_t r;
+    asm("{\n\t" ISP_LZ_REGS
+        ".reg .u32 y0, y1, e0, e1;\n\t"
+        "mov.b64 {x0, x1}, %1;\n\t"
+        "mov.b64 {y0, y1}, %2;\n\t"
+        "mov.b64 {n0, n1}, %3;\n\t"
+        "mov.b64 {i0, i1}, %4;\n\t"
+        "mul.wide.u32 W, x0, y0;\n\t"
+        "mov.b64 {p0, p1}, W;\n\t"
+        "mul.wide.u32 W, x0, y1;\n\t"
+        "mov.b64 {c0, c1}, W;\n\t"
+        "mul.wide.u32 W, x1, y0;\n\t"
+        "mov.b64 {e0, e1}, W;\n\t"
+        "mul.wide.u32 W, x1, y1;\n\t"
+        "mov.b64 {h0, h1}, W;\n\t"
+        "add.cc.u32 t1, p1, c0;\n\t"
+        "addc.cc.u32 t2, h0, c1;\n\t"
+        "addc.u32 t3, h1, 0;\n\t"
+        "add.cc.u32 t1, t1, e0;\n\t"
+        "addc.cc.u32 t2, t2, e1;\n\t"
+        "addc.u32 t3, t3, 0;\n\t"
+        ISP_LZ_REDC_SUM
+        "}"
+        : "=l"(r)
+        : "l"(a), "l"(b), "l"(n), "l"(nn));
+    return r;
+}
+#undef ISP_LZ_REDC_SUM
+#undef ISP_LZ_REGS
+
+// The canonical representative of a lazy x < 2n.
+__device__ __forceinline__ uint64_t mcanon64(uint64_t x, uint64_t n) { return x >= n ? x - n : x; }
+
 // ModAdd, Property 1: a + b mod n = a - (n - b) when a >= n - b.
 __device__ __forceinline__ uint64_t madd64(uint64_t a, uint64_t b, uint64_t n) {
     uint64_t nb = n - b;

@@ -108,8 +108,19 @@ __device__ __forceinline__ bool sprp2_64(uint64_t n) {
         // remaining bits of d, most significant first, from the top of dd
         uint64_t dd = d << (64 - top);
         // warp-uniform choice (queues are ordered by bit length, so warps
-        // rarely straddle 2^63): fused square-and-double below 2^63
-        if (!__any_sync(__activemask(), (unsigned)(n >> 63))) {
+        // rarely straddle 2^61 or 2^63): below 2^61 the fused square-and-double
+        // with lazy representatives in [0, 2n); below 2^63 the same with the
+        // reduction corrected every step; above, square then double
+        const unsigned int act = __activemask();
+        if (!__any_sync(act, (unsigned)(n >> 61))) {
+            const uint64_t nn = 0ull - M.ninv;
+#pragma unroll 2
+            for (int k = 0; k < top; k++) {
+                x = msqr64_shl_lz_ptx(x, n, nn, (uint32_t)(dd >> 63));
+                dd += dd;
+            }
+            x = mcanon64(x, n);
+        } else if (!__any_sync(act, (unsigned)(n >> 63))) {
 #pragma unroll 2
             for (int k = 0; k < top; k++) {
                 x = msqr64_shl_ptx(x, n, M.ninv, (uint32_t)(dd >> 63));
@@ -148,7 +159,9 @@ __device__ __forceinline__ uint64_t sel_table(const uint64_t (&tab)[T], uint32_t
 // entry (base i, digit k) is st[(i (T + 1) + k) * TS] with st = table + t:
 // one LDS per base and window (conflict-free across the warp) replaces the
 // 2T selects of sel_table.  TS = threads per block.
-template <int NB, int WIN, bool SM = false, int TS = 256>
+// LZ (n < 2^62): lazy additive reductions, representatives in [0, 2n),
+// reduced once before the comparisons.
+template <int NB, int WIN, bool SM = false, int TS = 256, bool LZ = false>
 __device__ __forceinline__ bool sprp_lockstep64(const Mont64& M, uint64_t R2, uint64_t d, int s,
                                                 const unsigned long long* bases, unsigned long long* st = nullptr) {
     constexpr int T = (1 << WIN) - 1;
@@ -181,16 +194,28 @@ __device__ __forceinline__ bool sprp_lockstep64(const Mont64& M, uint64_t R2, ui
         uint64_t mt[NB];
 #pragma unroll
         for (int i = 0; i < NB; i++) mt[i] = SM ? st[(i * (T + 1) + digit) * TS] : sel_table<T>(tab[i], digit, M.one);
+        if (LZ) {
+            const uint64_t nn = 0ull - M.ninv;
 #pragma unroll
-        for (int j = 0; j < WIN; j++) {
+            for (int j = 0; j < WIN; j++) {
 #pragma unroll
-            for (int i = 0; i < NB; i++) x[i] = msqr64_ptx(x[i], n, M.ninv);
+                for (int i = 0; i < NB; i++) x[i] = msqr64_lz_ptx(x[i], n, nn);
+            }
+#pragma unroll
+            for (int i = 0; i < NB; i++) x[i] = mmul64_lz_ptx(x[i], mt[i], n, nn);
+        } else {
+#pragma unroll
+            for (int j = 0; j < WIN; j++) {
+#pragma unroll
+                for (int i = 0; i < NB; i++) x[i] = msqr64_ptx(x[i], n, M.ninv);
+            }
+#pragma unroll
+            for (int i = 0; i < NB; i++) x[i] = mmul64_ptx(x[i], mt[i], n, M.ninv);
         }
-#pragma unroll
-        for (int i = 0; i < NB; i++) x[i] = mmul64_ptx(x[i], mt[i], n, M.ninv);
     }
 #pragma unroll
     for (int i = 0; i < NB; i++) {
+        if (LZ) x[i] = mcanon64(x[i], n);
         if (!done[i] && (x[i] == M.one || x[i] == M.mone)) done[i] = pass[i] = true;
     }
     for (int r = 1; r < s; r++) {
@@ -222,6 +247,13 @@ __device__ __forceinline__ bool sprp_multi64(uint64_t n, const unsigned long lon
     uint64_t d = n - 1;
     const int s = __ffsll((long long)d) - 1;
     d >>= s;
+    // warp-uniform: lazy reductions when every active lane's n < 2^62
+    if (!__any_sync(__activemask(), (unsigned)(n >> 62))) {
+#pragma unroll 1
+        for (int g = 0; g < NB; g += G)
+            if (!sprp_lockstep64<G, WIN, SM, TS, true>(M, R2, d, s, bases + g, st)) return false;
+        return true;
+    }
 #pragma unroll 1
     for (int g = 0; g < NB; g += G)
         if (!sprp_lockstep64<G, WIN, SM, TS>(M, R2, d, s, bases + g, st)) return false;
