@@ -96,7 +96,14 @@ void isprime_shutdown(void);
  *                    class; 1: Baillie-PSW for n >= 2^49 -- a strong Lucas test
  *                    (Selfridge parameters) after the base-2 strong test, the
  *                    paper's proposed next step; exact below
- *                    2^64 like Eq 4, so it never changes a bit of out
+ *                    2^64 like Eq 4, so it never changes a bit of out;
+ *                    2: reduced witness sets by magnitude:
+ *                    n < 2^32 base 2 + one base picked by a hash of n (table
+ *                    from tools/gen_witness32.c, checked against every strong
+ *                    base-2 pseudoprime below 2^32); n < 1,122,004,669,633 the
+ *                    Jaeschke set {2, 13, 23, 1662803}; above, Eq 4.  Exact, so
+ *                    it never changes a bit of out.  Applies to the pipeline's
+ *                    witness kernels (the short-array path keeps Eq 4)
  * "small_max"        arrays with n <= small_max (default 131072) and force_path 0
  *                    take one fused launch (trial division + Miller-Rabin per
  *                    element) instead of the plan / sieve / queue pipeline;

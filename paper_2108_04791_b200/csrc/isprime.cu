@@ -39,7 +39,7 @@ struct Options {
     int mr2_group = 3;       // 64-bit phase-2 bases run G at a time in lockstep (3 or 6)
     long long small_max = 1 << 17;  // n <= small_max (and force_path auto): one fused launch
     long long warp_max = 4096;      // n <= warp_max: one warp per element (one base per lane)
-    int witness = 0;         // 0: Eq 4 bases; 1: Baillie-PSW for n >= 2^49     // 1: a call may reuse the bitmap sieved by an earlier call
+    int witness = 0;         // 0: Eq 4 bases; 1: Baillie-PSW for n >= 2^49; 2: reduced sets by magnitude     // 1: a call may reuse the bitmap sieved by an earlier call
 };
 
 Options g_opt;
@@ -321,8 +321,14 @@ int launch_mr2(Ctx* c, cudaStream_t s, uint8_t* out, int grid) {
     const int cw = g_opt.kernel_timing;
     const int g = g_opt.mr2_group == 6 ? 6 : 3;
     if (g_opt.witness == 1) {  // Baillie-PSW for the 64-bit Montgomery class
-        if (full) mr2_kernel<3, true, 3, true><<<grid, MR_THREADS, 0, s>>>(c->plan, c->q, out, cw);
-        else mr2_kernel<3, false, 3, true><<<grid, MR_THREADS, 0, s>>>(c->plan, c->q, out, cw);
+        if (full) mr2_kernel<3, true, 3, 1><<<grid, MR_THREADS, 0, s>>>(c->plan, c->q, out, cw);
+        else mr2_kernel<3, false, 3, 1><<<grid, MR_THREADS, 0, s>>>(c->plan, c->q, out, cw);
+        CKL("mr2_kernel");
+        return ISP_OK;
+    }
+    if (g_opt.witness == 2) {  // reduced witness sets by magnitude
+        if (full) mr2_kernel<3, true, 3, 2><<<grid, MR_THREADS, 0, s>>>(c->plan, c->q, out, cw);
+        else mr2_kernel<3, false, 3, 2><<<grid, MR_THREADS, 0, s>>>(c->plan, c->q, out, cw);
         CKL("mr2_kernel");
         return ISP_OK;
     }
@@ -630,7 +636,7 @@ int isprime_set_option(const char* key, long long v) {
     else if (!strcmp(key, "sieve_cache")) { if (v < 0 || v > 1) return ISP_EINVAL; g_opt.sieve_cache = (int)v; }
     else if (!strcmp(key, "small_max")) { if (v < 0) return ISP_EINVAL; g_opt.small_max = v; }
     else if (!strcmp(key, "warp_max")) { if (v < 0 || v > (1 << 26)) return ISP_EINVAL; g_opt.warp_max = v; }
-    else if (!strcmp(key, "witness")) { if (v < 0 || v > 1) return ISP_EINVAL; g_opt.witness = (int)v; }
+    else if (!strcmp(key, "witness")) { if (v < 0 || v > 2) return ISP_EINVAL; g_opt.witness = (int)v; }
     else return ISP_EINVAL;
     return ISP_OK;
 }

@@ -16,6 +16,7 @@
 #pragma once
 #include <stdint.h>
 #include "witness.cuh"
+#include "witness32_table.h"
 
 namespace isp {
 
@@ -98,6 +99,18 @@ __constant__ unsigned long long c_bases64[6] = {325ull, 9375ull, 28178ull, 45077
 __constant__ uint32_t c_bases32_full[6] = {325u, 9375u, 28178u, 450775u, 9780504u, 1795265022u};
 __constant__ uint32_t c_bases32_red[2] = {7u, 61u};
 __constant__ unsigned long long c_bases32_red64[2] = {7ull, 61ull};
+// option witness = 2 (reduced witness sets by magnitude):
+// n < 2^32: base 2, then one base chosen by a hash of n (witness32_table.h,
+// tools/gen_witness32.c); 2^32 <= n < kJaeschkeBound4: bases {2, 13, 23,
+// 1662803}, exact below 1,122,004,669,633 (G. Jaeschke, "On strong
+// pseudoprimes to several bases", Math. Comp. 61 (1993); the bound itself is
+// a strong pseudoprime to all four, pinned by the CPU tests); above: Eq 4.
+__constant__ unsigned long long c_bases_j4[3] = {13ull, 23ull, 1662803ull};
+constexpr unsigned long long kJaeschkeBound4 = 1122004669633ull;
+__device__ const uint16_t c_hash_base32[256] = {ISP_HASH_BASE32_LIST};
+__device__ __forceinline__ unsigned long long hash_base32(uint32_t n) {
+    return c_hash_base32[(n * ISP_HASH_MUL32) >> 24];
+}
 // 32-bit class of the witness kernels on the FP64 pipe (lazy signed residues,
 // modmath.cuh fmul_lazy) instead of 32-bit Montgomery on the IMAD / ALU pipes
 #ifndef CLS32_FP64
@@ -1252,19 +1265,30 @@ __device__ __forceinline__ void stage_flush(WarpStage<T>& st, unsigned int& n, u
 // plenty of work remains, then single rounds of 32 (guided self-scheduling):
 // a warp that claims a 256-entry chunk near the end would otherwise run alone
 // for eight rounds while the rest of the GPU idles.
+// Chunks of MR_CHUNK entries per atomicAdd while plenty of work remains,
+// then shrinking with the work left: ceil(left / (div nw)) rounded up to 32,
+// at least 32 (guided self-scheduling; nw = warps of the grid).  A warp that
+// claims a 256-entry chunk near the end would otherwise run alone for eight
+// rounds while the rest of the GPU idles; claiming 32 at a time from the
+// start costs an atomic round trip per round, which cheap 32-bit entries
+// cannot hide.  div[r] = 0: fixed MR_CHUNK for region r.
 constexpr unsigned int MR_CHUNK = 256;
 constexpr unsigned int MR_CHUNK_TAIL = 32;
 
 __device__ __forceinline__ bool next_chunk(const unsigned int (&size)[3], unsigned int* cur, int& r, int& tried,
-                                           unsigned int& start, unsigned int& end, unsigned int tail) {
+                                           unsigned int& start, unsigned int& end, unsigned int nw,
+                                           const unsigned int (&div)[3]) {
     const int lane = threadIdx.x & 31;
     while (tried != 7) {
         if (!((tried >> r) & 1)) {
             unsigned int s0 = 0xFFFFFFFFu, ch = MR_CHUNK;
             if (size[r] && lane == 0) {
                 const unsigned int seen = *reinterpret_cast<volatile unsigned int*>(&cur[r]);  // racy estimate
-                ch = seen + tail < size[r] ? MR_CHUNK : MR_CHUNK_TAIL;
-                s0 = atomicAdd(&cur[r], ch);
+                if (div[r] && seen < size[r]) {
+                    const unsigned int g = ((size[r] - seen) / (div[r] * nw) + 31u) & ~31u;
+                    ch = g < MR_CHUNK_TAIL ? MR_CHUNK_TAIL : (g > MR_CHUNK ? MR_CHUNK : g);
+                }
+                s0 = seen < size[r] ? atomicAdd(&cur[r], ch) : seen;
             }
             s0 = __shfl_sync(0xffffffffu, s0, 0);
             ch = __shfl_sync(0xffffffffu, ch, 0);
@@ -1315,9 +1339,11 @@ mr1_kernel(DevPlan* __restrict__ plan, Queues q, int count_work) {
     const unsigned int gwarp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     int r = (int)(gwarp % 3u), tried = 0;
     unsigned int start = 0, n32s = 0, n64i = 0, n64f = 0;
-    // base-2 rounds are short: whole chunks to the end (tail 0)
     unsigned int end = 0;
-    while (next_chunk(size, plan->cur1, r, tried, start, end, 0u)) {
+    // base-2 rounds of 32-bit entries are short: whole chunks (div 0); the
+    // 64-bit classes shrink their chunks towards the end
+    const unsigned int div[3] = {0u, 2u, 2u};
+    while (next_chunk(size, plan->cur1, r, tried, start, end, gridDim.x * (MR_THREADS / 32), div)) {
         for (unsigned int b = start; b < end; b += 32) {
             const unsigned int i = b + lane;
             const bool act = i < end;
@@ -1366,7 +1392,7 @@ mr1_kernel(DevPlan* __restrict__ plan, Queues q, int count_work) {
 }
 
 // ------------------------------------------------------------- A4: MR phase 2
-template <int WIN, bool FULL32, int G64, bool LUCAS = false>
+template <int WIN, bool FULL32, int G64, int WIT = 0>
 __global__ void __launch_bounds__(MR_THREADS)
 mr2_kernel(DevPlan* __restrict__ plan, Queues q, uint8_t* __restrict__ out, int count_work) {
     // window tables of the lockstep bases in shared memory (transposed per thread)
@@ -1380,17 +1406,20 @@ mr2_kernel(DevPlan* __restrict__ plan, Queues q, uint8_t* __restrict__ out, int 
     const unsigned int gwarp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     int r = (int)(gwarp % 3u), tried = 0;
     unsigned int start = 0;
-    // tail: about one 256-entry chunk per warp of the grid left
-    const unsigned int tail = gridDim.x * (MR_THREADS / 32) * MR_CHUNK;
+    const unsigned int nw = gridDim.x * (MR_THREADS / 32);  // guided chunk sizes
     unsigned int end = 0;
-    while (next_chunk(size, plan->cur2, r, tried, start, end, tail)) {
+    const unsigned int div[3] = {1u, 2u, 2u};
+    while (next_chunk(size, plan->cur2, r, tried, start, end, nw, div)) {
         for (unsigned int b = start; b < end; b += 32) {
             const unsigned int i = b + lane;
             if (i >= end) continue;
             if (r == 0) {
                 const uint32_t n = q.p32_val[i];
                 bool prime;
-                if (CLS32_FP64)  // the 32-bit class on the FP64 pipe (exact below 2^49)
+                if (WIT == 2 && !FULL32) {  // one hashed base after base 2
+                    const unsigned long long a = hash_base32(n);
+                    prime = sprp_multi_f64<1, 1, WIN, SM, MR_THREADS>(n, &a, reinterpret_cast<double*>(st));
+                } else if (CLS32_FP64)  // the 32-bit class on the FP64 pipe (exact below 2^49)
                     prime = FULL32 ? sprp_multi_f64<6, 3, WIN, SM, MR_THREADS>(n, c_bases64, reinterpret_cast<double*>(st))
                                    : sprp_multi_f64<2, 2, WIN, SM, MR_THREADS>(n, c_bases32_red64, reinterpret_cast<double*>(st));
                 else
@@ -1398,19 +1427,21 @@ mr2_kernel(DevPlan* __restrict__ plan, Queues q, uint8_t* __restrict__ out, int 
                 if (prime) out[q.p32_idx[i]] = 1;
                 if (count_work) {
                     const unsigned long long d = odd_part(n);
-                    w32 += (unsigned long long)(FULL32 ? 6 : 2) * (modexp_squarings(d) + modexp_mults(d));
+                    w32 += (unsigned long long)(FULL32 ? 6 : WIT == 2 ? 1 : 2) * (modexp_squarings(d) + modexp_mults(d));
                 }
             } else {
                 const unsigned int k = r == 1 ? q.cap - 1 - i : i;
                 const unsigned long long n = q.p64_val[k];
                 const bool fp = n < FP_LIMIT;
-                // LUCAS: Baillie-PSW for the Montgomery class (strong Lucas after the base-2 phase)
-                const bool prime = fp ? sprp_multi_f64<6, G64, WIN, SM, MR_THREADS>(n, c_bases64, reinterpret_cast<double*>(st))
-                                      : (LUCAS ? slprp64(n) : sprp_multi64<6, G64, WIN, SM, MR_THREADS>(n, c_bases64, st));
+                const bool j4 = WIT == 2 && n < kJaeschkeBound4;
+                // WIT 1: Baillie-PSW for the Montgomery class (strong Lucas after the base-2 phase)
+                const bool prime = j4 ? sprp_multi_f64<3, 3, WIN, SM, MR_THREADS>(n, c_bases_j4, reinterpret_cast<double*>(st))
+                                 : fp ? sprp_multi_f64<6, G64, WIN, SM, MR_THREADS>(n, c_bases64, reinterpret_cast<double*>(st))
+                                      : (WIT == 1 ? slprp64(n) : sprp_multi64<6, G64, WIN, SM, MR_THREADS>(n, c_bases64, st));
                 if (prime) out[q.p64_idx[k]] = 1;
                 if (count_work) {
                     const unsigned long long d = odd_part(n);
-                    const unsigned long long w = 6ull * (modexp_squarings(d) + modexp_mults(d));
+                    const unsigned long long w = (j4 ? 3ull : 6ull) * (modexp_squarings(d) + modexp_mults(d));
                     if (fp) wf += w; else w64 += w;
                 }
             }

@@ -71,7 +71,7 @@ def test_options_validate():
     isp.set_option("win64", 3)
     assert isp.get_option("win64") == 3
     isp.set_option("win64", old)
-    for key, bad, good in (("witness", 2, 1), ("small_max", -1, 0), ("warp_max", -1, 64)):
+    for key, bad, good in (("witness", 3, 2), ("small_max", -1, 0), ("warp_max", -1, 64)):
         saved = isp.get_option(key)
         with pytest.raises(isp.IsPrimeError):
             isp.set_option(key, bad)

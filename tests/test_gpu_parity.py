@@ -51,7 +51,8 @@ def assert_same(got, exp, N=None):
 @pytest.fixture(autouse=True)
 def _default_options():
     saved = {k: isp.get_option(k) for k in ("force_path", "bases32", "td_primes32", "td_primes64",
-                                             "chunk_log2", "win64", "warp_p", "small_max", "warp_max")}
+                                             "chunk_log2", "win64", "warp_p", "small_max", "warp_max",
+                                             "witness")}
     yield
     for k, v in saved.items():
         isp.set_option(k, v)
@@ -162,6 +163,39 @@ def test_bpsw_witness_option():
         isp.set_option("witness", saved)
 
 
+def test_reduced_witness_option():
+    """Option witness = 2: below 2^32 base 2 plus one
+    hashed base, below 1,122,004,669,633 the Jaeschke set {2, 13, 23,
+    1662803}, above the Eq 4 set.  Every strong base-2 pseudoprime below 2^32
+    (the oracle's list) must come out composite, the Jaeschke bound itself and
+    the odd values around it must equal the oracle, and so must seeded data of
+    every magnitude and the full C2 / C5 counts."""
+    isp.set_option("witness", 2)
+    isp.set_option("small_max", 0)
+    spsp = np.array([int(r[0]) for r in _rows("spsp2_below_2p32.txt")], dtype=np.uint64)
+    assert spsp.shape[0] == 2314
+    assert not gpu(spsp).any()
+    B = 1122004669633
+    rng = np.random.default_rng(11)
+    near = np.concatenate([np.arange(B - 200_001, B + 200_001, 2, dtype=np.uint64),
+                           np.array([B], dtype=np.uint64),
+                           rng.integers(1 << 32, 1 << 42, size=1 << 20, dtype=np.uint64) | np.uint64(1)])
+    cs = np.array(workloads.chernick_numbers(), dtype=np.uint64)
+    vals = np.array([int(r[0]) for r in _rows("special_values.txt")], dtype=np.uint64)
+    for N in (near, cs, np.tile(vals, 64), workloads.generate("C2", count=(1 << 20) + 5),
+              workloads.generate("C5", count=(1 << 20) + 4097)):
+        assert_same(gpu(N), oracle.isprime(N), N)
+    assert gpu(np.array([B], dtype=np.uint64))[0] == 0
+    for cfg in ("C2", "C5"):
+        N = workloads.generate(cfg)
+        dN = torch.from_numpy(N.view(np.int64)).to(DEV)
+        dout = torch.empty(N.shape[0], dtype=torch.uint8, device=DEV)
+        dcount = torch.zeros(1, dtype=torch.int64, device=DEV)
+        isp.isprime_count_device(dN, dout, dcount)
+        torch.cuda.synchronize()
+        assert int(dcount.item()) == _counts()[cfg], cfg
+
+
 @pytest.mark.parametrize("count", [3000, 300_000])
 def test_base2_ladder_around_2_63(count):
     """The base-2 ladder fuses its doubling into the reduction below 2^63 and
@@ -229,7 +263,7 @@ def test_c4_shard_window_bit_exact():
     assert_same(gpu(N), oracle.dense_range(lo, N.shape[0]), N)
 
 
-@pytest.mark.parametrize("witness", [0, 1])
+@pytest.mark.parametrize("witness", [0, 1, 2])
 def test_random_all_magnitudes_bit_exact(witness):
     """2^22 values drawn three ways -- uniform over all of [0, 2^64), uniform
     bit length 1..64, and odd values just above/below powers of two -- through
@@ -304,12 +338,13 @@ def test_c4_full_dense_range_pi_2_32():
 def test_force_path_equivalence_all_32bit():
     """SPEC.md:392 analogue over the ENTIRE 32-bit domain: sieve path vs
     trial-division + Miller-Rabin path ({2,7,61}) vs Miller-Rabin with the full
-    Eq 4 base set.  Exhaustive GPU self-consistency; with the C4 count above it
-    ties the reduced base set to pi(2^32)."""
+    Eq 4 base set vs base 2 + one hashed base (option witness = 2).
+    Exhaustive GPU self-consistency; with the C4 count above it ties the
+    reduced base sets to pi(2^32)."""
     step = 1 << 28
     outs = {}
     dN = torch.empty(step, dtype=torch.int64, device=DEV)
-    o = {k: torch.empty(step, dtype=torch.uint8, device=DEV) for k in ("sieve", "mr3", "mr7")}
+    o = {k: torch.empty(step, dtype=torch.uint8, device=DEV) for k in ("sieve", "mr3", "mr7", "mrh")}
     total = 0
     for base in range(0, 1 << 32, step):
         torch.arange(base, base + step, dtype=torch.int64, device=DEV, out=dN)
@@ -319,9 +354,13 @@ def test_force_path_equivalence_all_32bit():
         isp.isprime_device(dN, o["mr3"])
         isp.set_option("bases32", 7)
         isp.isprime_device(dN, o["mr7"])
+        isp.set_option("bases32", 3); isp.set_option("witness", 2)  # base 2 + hashed base
+        isp.isprime_device(dN, o["mrh"])
+        isp.set_option("witness", 0)
         torch.cuda.synchronize()
         assert torch.equal(o["sieve"], o["mr3"]), base
         assert torch.equal(o["sieve"], o["mr7"]), base
+        assert torch.equal(o["sieve"], o["mrh"]), base
         total += int(o["sieve"].sum(dtype=torch.int64).item())
     assert total == 203280221
 
@@ -333,7 +372,7 @@ def test_options_do_not_change_results():
     exp = oracle.isprime(N)
     for key, vals in (("td_primes32", (0, 1, 5, 128)), ("td_primes64", (0, 3, 128)), ("win64", (1, 2, 3)),
                       ("force_path", (0, 1, 2)), ("chunk_log2", (16, 17, 28)), ("warp_p", (17, 600, 65536)),
-                      ("witness", (1, 0))):
+                      ("witness", (1, 2, 0))):
         saved = isp.get_option(key)
         for v in vals:
             isp.set_option(key, v)

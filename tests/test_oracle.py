@@ -251,3 +251,68 @@ def test_c1_prime_count():
     """Config C1's prime count (SURVEY.md 8(d) golden table: 7937)."""
     row = [r for r in _rows("generator.txt") if r[0] == "C1"][0]
     assert oracle.isprime(workloads.generate("C1")).sum() == int(row[3])
+
+
+# ---- reduced witness sets (option witness = 2, SURVEY.md 8(f) f1) ----------
+_CSRC = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "paper_2108_04791_b200", "csrc")
+
+
+def _hash_table():
+    """The product's hashed-base table, read from its generated header (the
+    numbers only; nothing of the product is imported)."""
+    txt = open(os.path.join(_CSRC, "witness32_table.h")).read()
+    mul = int(txt.split("#define ISP_HASH_MUL32", 1)[1].split()[0].rstrip("u"), 16)
+    body = txt.split("#define ISP_HASH_BASE32_LIST", 1)[1]
+    bases = [int(x) for x in body.replace("\\", " ").replace(",", " ").split()]
+    assert len(bases) == 256
+    return mul, bases
+
+
+def test_spsp2_golden_list():
+    """tests/golden/spsp2_below_2p32.txt (tests/golden/make_spsp2.py, oracle/
+    only): 2314 entries = the survey's independent count (SURVEY.md Appendix
+    A), starting 2047, 3277, 4033, 4681, 8321; each entry is
+    composite (sympy) and a strong probable prime to base 2 (oracle)."""
+    spsp = [int(r[0]) for r in _rows("spsp2_below_2p32.txt")]
+    assert len(spsp) == 2314 and spsp == sorted(set(spsp))
+    assert spsp[:5] == [2047, 3277, 4033, 4681, 8321] and spsp[-1] < 2**32
+    rng = np.random.default_rng(3)
+    for n in rng.choice(spsp, size=200, replace=False).tolist() + spsp[:20] + spsp[-20:]:
+        assert not sympy.isprime(n) and oracle.sprp(n, 2), n
+    ok = oracle.sprp_array(np.array(spsp, dtype=np.uint64), np.full(len(spsp), 2, dtype=np.uint64))
+    assert ok.all()
+
+
+def test_hash32_table_rejects_every_spsp2():
+    """Exactness of "base 2 + hashed base" below 2^32: a composite n < 2^32
+    that passes base 2 is in the oracle's list, and the product's table base
+    for n's bucket must reject it (oracle strong test).  Bases are < 2047, so a
+    base is never 0 mod such n (reading G3 cannot let one through)."""
+    mul, bases = _hash_table()
+    assert all(3 <= a < 2047 for a in bases)
+    spsp = np.array([int(r[0]) for r in _rows("spsp2_below_2p32.txt")], dtype=np.uint64)
+    h = ((spsp * np.uint64(mul)) & np.uint64(0xFFFFFFFF)) >> np.uint64(24)
+    a = np.array(bases, dtype=np.uint64)[h.astype(np.int64)]
+    assert not oracle.sprp_array(spsp, a).any()
+
+
+def test_jaeschke_set_bound_is_tight():
+    """{2, 13, 23, 1662803} is exact below 1,122,004,669,633 (Jaeschke 1993);
+    the bound is the smallest composite passing all four, so it must be
+    composite and pass each of them -- a misremembered base or bound fails
+    here.  The product's constants (csrc/kernels.cuh) must be these numbers."""
+    B = 1122004669633
+    assert not sympy.isprime(B) and not oracle.isprime_u64(B)
+    for a in (2, 13, 23, 1662803):
+        assert oracle.sprp(B, a), a
+    assert not all(oracle.sprp(B, a) for a in oracle.BASES)
+    src = open(os.path.join(_CSRC, "kernels.cuh")).read()
+    assert "c_bases_j4[3] = {13ull, 23ull, 1662803ull}" in src
+    assert f"kJaeschkeBound4 = {B}ull" in src
+    # below the bound the four bases agree with the oracle on seeded odd values
+    rng = np.random.default_rng(7)
+    n = rng.integers(1 << 32, B, size=20000, dtype=np.uint64) | np.uint64(1)
+    passed = np.ones(n.shape[0], dtype=bool)
+    for a in (2, 13, 23, 1662803):
+        passed &= oracle.sprp_array(n, np.full(n.shape[0], a, dtype=np.uint64)).astype(bool)
+    assert np.array_equal(passed, oracle.isprime(n).astype(bool))
