@@ -295,15 +295,17 @@ def run_reference(args, rank, world):
     print(json.dumps(line), flush=True)
 
 
-def witness_bpsw(isp, torch, dev, stream, args, counts):
-    """Option witness = 1 (Baillie-PSW: a strong Lucas test replaces the six
-    remaining Eq 4 bases for n >= 2^49 -- the paper's proposed next step,
-    PAPER.md:425-426).  Same workloads, same timing; the headline above is the
-    paper's Eq 4 method."""
+def witness_option(isp, torch, dev, stream, args, counts, mode, cfgs):
+    """Another exact witness mode on the same workloads with the same timing;
+    the headline above is the paper's Eq 4 method.  mode 1: Baillie-PSW (a
+    strong Lucas test replaces the six remaining Eq 4 bases for n >= 2^49, the
+    paper's proposed next step); mode 2: reduced witness sets
+    by magnitude (base 2 + one hashed base below 2^32,
+    Jaeschke's four bases below 1,122,004,669,633)."""
     res = {}
-    isp.set_option("witness", 1)
+    isp.set_option("witness", mode)
     try:
-        for c in ("C5", "C3"):
+        for c in cfgs:
             cn = workloads.CONFIGS[c][1]
             cN, _ = make_input(c, 0, torch, dev)
             cout = torch.empty(cn, dtype=torch.uint8, device=dev)
@@ -488,7 +490,8 @@ def main():
                 torch.cuda.empty_cache()
             line["per_config"] = per
         line["scalar_latency"] = scalar_latency(isp, torch, dev, stream)
-        line["witness_bpsw"] = witness_bpsw(isp, torch, dev, stream, args, counts)
+        line["witness_bpsw"] = witness_option(isp, torch, dev, stream, args, counts, 1, ("C5", "C3"))
+        line["witness_reduced"] = witness_option(isp, torch, dev, stream, args, counts, 2, ("C5", "C2"))
     if rank == 0:
         print(json.dumps(line), flush=True)
     if dist:
