@@ -39,7 +39,7 @@ struct Options {
     int mr2_group = 3;       // 64-bit phase-2 bases run G at a time in lockstep (3 or 6)
     long long small_max = 1 << 17;  // n <= small_max (and force_path auto): one fused launch
     long long warp_max = 4096;      // n <= warp_max: one warp per element (one base per lane)
-    int witness = 0;         // 0: Eq 4 bases; 1: Baillie-PSW for n >= 2^49; 2: reduced sets by magnitude     // 1: a call may reuse the bitmap sieved by an earlier call
+    int witness = 0;         // 0: Eq 4 bases; 1: Baillie-PSW for n >= 2^50; 2: reduced sets by magnitude     // 1: a call may reuse the bitmap sieved by an earlier call
 };
 
 Options g_opt;

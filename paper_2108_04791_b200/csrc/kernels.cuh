@@ -1150,10 +1150,10 @@ __device__ __forceinline__ bool sort_pays(const unsigned int* bins, int nb) {
     }
     if (cnt < 4096) return false;
     if ((double)sum < 0.92 * (double)mx * (double)cnt) return true;
-    // both sides of the FP64 / Montgomery boundary (bit length 49 | 50) present
+    // both sides of the FP64 / Montgomery boundary (bit length FP_BITS | FP_BITS + 1) present
     if (nb == 65) {
         unsigned long long lo = 0;
-        for (int b = 0; b <= 49; b++) lo += bins[b];
+        for (int b = 0; b <= FP_BITS; b++) lo += bins[b];
         if (lo > cnt / 64 && lo < cnt - cnt / 64) return true;
         // both sides of 2^63 (bit length 63 | 64): the base-2 ladder fuses its
         // doubling into the reduction only below 2^63, chosen per warp
@@ -1315,7 +1315,7 @@ __device__ __forceinline__ unsigned long long odd_part(unsigned long long n) { r
 __device__ __forceinline__ unsigned int fp_class_count(const DevPlan* plan) {
     if (!plan->sorted64) return 0u;
     unsigned int c = 0;
-    for (int b = 0; b <= 49; b++) c += plan->bins64[b];  // bit length <= 49 <=> n < 2^49
+    for (int b = 0; b <= FP_BITS; b++) c += plan->bins64[b];  // bit length <= FP_BITS <=> n < FP_LIMIT
     return c;
 }
 
@@ -1365,7 +1365,7 @@ mr1_kernel(DevPlan* __restrict__ plan, Queues q, int count_work) {
                 if (act) {
                     n = q64v[k];
                     idx = q64i[k];
-                    // magnitude-class dispatch: below 2^49 on the FP64 pipe, above with
+                    // magnitude-class dispatch: below 2^50 on the FP64 pipe, above with
                     // 64-bit Montgomery (uniform per region when the queue is sorted)
                     fp = n < FP_LIMIT;
                     pass = fp ? sprp2_f64(n) : sprp2_64(n);
@@ -1419,7 +1419,7 @@ mr2_kernel(DevPlan* __restrict__ plan, Queues q, uint8_t* __restrict__ out, int 
                 if (WIT == 2 && !FULL32) {  // one hashed base after base 2
                     const unsigned long long a = hash_base32(n);
                     prime = sprp_multi_f64<1, 1, WIN, SM, MR_THREADS>(n, &a, reinterpret_cast<double*>(st));
-                } else if (CLS32_FP64)  // the 32-bit class on the FP64 pipe (exact below 2^49)
+                } else if (CLS32_FP64)  // the 32-bit class on the FP64 pipe (exact below 2^50)
                     prime = FULL32 ? sprp_multi_f64<6, 3, WIN, SM, MR_THREADS>(n, c_bases64, reinterpret_cast<double*>(st))
                                    : sprp_multi_f64<2, 2, WIN, SM, MR_THREADS>(n, c_bases32_red64, reinterpret_cast<double*>(st));
                 else

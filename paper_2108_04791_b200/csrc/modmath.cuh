@@ -507,18 +507,21 @@ __device__ __forceinline__ uint64_t mont64_r2(const Mont64& M) {
     return x;
 }
 
-// ------------------------------------------------------- FP64, n < 2^49 ----
+// ------------------------------------------------------- FP64, n < 2^50 ----
 // The paper's medium class (2^18 .. 2^49) is the range where
 // double precision is exact -- and on B200 the FP64 pipe issues 64 DFMA
 // lanes/clk/SM (profiles/r1_imad_peak.json: 63.1) against 25 for the
-// IMAD.WIDE.U32 that 64-bit Montgomery needs.  For odd n < 2^49 and a, b < n:
-//   h = fl(ab), l = fma(a, b, -h) = ab - h exactly (|l| <= 2^45),
-//   q = nearest integer to fl(h * fl(1/n)): |q - ab/n| < 0.7,
-//   r = fma(-q, n, h) + l = ab - qn exactly (|r| < 2^50), in (-n, n),
+// IMAD.WIDE.U32 that 64-bit Montgomery needs.  For odd n < 2^50 and a, b < n:
+//   h = fl(ab), l = fma(a, b, -h) = ab - h exactly (|l| <= 2^46),
+//   q = nearest integer to fl(h * fl(1/n)): |q - ab/n| < 1/2 + 1/8 + 1/8,
+//   r = fma(-q, n, h) + l = ab - qn exactly, in (-n, n),
 // and one conditional +n gives ab mod n.  Rounding to an integer uses the
-// 1.5 * 2^52 addend (valid for |x| < 2^51).
+// 1.5 * 2^52 addend (valid for |x| < 2^51).  (The paper's class boundary is
+// 2^49; the arithmetic's is 2^50, so the 50-bit values join the FP64 class.)
 constexpr double FP_RND = 6755399441055744.0;  // 1.5 * 2^52
-constexpr unsigned long long FP_LIMIT = 1ull << 49;
+// The FP64 class: odd n < 2^FP_BITS (fmul_lazy's bound below holds to 2^50).
+constexpr int FP_BITS = 50;
+constexpr unsigned long long FP_LIMIT = 1ull << FP_BITS;
 
 struct ModF {
     double n, ninv, nm1;  // n, fl(1/n), n - 1
@@ -541,13 +544,16 @@ __device__ __forceinline__ double fmulmod(double a, double b, const ModF& M) {
 }
 
 // Lazy signed product for the witness loops: a, b exact integers with |a| <
-// 2n, |b| < n (n < 2^49).  Returns the signed representative r == a*b (mod n)
-// with |r| < 0.75 n -- no final correction, because the next square does not
-// care about the sign and every later product accepts |.| < n.
-//   h + l = a b exactly (|ab| < 2 n^2 < 2^99, |l| <= ulp(h)/2 <= n 2^-52 * n);
-//   q = round(h * fl(1/n)) in one FMA with the 1.5 * 2^52 addend:
-//       |q - ab/n| <= 1/2 + |l|/n + (h/n) 2^-53 < 3/4;
-//   r = fma(-q, n, h) + l: both steps exact (|h - qn| < n + |l| < 2^50).
+// 2n, |b| < n, n < 2^50.  Returns the signed representative r == a*b (mod n)
+// with |r| < n -- no final correction, because the next square does not care
+// about the sign and every later product accepts |.| < n.
+//   h + l = a b exactly (|ab| < 2 n^2 < 2^101, so |l| <= ulp(h)/2 <= 2^47);
+//   q = round(h * fl(1/n)) in one FMA with the 1.5 * 2^52 addend (valid since
+//       |h / n| < 2n <= 2^51):
+//       |q - ab/n| <= 1/2 + (h/n) 2^-53 + |l|/n < 1/2 + 1/4 + 1/4 = 1
+//       (n < 2^49: < 1/2 + 1/8 + 1/8, |r| < 0.75 n; the bit-length sort
+//       keeps 2^49 <= n < 2^50 in warps of their own either way);
+//   r = fma(-q, n, h) + l: both steps exact (integers, |h - qn| < n + |l| < 2^51).
 // 7 FP64-pipe instructions for a square-and-double step (fsqr_lazy with f = 2)
 // against 10 FP64 + 4 select/compare instructions for fmulmod + faddmod.
 __device__ __forceinline__ double fmul_lazy(double a, double b, const ModF& M) {

@@ -261,7 +261,7 @@ __device__ __forceinline__ bool sprp_multi64(uint64_t n, const unsigned long lon
 }
 
 // ------------------------------------------------------- FP64 class ----
-// The same two phases on the FP64 pipe for odd n < 2^49 (modmath.cuh, ModF):
+// The same two phases on the FP64 pipe for odd n < 2^50 (modmath.cuh, ModF):
 // plain residues (no Montgomery form) kept as signed lazy representatives
 // |x| < n, so 1 is 1.0 or 1 - n and -1 is -1.0 or n - 1.
 __device__ __forceinline__ bool sprp2_f64(unsigned long long n) {

@@ -90,7 +90,7 @@ def test_chernick_and_pseudoprimes():
 
 
 def test_boundary_primes_and_neighbours():
-    centres = [2**18, 2**20, 2**31, 2**32, 2**33, 2**49, 2**52, 2**53, 2**62, 2**63, 2**64 - 1]
+    centres = [2**18, 2**20, 2**31, 2**32, 2**33, 2**49, 2**50, 2**52, 2**53, 2**61, 2**62, 2**63, 2**64 - 1]
     vals = []
     for c in centres:
         lo = max(0, c - 3000)
@@ -101,6 +101,27 @@ def test_boundary_primes_and_neighbours():
     for small_max in (0, 1 << 17):  # pipeline and short-array path
         isp.set_option("small_max", small_max)
         assert_same(gpu(N), exp, N)
+
+
+@pytest.mark.parametrize("witness", [0, 1, 2])
+def test_fp64_class_top_bit_exact(witness):
+    """The FP64 class reaches 2^50 (modmath.cuh fmul_lazy: |q - ab/n| < 1, so
+    |r| < n, at the top of the range): 2^20 random odd values with bit length
+    50 and 49, the odd values just below 2^50, products of two primes near
+    2^25, through the pipeline (every witness mode) and the short-array path."""
+    isp.set_option("witness", witness)
+    rng = np.random.default_rng(50 + witness)
+    top = rng.integers(1 << 49, 1 << 50, size=1 << 19, dtype=np.uint64) | np.uint64(1)
+    mid = rng.integers(1 << 48, 1 << 49, size=1 << 19, dtype=np.uint64) | np.uint64(1)
+    below = np.arange((1 << 50) - 200_001, 1 << 50, 2, dtype=np.uint64)
+    ps = [33554393, 33554383, 33554371, 33554347, 33554341, 33554317]  # primes below 2^25
+    semi = np.array([p * q for p in ps for q in ps], dtype=np.uint64)
+    N = np.concatenate([top, mid, below, semi])
+    exp = oracle.isprime(N)
+    for small_max in (0, 1 << 17):
+        isp.set_option("small_max", small_max)
+        assert_same(gpu(N), exp, N)
+        assert_same(gpu(N[: 1 << 16]), exp[: 1 << 16], N[: 1 << 16])
 
 
 def test_all_below_2_20_every_path():
