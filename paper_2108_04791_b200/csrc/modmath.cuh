@@ -507,20 +507,22 @@ __device__ __forceinline__ uint64_t mont64_r2(const Mont64& M) {
     return x;
 }
 
-// ------------------------------------------------------- FP64, n < 2^50 ----
+// ------------------------------------------------------- FP64, n < 2^51 ----
 // The paper's medium class (2^18 .. 2^49) is the range where
 // double precision is exact -- and on B200 the FP64 pipe issues 64 DFMA
 // lanes/clk/SM (profiles/r1_imad_peak.json: 63.1) against 25 for the
-// IMAD.WIDE.U32 that 64-bit Montgomery needs.  For odd n < 2^50 and a, b < n:
-//   h = fl(ab), l = fma(a, b, -h) = ab - h exactly (|l| <= 2^46),
-//   q = nearest integer to fl(h * fl(1/n)): |q - ab/n| < 1/2 + 1/8 + 1/8,
+// IMAD.WIDE.U32 that 64-bit Montgomery needs.  For odd n < 2^51 and a, b < n:
+//   h = fl(ab), l = fma(a, b, -h) = ab - h exactly (|l| <= 2^48),
+//   q = nearest integer to fl(h * fl(1/n)): |q - ab/n| < 1/2 + 1/4 + 1/4,
 //   r = fma(-q, n, h) + l = ab - qn exactly, in (-n, n),
 // and one conditional +n gives ab mod n.  Rounding to an integer uses the
 // 1.5 * 2^52 addend (valid for |x| < 2^51).  (The paper's class boundary is
-// 2^49; the arithmetic's is 2^50, so the 50-bit values join the FP64 class.)
+// 2^49; the arithmetic's is 2^51, so the 50- and 51-bit values join the FP64
+// class.)
 constexpr double FP_RND = 6755399441055744.0;  // 1.5 * 2^52
-// The FP64 class: odd n < 2^FP_BITS (fmul_lazy's bound below holds to 2^50).
-constexpr int FP_BITS = 50;
+// The FP64 class: odd n < 2^FP_BITS (fmul_lazy's bound below holds to 2^51
+// for products of factors below n, to 2^50 with one factor doubled).
+constexpr int FP_BITS = 51;
 constexpr unsigned long long FP_LIMIT = 1ull << FP_BITS;
 
 struct ModF {
@@ -544,7 +546,9 @@ __device__ __forceinline__ double fmulmod(double a, double b, const ModF& M) {
 }
 
 // Lazy signed product for the witness loops: a, b exact integers with |a| <
-// 2n, |b| < n, n < 2^50.  Returns the signed representative r == a*b (mod n)
+// 2n, |b| < n, n < 2^50 -- or |a|, |b| < n, n < 2^51 (the same three bounds
+// below: |h / n| < n < 2^51, |l| <= 2^48, so |l| / n and (h/n) 2^-53 stay
+// below 1/4).  Returns the signed representative r == a*b (mod n)
 // with |r| < n -- no final correction, because the next square does not care
 // about the sign and every later product accepts |.| < n.
 //   h + l = a b exactly (|ab| < 2 n^2 < 2^101, so |l| <= ulp(h)/2 <= 2^47);
@@ -567,6 +571,16 @@ __device__ __forceinline__ double fmul_lazy(double a, double b, const ModF& M) {
 // power-of-two scaling of one factor).  |x| < n, b in {0, 1}.
 __device__ __forceinline__ double fsqr_dbl_lazy(double x, bool b, const ModF& M) {
     return fmul_lazy(x * (b ? 2.0 : 1.0), x, M);
+}
+
+// b ? 2y mod n : y for |y| < n < 2^51, lazily: z = 2^b y exactly (|z| < 2n),
+// k = round(z / n) in {-2 .. 2} (the 1.5 * 2^52 addend, |z / n| < 2), r = z - k n
+// exact with |r| <= n/2 + 1.  The base-2 ladder's doubling where folding it
+// into the product would break fmul_lazy's bound (2^50 <= n < 2^51).
+__device__ __forceinline__ double fdbl_if_lazy(double y, bool b, const ModF& M) {
+    const double z = y * (b ? 2.0 : 1.0);
+    const double k = fma(z, M.ninv, FP_RND) - FP_RND;
+    return fma(-k, M.n, z);
 }
 
 // Signed representative -> congruence tests (|x| < n).

@@ -274,10 +274,21 @@ __device__ __forceinline__ bool sprp2_f64(unsigned long long n) {
     double x = 2.0;  // top bit of d
     if (top > 0) {
         unsigned long long dd = d << (64 - top);  // remaining bits, MSB first
+        if (!__any_sync(__activemask(), (unsigned)(n >> 50))) {
+            // n < 2^50: the doubling folded into the product (|2x| < 2n is allowed)
 #pragma unroll 2
-        for (int k = 0; k < top; k++) {
-            x = fsqr_dbl_lazy(x, (long long)dd < 0, M);
-            dd += dd;
+            for (int k = 0; k < top; k++) {
+                x = fsqr_dbl_lazy(x, (long long)dd < 0, M);
+                dd += dd;
+            }
+        } else {
+            // 2^50 <= n < 2^51: square (|x| < n), then double and reduce once
+            // (|2y| < 2n, k = round(2y / n) in {-2 .. 2})
+#pragma unroll 2
+            for (int k = 0; k < top; k++) {
+                x = fdbl_if_lazy(fmul_lazy(x, x, M), (long long)dd < 0, M);
+                dd += dd;
+            }
         }
     }
     if (f_is_one(x, M) || f_is_mone(x, M)) return true;

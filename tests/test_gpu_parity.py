@@ -90,7 +90,7 @@ def test_chernick_and_pseudoprimes():
 
 
 def test_boundary_primes_and_neighbours():
-    centres = [2**18, 2**20, 2**31, 2**32, 2**33, 2**49, 2**50, 2**52, 2**53, 2**61, 2**62, 2**63, 2**64 - 1]
+    centres = [2**18, 2**20, 2**31, 2**32, 2**33, 2**49, 2**50, 2**51, 2**52, 2**53, 2**61, 2**62, 2**63, 2**64 - 1]
     vals = []
     for c in centres:
         lo = max(0, c - 3000)
@@ -105,23 +105,25 @@ def test_boundary_primes_and_neighbours():
 
 @pytest.mark.parametrize("witness", [0, 1, 2])
 def test_fp64_class_top_bit_exact(witness):
-    """The FP64 class reaches 2^50 (modmath.cuh fmul_lazy: |q - ab/n| < 1, so
-    |r| < n, at the top of the range): 2^20 random odd values with bit length
-    50 and 49, the odd values just below 2^50, products of two primes near
-    2^25, through the pipeline (every witness mode) and the short-array path."""
+    """The FP64 class reaches 2^51 (modmath.cuh fmul_lazy: |q - ab/n| < 1, so
+    |r| < n, at the top of the range; the base-2 ladder doubles separately at
+    bit length 51): random odd values of bit length 49, 50 and 51, the odd
+    values just below 2^50 and 2^51, products of two primes near 2^25 and
+    2^25.5, through the pipeline (every witness mode) and the short-array path."""
     isp.set_option("witness", witness)
     rng = np.random.default_rng(50 + witness)
-    top = rng.integers(1 << 49, 1 << 50, size=1 << 19, dtype=np.uint64) | np.uint64(1)
-    mid = rng.integers(1 << 48, 1 << 49, size=1 << 19, dtype=np.uint64) | np.uint64(1)
-    below = np.arange((1 << 50) - 200_001, 1 << 50, 2, dtype=np.uint64)
+    vals = [rng.integers(1 << (b - 1), 1 << b, size=1 << 18, dtype=np.uint64) | np.uint64(1) for b in (49, 50, 51)]
+    below = [np.arange((1 << b) - 100_001, 1 << b, 2, dtype=np.uint64) for b in (50, 51)]
     ps = [33554393, 33554383, 33554371, 33554347, 33554341, 33554317]  # primes below 2^25
-    semi = np.array([p * q for p in ps for q in ps], dtype=np.uint64)
-    N = np.concatenate([top, mid, below, semi])
+    qs = [47453111, 47453099, 47453053, 47453039]  # primes below 2^25.5
+    semi = np.array([p * q for p in ps + qs for q in ps + qs], dtype=np.uint64)
+    N = np.concatenate(vals + below + [semi])
     exp = oracle.isprime(N)
     for small_max in (0, 1 << 17):
         isp.set_option("small_max", small_max)
         assert_same(gpu(N), exp, N)
         assert_same(gpu(N[: 1 << 16]), exp[: 1 << 16], N[: 1 << 16])
+        assert_same(gpu(N[-(1 << 12):]), exp[-(1 << 12):], N[-(1 << 12):])
 
 
 def test_all_below_2_20_every_path():
