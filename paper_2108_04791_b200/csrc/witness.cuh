@@ -170,14 +170,17 @@ __device__ __forceinline__ bool sprp_lockstep64(const Mont64& M, uint64_t R2, ui
     const int nw = (nbits + WIN - 1) / WIN;
     uint64_t tab[NB][T], x[NB];
     bool done[NB], pass[NB];
+    const uint64_t nn = 0ull - M.ninv;
 #pragma unroll
     for (int i = 0; i < NB; i++) {
         uint64_t a = bases[i];
         if (a >= n) a %= n;
         done[i] = pass[i] = (a == 0);
-        tab[i][0] = mmul64(a, R2, M);
+        // table entries: lazy (< 2n) in the LZ range, canonical otherwise
+        tab[i][0] = LZ ? mmul64_lz_ptx(a, R2, n, nn) : mmul64_ptx(a, R2, n, M.ninv);
 #pragma unroll
-        for (int k = 1; k < T; k++) tab[i][k] = mmul64(tab[i][k - 1], tab[i][0], M);
+        for (int k = 1; k < T; k++)
+            tab[i][k] = LZ ? mmul64_lz_ptx(tab[i][k - 1], tab[i][0], n, nn) : mmul64_ptx(tab[i][k - 1], tab[i][0], n, M.ninv);
         if (SM) {
             st[(i * (T + 1)) * TS] = M.one;
 #pragma unroll
@@ -195,7 +198,6 @@ __device__ __forceinline__ bool sprp_lockstep64(const Mont64& M, uint64_t R2, ui
 #pragma unroll
         for (int i = 0; i < NB; i++) mt[i] = SM ? st[(i * (T + 1) + digit) * TS] : sel_table<T>(tab[i], digit, M.one);
         if (LZ) {
-            const uint64_t nn = 0ull - M.ninv;
 #pragma unroll
             for (int j = 0; j < WIN; j++) {
 #pragma unroll
@@ -223,7 +225,7 @@ __device__ __forceinline__ bool sprp_lockstep64(const Mont64& M, uint64_t R2, ui
 #pragma unroll
         for (int i = 0; i < NB; i++) {
             if (!done[i]) {
-                x[i] = msqr64(x[i], M);
+                x[i] = LZ ? mcanon64(msqr64_lz_ptx(x[i], n, nn), n) : msqr64_ptx(x[i], n, M.ninv);
                 if (x[i] == M.mone) done[i] = pass[i] = true;
                 else if (x[i] == M.one) done[i] = true;
             }
