@@ -93,7 +93,7 @@ void isprime_shutdown(void);
  *                    reuse the bitmap an earlier call on this device produced
  * "mr2_group"        3 or 6: 64-bit phase-2 bases run in lockstep groups of this size
  * "witness"          0 (default): the Eq 4 bases after base 2 for every
- *                    class; 1: Baillie-PSW for n >= 2^49 -- a strong Lucas test
+ *                    class; 1: Baillie-PSW for n >= 2^51 -- a strong Lucas test
  *                    (Selfridge parameters) after the base-2 strong test, the
  *                    paper's proposed next step; exact below
  *                    2^64 like Eq 4, so it never changes a bit of out;
@@ -131,7 +131,7 @@ typedef struct {
                                         "kernel_timing" is 1: mr1 32-bit, mr1 64-bit,
                                         mr2 32-bit, mr2 64-bit (square-and-multiply count);
                                         the 64-bit entries count the Montgomery class only */
-    uint64_t mulmods_fp64[2];        /* same for the FP64 class (odd n < 2^49): mr1, mr2 */
+    uint64_t mulmods_fp64[2];        /* same for the FP64 class (odd 2^32 <= n < 2^51): mr1, mr2 */
 } isprime_stats;
 
 /* Synchronises the current device, copies the accumulated statistics. */
