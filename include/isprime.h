@@ -111,6 +111,14 @@ void isprime_shutdown(void);
  * "warp_max"         within the short-array path, n <= warp_max (default 4096)
  *                    runs one warp per element with one Eq 4 base per lane
  *                    (latency of one exponentiation instead of seven)
+ * "sieve_fs_per_int", "sieve_fixed_ns", "mr32_fs_per_bit", "mr_fixed_ns"
+ *                    the plan's cost model (femtoseconds per integer of sieve
+ *                    window, nanoseconds per sieve pass, femtoseconds per odd
+ *                    element-bit of trial division + Miller-Rabin, nanoseconds of
+ *                    witness-kernel latency floor); defaults fitted on a B200 by
+ *                    tools/costfit.py (the Fig BestFit analogue).
+ *                    Path choice only: never changes a bit of out
+ * "warp_p"           sieve: primes below this cross off warp-cooperatively
  * "kernel_timing"    1: bracket every launch with CUDA events on its stream and
  *                    accumulate per-kernel device time (isprime_get_kernel_times)
  * Returns ISP_OK or ISP_EINVAL. */

@@ -30,9 +30,11 @@ struct Options {
     int chunk_log2 = 30;     // device chunk: 2^30 elements need <= 64 GB of queues (of 180 GB); halved on ENOMEM
     int win64 = 3;           // phase-2 window bits (tables in shared memory; 3 measured best)
     int warp_p = 2048;
-    long long sieve_fs_per_int = 700;     // femtoseconds per integer of window (measured: C4 0.68 ps)
-    long long sieve_fixed_ns = 8000;
-    long long mr32_fs_per_bit = 900;      // femtoseconds per odd element per bit (trial division + MR, C2)
+    // plan cost model, fitted on a B200 by tools/costfit.py (profiles/r1_costfit.json)
+    long long sieve_fs_per_int = 331;     // femtoseconds per integer of window
+    long long sieve_fixed_ns = 4475;
+    long long mr32_fs_per_bit = 1594;     // femtoseconds per odd element per bit (trial division + MR)
+    long long mr_fixed_ns = 24486;        // witness kernels' latency floor
     unsigned long long sieve_max = 1ull << 32;
     int kernel_timing = 0;
     int sieve_cache = 0;
@@ -363,6 +365,7 @@ int device_impl(Ctx* c, const unsigned long long* dN, uint8_t* dout, size_t n, c
     P.sieve_ps_per_int = (float)g_opt.sieve_fs_per_int * 1e-3f;
     P.sieve_fixed_ps = (float)g_opt.sieve_fixed_ns * 1e3f;
     P.mr32_ps_per_bit = (float)g_opt.mr32_fs_per_bit * 1e-3f;
+    P.mr_fixed_ps = (float)g_opt.mr_fixed_ns * 1e3f;
     TDParams td;
     td.n32 = td_round(g_opt.td32);
     td.n64 = td_round(g_opt.td64);
@@ -631,6 +634,7 @@ int isprime_set_option(const char* key, long long v) {
     else if (!strcmp(key, "sieve_fs_per_int")) { if (v < 0) return ISP_EINVAL; g_opt.sieve_fs_per_int = v; }
     else if (!strcmp(key, "sieve_fixed_ns")) { if (v < 0) return ISP_EINVAL; g_opt.sieve_fixed_ns = v; }
     else if (!strcmp(key, "mr32_fs_per_bit")) { if (v < 0) return ISP_EINVAL; g_opt.mr32_fs_per_bit = v; }
+    else if (!strcmp(key, "mr_fixed_ns")) { if (v < 0) return ISP_EINVAL; g_opt.mr_fixed_ns = v; }
     else if (!strcmp(key, "kernel_timing")) { if (v < 0 || v > 1) return ISP_EINVAL; g_opt.kernel_timing = (int)v; }
     else if (!strcmp(key, "mr2_group")) { if (v != 3 && v != 6) return ISP_EINVAL; g_opt.mr2_group = (int)v; }
     else if (!strcmp(key, "sieve_cache")) { if (v < 0 || v > 1) return ISP_EINVAL; g_opt.sieve_cache = (int)v; }
@@ -655,6 +659,7 @@ long long isprime_get_option(const char* key) {
     if (!strcmp(key, "sieve_fs_per_int")) return g_opt.sieve_fs_per_int;
     if (!strcmp(key, "sieve_fixed_ns")) return g_opt.sieve_fixed_ns;
     if (!strcmp(key, "mr32_fs_per_bit")) return g_opt.mr32_fs_per_bit;
+    if (!strcmp(key, "mr_fixed_ns")) return g_opt.mr_fixed_ns;
     if (!strcmp(key, "kernel_timing")) return g_opt.kernel_timing;
     if (!strcmp(key, "sieve_cache")) return g_opt.sieve_cache;
     if (!strcmp(key, "mr2_group")) return g_opt.mr2_group;

@@ -66,6 +66,7 @@ struct PlanParams {
     float sieve_ps_per_int;    // sieve cost per integer of span
     float sieve_fixed_ps;      // fixed cost of one sieve pass
     float mr32_ps_per_bit;     // MR cost per odd element per bit (n < 2^32)
+    float mr_fixed_ps;         // latency floor of the witness kernels when any element needs them
     int invalidate;            // 1: forget the bitmap held from an earlier call (first chunk of a call)
 };
 
@@ -426,17 +427,24 @@ __global__ void __launch_bounds__(PLAN_THREADS) plan_kernel(const unsigned long 
             if (lane >= o) covered += y;
         }
         const double mr_all = __shfl_sync(0xffffffffu, covered, 31);
+        // the witness kernels' latency floor is paid unless the window leaves
+        // them nothing (no sampled value >= 2^32 and every small one covered)
+        const bool big = mx >= (1ull << 32);
+        const double fixed_all = (double)P.mr_fixed_ps;
         // candidate of this lane: [0, 2^b)
         double cost = 1e300;
         unsigned long long clo = 0, chi = 1ull << b;
-        if (chi <= wmax) cost = P.sieve_fixed_ps + (double)chi * P.sieve_ps_per_int + (mr_all - covered);
+        if (chi <= wmax)
+            cost = P.sieve_fixed_ps + (double)chi * P.sieve_ps_per_int + (mr_all - covered) +
+                   ((big || mr_all - covered > 0.0) ? fixed_all : 0.0);
         int cand = 2 + lane;  // 0 none, 1 held bitmap, 2.. [0,2^b), 40 [min,max]
         // lane 0 also weighs "none" and the held bitmap; lane 1 the [min, max] window
         if (lane == 0) {
-            if (mr_all <= cost) { cost = mr_all; cand = 0; clo = 0; chi = 0; }
+            if (mr_all + fixed_all <= cost) { cost = mr_all + fixed_all; cand = 0; clo = 0; chi = 0; }
             if (vhi > vlo) {
                 const double miss = mr_all * (1.0 - (double)in_valid / (double)nsamp_small);
-                if (miss < cost) { cost = miss; cand = 1; clo = vlo; chi = vhi; }
+                const double c = miss + ((big || miss > 0.0) ? fixed_all : 0.0);
+                if (c < cost) { cost = c; cand = 1; clo = vlo; chi = vhi; }
             }
         } else if (lane == 1) {
             const unsigned long long margin = (unsigned long long)(((double)(mx - mn) / (double)nsamp_small) * 4.0) + 64;
@@ -446,7 +454,7 @@ __global__ void __launch_bounds__(PLAN_THREADS) plan_kernel(const unsigned long 
             lo &= ~63ull;
             hi = (hi + 63) & ~63ull;
             if (hi - lo <= wmax) {
-                const double c = P.sieve_fixed_ps + (double)(hi - lo) * P.sieve_ps_per_int;
+                const double c = P.sieve_fixed_ps + (double)(hi - lo) * P.sieve_ps_per_int + (big ? fixed_all : 0.0);
                 if (c < cost) { cost = c; cand = 40; clo = lo; chi = hi; }
             }
         }
