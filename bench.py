@@ -42,11 +42,13 @@ UNIT = "Gints/s"
 #     (a squaring needs 3 WIDE for a^2 -> 16; the multiply count below does not
 #      separate squarings, so 18 is a conservative, i.e. higher, work figure)
 #   32-bit Montgomery: 1 WIDE + 1 IMAD + 1 HI -> 5 FMA-heavy slots
-#   FP64 (n < 2^49), lazy signed residues: DMUL (h), DFMA (l), DFMA + DADD (q), DFMA + DADD (r)
+#   FP64 (n < 2^51), lazy signed residues: DMUL (h), DFMA (l), DFMA + DADD (q), DFMA + DADD (r)
 #     -> 6 FP64 lane-ops (modmath.cuh fmul_lazy)
+# The 32-bit class runs on the FP64 pipe too (csrc/kernels.cuh CLS32_FP64 = 1).
 SLOTS_MULMOD64 = 18
 SLOTS_MULMOD32 = 5
 FP64_OPS_MULMOD = 6
+CLS32_ON_FP64 = True
 LANES_PER_CLK_SM = 64  # FMA-heavy and FP64 pipes: 16 lanes/clk per SMSP x 4 (B300_MICROARCH.md; measured 63.2 / 63.1)
 HBM_BYTES_PER_ELEM = 9      # 8-B value read + 1-B result written
 
@@ -220,8 +222,8 @@ def roofline(kern_ms, stats, n, steps, peaks, peaks_kind, clocks, cfg=None):
     if name in ("mr1", "mr2"):
         mm, mf = stats["mulmods"], stats["mulmods_fp64"]
         k = 0 if name == "mr1" else 2
-        fma_slots = mm[k] * SLOTS_MULMOD32 + mm[k + 1] * SLOTS_MULMOD64
-        fp64_ops = mf[0 if name == "mr1" else 1] * FP64_OPS_MULMOD
+        fma_slots = (0 if CLS32_ON_FP64 else mm[k] * SLOTS_MULMOD32) + mm[k + 1] * SLOTS_MULMOD64
+        fp64_ops = (mf[0 if name == "mr1" else 1] + (mm[k] if CLS32_ON_FP64 else 0)) * FP64_OPS_MULMOD
         busiest = max(fma_slots, fp64_ops)
         achieved = busiest / steps / (ms * 1e-3) / 1e12
         mhz = peaks.get("sm_max_mhz", 1965.0)
@@ -231,8 +233,8 @@ def roofline(kern_ms, stats, n, steps, peaks, peaks_kind, clocks, cfg=None):
                 "traffic": traffic, "ncu": ncu,
                 "peak_source": f"derived: 148 SMs x {LANES_PER_CLK_SM} lanes/clk x {mhz:.0f} MHz "
                                "(B300_MICROARCH.md pipe rates; MEASURED_PEAKS sm_max_mhz)",
-                "work": f"per step: {fma_slots / steps:.4g} FMA-heavy slots ({SLOTS_MULMOD32}/32-bit, {SLOTS_MULMOD64}/64-bit "
-                        f"Montgomery mulmod) and {fp64_ops / steps:.4g} FP64 ops ({FP64_OPS_MULMOD}/mulmod); "
+                "work": f"per step: {fma_slots / steps:.4g} FMA-heavy slots ({SLOTS_MULMOD64}/64-bit Montgomery mulmod) "
+                        f"and {fp64_ops / steps:.4g} FP64 ops ({FP64_OPS_MULMOD}/mulmod of the FP64 and 32-bit classes); "
                         "mulmods = square-and-multiply count of ModExp",
                 "ms_per_step": round(ms, 4)}
     nbytes = HBM_BYTES_PER_ELEM * n
