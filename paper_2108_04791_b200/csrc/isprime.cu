@@ -38,6 +38,7 @@ struct Options {
     unsigned long long sieve_max = 1ull << 32;
     int kernel_timing = 0;
     int sieve_cache = 0;
+    int pdl = 1;             // programmatic dependent launch of the pipeline kernels
     int mr2_group = 3;       // 64-bit phase-2 bases run G at a time in lockstep (3 or 6)
     long long small_max = 1 << 17;  // n <= small_max (and force_path auto): one fused launch
     long long warp_max = 4096;      // n <= warp_max: one warp per element (one base per lane)
@@ -155,6 +156,25 @@ int cuda_fail(cudaError_t e, const char* what) {
         cudaError_t e_ = cudaGetLastError();             \
         if (e_ != cudaSuccess) return cuda_fail(e_, what); \
     } while (0)
+
+// Launch a pipeline kernel with programmatic stream serialisation (option
+// "pdl", default 1): its launch overlaps the tail of the kernel before it on
+// the stream; the kernel waits (kernels.cuh pdl_wait) before touching memory.
+template <typename... KArgs, typename... Args>
+cudaError_t launch_k(void (*k)(KArgs...), unsigned grid, unsigned block, size_t smem, cudaStream_t s,
+                     Args... args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(block);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = g_opt.pdl ? 1 : 0;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, k, static_cast<KArgs>(args)...);
+}
 
 int occupancy(const void* fn, int threads, size_t smem) {
     int b = 0;
@@ -293,11 +313,11 @@ template <int A>
 void launch_classify_b(int n64, int g, cudaStream_t s, const unsigned long long* N, uint8_t* out, uint32_t len,
                        Ctx* c, const TDParams& td, int vin, int vout, uint32_t ss) {
     switch (n64) {
-        case 32: classify_kernel<A, 32><<<g, CLS_THREADS, 0, s>>>(N, out, len, c->plan, c->bitmap, c->q, td, vin, vout, ss); break;
-        case 24: classify_kernel<A, 24><<<g, CLS_THREADS, 0, s>>>(N, out, len, c->plan, c->bitmap, c->q, td, vin, vout, ss); break;
-        case 16: classify_kernel<A, 16><<<g, CLS_THREADS, 0, s>>>(N, out, len, c->plan, c->bitmap, c->q, td, vin, vout, ss); break;
-        case 8: classify_kernel<A, 8><<<g, CLS_THREADS, 0, s>>>(N, out, len, c->plan, c->bitmap, c->q, td, vin, vout, ss); break;
-        default: classify_kernel<A, 0><<<g, CLS_THREADS, 0, s>>>(N, out, len, c->plan, c->bitmap, c->q, td, vin, vout, ss); break;
+        case 32: launch_k(classify_kernel<A, 32>, g, CLS_THREADS, 0, s, N, out, len, c->plan, c->bitmap, c->q, td, vin, vout, ss); break;
+        case 24: launch_k(classify_kernel<A, 24>, g, CLS_THREADS, 0, s, N, out, len, c->plan, c->bitmap, c->q, td, vin, vout, ss); break;
+        case 16: launch_k(classify_kernel<A, 16>, g, CLS_THREADS, 0, s, N, out, len, c->plan, c->bitmap, c->q, td, vin, vout, ss); break;
+        case 8: launch_k(classify_kernel<A, 8>, g, CLS_THREADS, 0, s, N, out, len, c->plan, c->bitmap, c->q, td, vin, vout, ss); break;
+        default: launch_k(classify_kernel<A, 0>, g, CLS_THREADS, 0, s, N, out, len, c->plan, c->bitmap, c->q, td, vin, vout, ss); break;
     }
 }
 
@@ -314,8 +334,8 @@ void launch_classify(int n32, int n64, int g, cudaStream_t s, const unsigned lon
 
 template <int WIN, int G>
 void launch_mr2_w(Ctx* c, cudaStream_t s, uint8_t* out, int grid, bool full, int cw) {
-    if (full) mr2_kernel<WIN, true, G><<<grid, MR_THREADS, 0, s>>>(c->plan, c->q, out, cw);
-    else mr2_kernel<WIN, false, G><<<grid, MR_THREADS, 0, s>>>(c->plan, c->q, out, cw);
+    if (full) launch_k(mr2_kernel<WIN, true, G>, grid, MR_THREADS, 0, s, c->plan, c->q, out, cw);
+    else launch_k(mr2_kernel<WIN, false, G>, grid, MR_THREADS, 0, s, c->plan, c->q, out, cw);
 }
 
 int launch_mr2(Ctx* c, cudaStream_t s, uint8_t* out, int grid) {
@@ -323,14 +343,14 @@ int launch_mr2(Ctx* c, cudaStream_t s, uint8_t* out, int grid) {
     const int cw = g_opt.kernel_timing;
     const int g = g_opt.mr2_group == 6 ? 6 : 3;
     if (g_opt.witness == 1) {  // Baillie-PSW for the 64-bit Montgomery class
-        if (full) mr2_kernel<3, true, 3, 1><<<grid, MR_THREADS, 0, s>>>(c->plan, c->q, out, cw);
-        else mr2_kernel<3, false, 3, 1><<<grid, MR_THREADS, 0, s>>>(c->plan, c->q, out, cw);
+        if (full) launch_k(mr2_kernel<3, true, 3, 1>, grid, MR_THREADS, 0, s, c->plan, c->q, out, cw);
+        else launch_k(mr2_kernel<3, false, 3, 1>, grid, MR_THREADS, 0, s, c->plan, c->q, out, cw);
         CKL("mr2_kernel");
         return ISP_OK;
     }
     if (g_opt.witness == 2) {  // reduced witness sets by magnitude
-        if (full) mr2_kernel<3, true, 3, 2><<<grid, MR_THREADS, 0, s>>>(c->plan, c->q, out, cw);
-        else mr2_kernel<3, false, 3, 2><<<grid, MR_THREADS, 0, s>>>(c->plan, c->q, out, cw);
+        if (full) launch_k(mr2_kernel<3, true, 3, 2>, grid, MR_THREADS, 0, s, c->plan, c->q, out, cw);
+        else launch_k(mr2_kernel<3, false, 3, 2>, grid, MR_THREADS, 0, s, c->plan, c->q, out, cw);
         CKL("mr2_kernel");
         return ISP_OK;
     }
@@ -402,7 +422,7 @@ int device_impl(Ctx* c, const unsigned long long* dN, uint8_t* dout, size_t n, c
         P.invalidate = (base == 0 && !g_opt.sieve_cache) ? 1 : 0;
         {
             KScope ks(K_PLAN, s);
-            plan_kernel<<<1, PLAN_THREADS, 0, s>>>(N, len, c->plan, P);
+            launch_k(plan_kernel, 1, PLAN_THREADS, 0, s, N, (unsigned long long)len, c->plan, P);
             CKL("plan_kernel");
         }
         {
@@ -410,8 +430,8 @@ int device_impl(Ctx* c, const unsigned long long* dN, uint8_t* dout, size_t n, c
             // first base prime >= warp_p (the warp-cooperative / per-thread split)
             int first_large = FIRST_CROSS_PRIME_IDX;
             while (first_large < c->nbp && c->hbp[first_large].x < (uint32_t)g_opt.warp_p) first_large++;
-            sieve_kernel<<<c->grid_sieve, SIEVE_THREADS, SEG_ODD, s>>>(c->plan, c->bitmap, c->bp, c->nbp, c->patt,
-                                                                         first_large);
+            launch_k(sieve_kernel, c->grid_sieve, SIEVE_THREADS, SEG_ODD, s, c->plan, c->bitmap, c->bp, c->nbp, c->patt,
+                     first_large);
             CKL("sieve_kernel");
         }
         {
@@ -420,8 +440,8 @@ int device_impl(Ctx* c, const unsigned long long* dN, uint8_t* dout, size_t n, c
             while (first_large < c->nbp && c->hbp[first_large].x < (uint32_t)g_opt.warp_p) first_large++;
             // 16-byte loads of element pairs need N 16-B aligned and out 2-B aligned
             const int vec = ((((uintptr_t)N & 15) == 0) && (((uintptr_t)out & 1) == 0)) ? 1 : 0;
-            dense_kernel<<<c->sms, DENSE_THREADS, 2 * SEG_ODD, s>>>(c->plan, N, out, len, c->bp, c->nbp, c->patt,
-                                                                      first_large, vec);
+            launch_k(dense_kernel, c->sms, DENSE_THREADS, 2 * SEG_ODD, s, c->plan, N, out, len, c->bp, c->nbp, c->patt,
+                     first_large, vec);
             CKL("dense_kernel");
         }
         const uint32_t ntiles = (len + CLS_TILE - 1) / CLS_TILE;
@@ -439,12 +459,12 @@ int device_impl(Ctx* c, const unsigned long long* dN, uint8_t* dout, size_t n, c
         {
             KScope ks(K_SORT, s);
             const int gs = c->grid_sort < gcls ? c->grid_sort : gcls;
-            qscatter_kernel<<<gs, SORT_THREADS, 0, s>>>(c->plan, c->q, gcls, seg_stride);
+            launch_k(qscatter_kernel, gs, SORT_THREADS, 0, s, c->plan, c->q, gcls, seg_stride);
             CKL("qscatter_kernel");
         }
         {
             KScope ks(K_MR1, s);
-            mr1_kernel<<<mr_grid(c->grid_mr1, len), MR_THREADS, 0, s>>>(c->plan, c->q, g_opt.kernel_timing);
+            launch_k(mr1_kernel, mr_grid(c->grid_mr1, len), MR_THREADS, 0, s, c->plan, c->q, g_opt.kernel_timing);
             CKL("mr1_kernel");
         }
         {
@@ -637,6 +657,7 @@ int isprime_set_option(const char* key, long long v) {
     else if (!strcmp(key, "mr_fixed_ns")) { if (v < 0) return ISP_EINVAL; g_opt.mr_fixed_ns = v; }
     else if (!strcmp(key, "kernel_timing")) { if (v < 0 || v > 1) return ISP_EINVAL; g_opt.kernel_timing = (int)v; }
     else if (!strcmp(key, "mr2_group")) { if (v != 3 && v != 6) return ISP_EINVAL; g_opt.mr2_group = (int)v; }
+    else if (!strcmp(key, "pdl")) { if (v < 0 || v > 1) return ISP_EINVAL; g_opt.pdl = (int)v; }
     else if (!strcmp(key, "sieve_cache")) { if (v < 0 || v > 1) return ISP_EINVAL; g_opt.sieve_cache = (int)v; }
     else if (!strcmp(key, "small_max")) { if (v < 0) return ISP_EINVAL; g_opt.small_max = v; }
     else if (!strcmp(key, "warp_max")) { if (v < 0 || v > (1 << 26)) return ISP_EINVAL; g_opt.warp_max = v; }
@@ -663,6 +684,7 @@ long long isprime_get_option(const char* key) {
     if (!strcmp(key, "kernel_timing")) return g_opt.kernel_timing;
     if (!strcmp(key, "sieve_cache")) return g_opt.sieve_cache;
     if (!strcmp(key, "mr2_group")) return g_opt.mr2_group;
+    if (!strcmp(key, "pdl")) return g_opt.pdl;
     if (!strcmp(key, "small_max")) return g_opt.small_max;
     if (!strcmp(key, "warp_max")) return g_opt.warp_max;
     if (!strcmp(key, "witness")) return g_opt.witness;

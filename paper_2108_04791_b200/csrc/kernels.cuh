@@ -33,6 +33,13 @@ constexpr int CLS_TILE = CLS_THREADS * 2 * CLS_PAIRS; // 2048 elements per tile
 constexpr int MR_THREADS = 256;
 constexpr int MAX_SEG = 4096;                         // classify blocks (queue segments) per launch
 
+// Programmatic dependent launch: the pipeline kernels are launched with the
+// programmatic-serialisation attribute (isprime.cu launch_k), so a kernel's
+// launch overlaps the tail of the one before it; each waits here, before its
+// first global access, until the previous grid has completed and its writes
+// are visible.  A no-op when the kernel was launched without the attribute.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
 // Device-resident plan and counters (one per device context).
 struct DevPlan {
     unsigned long long wlo, whi;            // window for the current chunk
@@ -330,6 +337,7 @@ constexpr int PLAN_SAMPLES = 4096;
 
 __global__ void __launch_bounds__(PLAN_THREADS) plan_kernel(const unsigned long long* __restrict__ N,
                                                             unsigned long long len, DevPlan* plan, PlanParams P) {
+    pdl_wait();
     __shared__ unsigned int hist[33];
     __shared__ unsigned long long wmin[PLAN_THREADS / 32], wmaxv[PLAN_THREADS / 32];
     __shared__ unsigned int in_valid, nsamp_small, s_notdense;
@@ -614,6 +622,7 @@ __global__ void __launch_bounds__(SIEVE_THREADS, 2)
 sieve_kernel(const DevPlan* __restrict__ plan, uint32_t* __restrict__ bitmap,
              const uint2* __restrict__ bp, int nbp, const uint8_t* __restrict__ patt,
              int first_large) {
+    pdl_wait();
     extern __shared__ __align__(16) uint8_t seg[];
     if (!plan->sieve_needed) return;
     const unsigned long long wlo = plan->wlo, whi = plan->whi;
@@ -669,6 +678,7 @@ __global__ void __launch_bounds__(DENSE_THREADS, 1)
 dense_kernel(DevPlan* __restrict__ plan, const unsigned long long* __restrict__ N, uint8_t* __restrict__ out,
              uint32_t len, const uint2* __restrict__ bp, int nbp, const uint8_t* __restrict__ patt, int first_large,
              int vec) {
+    pdl_wait();
     extern __shared__ __align__(16) uint8_t dseg[];  // two SEG_ODD buffers
     if (!plan->dense) return;
     const unsigned long long wlo = plan->wlo, whi = plan->whi, n0 = plan->dense_base;
@@ -781,6 +791,7 @@ __global__ void __launch_bounds__(CLS_THREADS)
 classify_kernel(const unsigned long long* __restrict__ N, uint8_t* __restrict__ out, uint32_t len,
                 DevPlan* __restrict__ plan, const uint32_t* __restrict__ bitmap, Queues q, TDParams td,
                 int vec_in, int vec_out, uint32_t seg_stride) {
+    pdl_wait();
     __shared__ ClsSmem sm;
     const uint32_t segbase = blockIdx.x * seg_stride;
     // dense_kernel already classified a dense range; if it found a mismatch,
@@ -1174,6 +1185,7 @@ __device__ __forceinline__ bool sort_pays(const unsigned int* bins, int nb) {
 
 __global__ void __launch_bounds__(SORT_THREADS) qscatter_kernel(DevPlan* __restrict__ plan, Queues q, int nseg,
                                                                 uint32_t seg_stride) {
+    pdl_wait();
     __shared__ unsigned int spre[65], scnt[65], sbase[65], swarp[SORT_THREADS / 32];
     __shared__ unsigned int spfx[MAX_SEG];
     __shared__ unsigned int do32, do64;
@@ -1329,6 +1341,7 @@ __device__ __forceinline__ unsigned int fp_class_count(const DevPlan* plan) {
 
 __global__ void __launch_bounds__(MR_THREADS)
 mr1_kernel(DevPlan* __restrict__ plan, Queues q, int count_work) {
+    pdl_wait();
     __shared__ WarpStage<uint32_t> st32[MR_THREADS / 32];
     __shared__ WarpStage<unsigned long long> st64i[MR_THREADS / 32], st64f[MR_THREADS / 32];
     __shared__ unsigned int s_nf;
@@ -1403,6 +1416,7 @@ mr1_kernel(DevPlan* __restrict__ plan, Queues q, int count_work) {
 template <int WIN, bool FULL32, int G64, int WIT = 0>
 __global__ void __launch_bounds__(MR_THREADS)
 mr2_kernel(DevPlan* __restrict__ plan, Queues q, uint8_t* __restrict__ out, int count_work) {
+    pdl_wait();
     // window tables of the lockstep bases in shared memory (transposed per thread)
     constexpr bool SM = G64 * (1 << WIN) <= 24;  // <= 48 KB of static shared memory
     __shared__ unsigned long long s_tab[SM ? G64 * (1 << WIN) * MR_THREADS : 1];
