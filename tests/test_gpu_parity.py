@@ -358,6 +358,30 @@ def test_c4_full_dense_range_pi_2_32():
     torch.cuda.empty_cache()
 
 
+def test_more_than_2_32_elements():
+    """n > 2^32 elements (include/isprime.h: "n may exceed 2^32"): N[i] = i mod
+    2^32 for i < 2^32 + 2^20, so the count is pi(2^32) + pi(2^20) = 203,280,221
+    + 82,025, and the elements past 2^32 equal the oracle."""
+    n = (1 << 32) + (1 << 20)
+    # filled 2^30 elements at a time: one torch kernel over more than 2^32
+    # elements wrote zeros past 2^32 here (torch 2.11 arange / bitwise_and)
+    dN = torch.empty(n, dtype=torch.int64, device=DEV)
+    for s0 in range(0, n, 1 << 30):
+        m = min(1 << 30, n - s0)
+        torch.arange(s0, s0 + m, dtype=torch.int64, device=DEV, out=dN[s0:s0 + m])
+        dN[s0:s0 + m].bitwise_and_(0xFFFFFFFF)
+    assert dN[1 << 32: (1 << 32) + 3].tolist() == [0, 1, 2]
+    dout = torch.empty(n, dtype=torch.uint8, device=DEV)
+    dcount = torch.zeros(1, dtype=torch.int64, device=DEV)
+    isp.isprime_count_device(dN, dout, dcount)
+    torch.cuda.synchronize()
+    assert int(dcount.item()) == 203280221 + 82025
+    tail = dout[1 << 32:].cpu().numpy()
+    assert_same(tail, oracle.sieve(1 << 20), np.arange(1 << 20, dtype=np.uint64))
+    del dN, dout
+    torch.cuda.empty_cache()
+
+
 def test_force_path_equivalence_all_32bit():
     """SPEC.md:392 analogue over the ENTIRE 32-bit domain: sieve path vs
     trial-division + Miller-Rabin path ({2,7,61}) vs Miller-Rabin with the full
