@@ -228,8 +228,11 @@ def roofline(kern_ms, stats, n, steps, peaks, peaks_kind, clocks, cfg=None):
         achieved = busiest / steps / (ms * 1e-3) / 1e12
         mhz = peaks.get("sm_max_mhz", 1965.0)
         peak = 148 * LANES_PER_CLK_SM * mhz * 1e6 / 1e12
+        per_pipe = {"fmaheavy": round(fma_slots / steps / (ms * 1e-3) / 1e12 / peak, 4),
+                    "fp64": round(fp64_ops / steps / (ms * 1e-3) / 1e12 / peak, 4)}
         return {"kernel": name, "bound": "alu", "achieved": round(achieved, 4), "peak": round(peak, 3),
                 "unit": "T lane-slots/s (busiest of FMA-heavy / FP64 pipe)", "frac": round(achieved / peak, 4),
+                "frac_per_pipe": per_pipe,
                 "traffic": traffic, "ncu": ncu,
                 "peak_source": f"derived: 148 SMs x {LANES_PER_CLK_SM} lanes/clk x {mhz:.0f} MHz "
                                "(B300_MICROARCH.md pipe rates; MEASURED_PEAKS sm_max_mhz)",
