@@ -332,8 +332,11 @@ __global__ void init_presieve_kernel(uint8_t* patt) {
 // the element count and the maximum); its constants are B200 costs, not the
 // MATLAB fits.  The plan changes only the time, never the result: any element
 // outside the window takes the trial-division / Miller-Rabin route.
-constexpr int PLAN_THREADS = 256;
+constexpr int PLAN_THREADS = 1024;
 constexpr int PLAN_SAMPLES = 4096;
+#ifndef PLAN_RUN
+#define PLAN_RUN 4                                    // consecutive elements per sampled stratum
+#endif
 
 __global__ void __launch_bounds__(PLAN_THREADS) plan_kernel(const unsigned long long* __restrict__ N,
                                                             unsigned long long len, DevPlan* plan, PlanParams P) {
@@ -344,6 +347,11 @@ __global__ void __launch_bounds__(PLAN_THREADS) plan_kernel(const unsigned long 
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
     if (tid < 33) hist[tid] = 0;
     if (tid == 0) { in_valid = 0; nsamp_small = 0; s_notdense = 0; }
+    // per-chunk resets of the sort bins and work cursors (read only by the
+    // kernels after this one), spread over the block
+    if (tid < 33) { plan->bins32[tid] = 0; plan->cur32[tid] = 0; }
+    if (tid >= 64 && tid < 64 + 65) { plan->bins64[tid - 64] = 0; plan->cur64[tid - 64] = 0; }
+    if (tid >= 160 && tid < 163) { plan->cur1[tid - 160] = 0; plan->cur2[tid - 160] = 0; }
     __syncthreads();
     const unsigned long long n0 = len ? N[0] : 0ull;  // a dense range is N[i] = n0 + i
     const unsigned long long vlo = P.invalidate ? 0ull : plan->valid_lo;
@@ -352,31 +360,38 @@ __global__ void __launch_bounds__(PLAN_THREADS) plan_kernel(const unsigned long 
     unsigned long long lmin = ~0ull, lmax = 0;
     unsigned int lin = 0, lcnt = 0;
     if (P.force == 0) {
-        // PLAN_SAMPLES / 8 strata, 8 consecutive elements from a pseudo-random
-        // offset in each: one cache line per stratum, and few enough distinct
-        // 2 MB pages that one SM's TLB walks stay cheap on multi-GB arrays.
-        constexpr int PER = PLAN_SAMPLES / PLAN_THREADS;   // 16 = 2 strata x 8
-        const unsigned long long NS = (S + 7) / 8;          // strata
+        // PLAN_SAMPLES / PLAN_RUN strata, PLAN_RUN consecutive elements from a
+        // pseudo-random offset in each (one 32-byte sector), one stratum per
+        // thread: the kernel is a single block on the critical path of every
+        // call, so it is made of many short warps (1024 threads, no 64-bit
+        // division) rather than a few long ones (256 threads: 13 us).
+        constexpr int PER = PLAN_SAMPLES / PLAN_THREADS;   // strata of PLAN_RUN consecutive elements per thread
+        const unsigned long long NS = (S + PLAN_RUN - 1) / PLAN_RUN;  // strata
         unsigned long long v[PER];
 #pragma unroll
-        for (int r = 0; r < PER / 8; r++) {
+        for (int r = 0; r < PER / PLAN_RUN; r++) {
             const unsigned long long k = (unsigned long long)tid + (unsigned long long)r * PLAN_THREADS;
             unsigned long long at = 0, avail = 0;
             if (k < NS) {
-                const unsigned long long lo = (k * len) / NS, hi = ((k + 1) * len) / NS;  // stratum [lo, hi)
+                // stratum [lo, hi): k len < 2^42 is exact in a double, and lo of
+                // stratum k + 1 is the same expression as hi of stratum k
+                const double f = (double)len / (double)NS;
+                const unsigned long long lo = (unsigned long long)((double)k * f);
+                unsigned long long hi = (unsigned long long)((double)(k + 1) * f);
+                if (k + 1 == NS || hi > len) hi = len;
                 unsigned int h = (unsigned int)k * 0x9E3779B1u;
                 h ^= h >> 15;
                 h *= 0x2C1B3C6Du;
                 h ^= h >> 12;
                 const unsigned long long span = hi - lo;
-                at = lo + (span > 8 ? h % (unsigned int)(span - 7) : 0u);
-                avail = span < 8 ? span : 8;
+                at = lo + (span > PLAN_RUN ? h % (unsigned int)(span - PLAN_RUN + 1) : 0u);
+                avail = span < PLAN_RUN ? span : PLAN_RUN;
             }
             bool bad = false;
 #pragma unroll
-            for (int e = 0; e < 8; e++) {
-                v[8 * r + e] = (unsigned long long)e < avail ? N[at + e] : 0ull;
-                bad |= (unsigned long long)e < avail && v[8 * r + e] != n0 + at + e;
+            for (int e = 0; e < PLAN_RUN; e++) {
+                v[PLAN_RUN * r + e] = (unsigned long long)e < avail ? N[at + e] : 0ull;
+                bad |= (unsigned long long)e < avail && v[PLAN_RUN * r + e] != n0 + at + e;
             }
             if (bad) s_notdense = 1;
         }
@@ -413,11 +428,15 @@ __global__ void __launch_bounds__(PLAN_THREADS) plan_kernel(const unsigned long 
     }
     __syncthreads();
     if (wid != 0) return;
-    unsigned long long mn = ~0ull, mx = 0;
+    static_assert(PLAN_THREADS / 32 <= 32, "one warp reduces the per-warp extrema");
+    unsigned long long mn = lane < PLAN_THREADS / 32 ? wmin[lane] : ~0ull;
+    unsigned long long mx = lane < PLAN_THREADS / 32 ? wmaxv[lane] : 0ull;
 #pragma unroll
-    for (int w = 0; w < PLAN_THREADS / 32; w++) {
-        mn = wmin[w] < mn ? wmin[w] : mn;
-        mx = wmaxv[w] > mx ? wmaxv[w] : mx;
+    for (int o = 16; o > 0; o >>= 1) {
+        const unsigned long long a = __shfl_xor_sync(0xffffffffu, mn, o);
+        const unsigned long long b2 = __shfl_xor_sync(0xffffffffu, mx, o);
+        mn = a < mn ? a : mn;
+        mx = b2 > mx ? b2 : mx;
     }
     const unsigned long long wmax = P.wmax;
     unsigned long long wlo = 0, whi = 0;
@@ -506,12 +525,9 @@ __global__ void __launch_bounds__(PLAN_THREADS) plan_kernel(const unsigned long 
     plan->whi = whi;
     plan->sieve_needed = need;
     for (int q = 0; q < 4; q++) { plan->total[q] += plan->counts[q]; plan->counts[q] = 0; }
-    for (int b = 0; b < 33; b++) { plan->bins32[b] = 0; plan->cur32[b] = 0; }
-    for (int b = 0; b < 65; b++) { plan->bins64[b] = 0; plan->cur64[b] = 0; }
     plan->sorted32 = plan->sorted64 = 0;
     plan->total[3] += plan->pback;  // FP64-class base-2 passes count with the 64-bit ones
     plan->pback = 0;
-    for (int r = 0; r < 3; r++) { plan->cur1[r] = 0; plan->cur2[r] = 0; }
     plan->chunks += 1;
 }
 
