@@ -412,6 +412,49 @@ def test_force_path_equivalence_all_32bit():
     assert total == 203280221
 
 
+# ------------------------------------------------------------------ streams and threads
+def test_calls_on_two_streams_and_threads():
+    """The library keeps one set of queues per device: a call on another
+    stream waits for the previous call's completion event (isprime.cu
+    last_done), so back-to-back calls on two streams with no host sync in
+    between, and host-API calls from two threads at once, all stay exact."""
+    import threading
+    A = np.concatenate([workloads.generate("C5", count=1 << 20), workloads.generate("C2", count=1 << 19)])
+    B = np.concatenate([workloads.generate("C3", count=1 << 20), workloads.generate("C1", count=50_000)])
+    expA, expB = oracle.isprime(A), oracle.isprime(B)
+    isp.set_option("small_max", 0)
+    s1, s2 = torch.cuda.Stream(), torch.cuda.Stream()
+    dA = torch.from_numpy(A.view(np.int64)).to(DEV)
+    dB = torch.from_numpy(B.view(np.int64)).to(DEV)
+    torch.cuda.synchronize()
+    outs = []
+    for k in range(3):
+        oA = torch.full((A.shape[0],), 7, dtype=torch.uint8, device=DEV)
+        oB = torch.full((B.shape[0],), 7, dtype=torch.uint8, device=DEV)
+        torch.cuda.synchronize()
+        isp.isprime_device(dA, oA, stream=s1)
+        isp.isprime_device(dB, oB, stream=s2)
+        isp.isprime_device(dA, oA, stream=s2 if k == 2 else s1)
+        outs.append((oA, oB))
+    torch.cuda.synchronize()
+    for oA, oB in outs:
+        assert_same(oA.cpu().numpy(), expA, A)
+        assert_same(oB.cpu().numpy(), expB, B)
+    res = {}
+
+    def host_call(name, N):
+        res[name] = isp.isprime(N)
+
+    th = [threading.Thread(target=host_call, args=(nm, N)) for nm, N in (("A", A), ("B", B), ("A2", A))]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join()
+    assert_same(res["A"], expA, A)
+    assert_same(res["A2"], expA, A)
+    assert_same(res["B"], expB, B)
+
+
 # ------------------------------------------------------------------ options never change a bit
 def test_options_do_not_change_results():
     N = np.concatenate([workloads.generate("C5", count=300_000), workloads.generate("C2", count=100_000),
