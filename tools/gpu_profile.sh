@@ -3,7 +3,8 @@
 #   gpurun_out/bench.json          default bench.py line (no profiler attached)
 #   gpurun_out/launches_C5.csv     ncu launch list of the same bench command (gpu__time_duration per launch)
 #   gpurun_out/prof_C5.ncu-rep     ncu --set full of plan/sieve/classify/sort/mr1/mr2 on C5
-#   gpurun_out/prof_C4.ncu-rep     ncu --set full of classify + sieve on a C4 chunk
+#   gpurun_out/prof_C4.ncu-rep     ncu --set full of dense + classify + sieve on a C4 chunk
+#   gpurun_out/prof_C3.ncu-rep, prof_C2.ncu-rep   the witness kernels and classify on C3 / C2
 # Every profiled command first exits 0 without ncu.
 set -u
 cd "$(dirname "$0")/.."
@@ -20,3 +21,9 @@ echo "full C5 rc=$?" >> gpurun_out/prof_status.txt
 python tools/explore.py C4 > gpurun_out/ncu_plain_c4.json 2>&1 && \
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:"dense_kernel|classify_kernel|sieve_kernel" -s 9 -c 3 -o gpurun_out/prof_C4 python tools/explore.py C4 > gpurun_out/ncu_full_c4.log 2>&1
 echo "full C4 rc=$?" >> gpurun_out/prof_status.txt
+python tools/explore.py C3 > gpurun_out/ncu_plain_c3.json 2>&1 && \
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:"classify_kernel|mr1_kernel|mr2_kernel" -s 9 -c 3 -o gpurun_out/prof_C3 python tools/explore.py C3 > gpurun_out/ncu_full_c3.log 2>&1
+echo "full C3 rc=$?" >> gpurun_out/prof_status.txt
+python tools/explore.py C2 > gpurun_out/ncu_plain_c2.json 2>&1 && \
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:"classify_kernel|mr1_kernel|mr2_kernel" -s 9 -c 3 -o gpurun_out/prof_C2 python tools/explore.py C2 > gpurun_out/ncu_full_c2.log 2>&1
+echo "full C2 rc=$?" >> gpurun_out/prof_status.txt

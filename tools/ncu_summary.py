@@ -11,6 +11,7 @@ import csv
 import io
 import json
 import os
+import re
 import subprocess
 import sys
 
@@ -89,11 +90,19 @@ def main():
     tpath = os.path.join(os.path.dirname(os.path.abspath(__file__)), "..", "profiles", "ncu_kernel_metrics.json")
     old = json.load(open(tpath)) if os.path.exists(tpath) else {}
     src = os.path.relpath(os.path.join(outdir, "full_summary.json"), os.path.dirname(tpath))
+    # entries are keyed "<short>@<config>" when the output directory names the
+    # configuration (r1_ncu_C5_v11 -> C5), which bench.py looks up per config;
+    # the plain "<short>" key is refreshed only by launches that did work (a
+    # no-op launch, e.g. classify on a dense chunk, must not stand for the kernel)
+    m = re.search(r"_(C\d)_", os.path.basename(os.path.normpath(outdir)) + "_")
+    cfg = m.group(1) if m else None
     for base, s in summary.items():
         def pct(k):
             v = s.get(k)
             return float(v.split()[0]) if v else None
-        old[s["short"]] = {
+        dur = s.get("gpu__time_duration.sum", "0 ms").split()
+        dur_ms = float(dur[0]) * (1e-3 if len(dur) > 1 and dur[1] == "us" else 1.0)
+        ent = {
             "dram_bytes_per_launch": s["dram_bytes_per_launch"],
             "fmaheavy_pipe_pct": pct("sm__pipe_fmaheavy_cycles_active.avg.pct_of_peak_sustained_elapsed"),
             "fp64_pipe_pct": pct("sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active"),
@@ -102,6 +111,10 @@ def main():
             "dram_pct": pct("gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed"),
             "source": src,
         }
+        if cfg:
+            old[f"{s['short']}@{cfg}"] = ent
+        if dur_ms >= 0.05:
+            old[s["short"]] = ent
     with open(tpath, "w") as f:
         json.dump(old, f, indent=1)
     print(json.dumps({k: {kk: vv for kk, vv in v.items() if kk in ("short", "gpu__time_duration.sum",
