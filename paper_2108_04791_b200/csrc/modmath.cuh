@@ -567,18 +567,26 @@ __device__ __forceinline__ double fmul_lazy(double a, double b, const ModF& M) {
     return fma(-q, M.n, h) + l;
 }
 
-// x^2 * 2^b for the base-2 ladder (ModMultiply case 3 folded in as an exact
-// power-of-two scaling of one factor).  |x| < n, b in {0, 1}.
-__device__ __forceinline__ double fsqr_dbl_lazy(double x, bool b, const ModF& M) {
-    return fmul_lazy(x * (b ? 2.0 : 1.0), x, M);
+// x * 2^b for b = bit 31 of w, by adding b to the exponent field of the
+// double (exact for any nonzero x of normal magnitude; the ladders' residues of
+// powers of 2 are never 0 for odd n) -- three integer instructions instead of
+// a 64-bit compare, a select and a DMUL on the FP64 pipe.
+__device__ __forceinline__ double fscale2_top(double x, uint32_t w) {
+    return __hiloint2double(__double2hiint(x) + (int)((w >> 31) << 20), __double2loint(x));
 }
 
-// b ? 2y mod n : y for |y| < n < 2^51, lazily: z = 2^b y exactly (|z| < 2n),
+// x^2 * 2^b for the base-2 ladder (ModMultiply case 3 folded in as an exact
+// power-of-two scaling of one factor).  |x| < n, b = bit 31 of w.
+__device__ __forceinline__ double fsqr_dbl_lazy(double x, uint32_t w, const ModF& M) {
+    return fmul_lazy(fscale2_top(x, w), x, M);
+}
+
+// 2^b y mod n (b = bit 31 of w) for |y| < n < 2^51, lazily: z = 2^b y exactly (|z| < 2n),
 // k = round(z / n) in {-2 .. 2} (the 1.5 * 2^52 addend, |z / n| < 2), r = z - k n
 // exact with |r| <= n/2 + 1.  The base-2 ladder's doubling where folding it
 // into the product would break fmul_lazy's bound (2^50 <= n < 2^51).
-__device__ __forceinline__ double fdbl_if_lazy(double y, bool b, const ModF& M) {
-    const double z = y * (b ? 2.0 : 1.0);
+__device__ __forceinline__ double fdbl_if_lazy(double y, uint32_t w, const ModF& M) {
+    const double z = fscale2_top(y, w);  // 2^b y, b = bit 31 of w
     const double k = fma(z, M.ninv, FP_RND) - FP_RND;
     return fma(-k, M.n, z);
 }

@@ -280,7 +280,7 @@ __device__ __forceinline__ bool sprp2_f64(unsigned long long n) {
             // n < 2^50: the doubling folded into the product (|2x| < 2n is allowed)
 #pragma unroll 2
             for (int k = 0; k < top; k++) {
-                x = fsqr_dbl_lazy(x, (long long)dd < 0, M);
+                x = fsqr_dbl_lazy(x, (uint32_t)(dd >> 32), M);
                 dd += dd;
             }
         } else {
@@ -288,7 +288,7 @@ __device__ __forceinline__ bool sprp2_f64(unsigned long long n) {
             // (|2y| < 2n, k = round(2y / n) in {-2 .. 2})
 #pragma unroll 2
             for (int k = 0; k < top; k++) {
-                x = fdbl_if_lazy(fmul_lazy(x, x, M), (long long)dd < 0, M);
+                x = fdbl_if_lazy(fmul_lazy(x, x, M), (uint32_t)(dd >> 32), M);
                 dd += dd;
             }
         }
