@@ -159,13 +159,16 @@ int isprime_reset_kernel_times(void);
 
 /* out[i] = 1 iff n[i] (odd, >= 3) is a strong probable prime to base a[i]
  * (Eq 1-3; a reduced mod n, 0 passes), computed with the
- * device Montgomery library of the witness kernels (32-bit when n < 2^32).
+ * device arithmetic of the witness kernels for n's class (FP64 lazy residues
+ * below 2^51, 64-bit Montgomery above; window width from option "win64").
  * Device pointers, stream-ordered.  Elements with n even or < 3 give 0. */
 int isprime_sprp_device(const uint64_t* dn, const uint64_t* da, uint8_t* dout,
                         size_t count, void* stream);
 
-/* out[i] = a[i] * b[i] mod m[i] through Montgomery form (odd m >= 3; a, b are
- * reduced mod m first).  Device pointers, stream-ordered.  m even -> 0. */
+/* out[i] = a[i] * b[i] mod m[i] (odd m >= 3; a, b are reduced mod m first) with
+ * the product the witness kernels use for m's class: FP64 lazy residues below
+ * 2^51, the lazy additive Montgomery REDC below 2^62, the subtraction REDC
+ * above.  Device pointers, stream-ordered.  m even -> 0. */
 int isprime_mulmod_device(const uint64_t* da, const uint64_t* db,
                           const uint64_t* dm, uint64_t* dout, size_t count,
                           void* stream);

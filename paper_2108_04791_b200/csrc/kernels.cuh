@@ -1631,7 +1631,7 @@ __global__ void sprp_diag_kernel(const unsigned long long* __restrict__ n, const
     const unsigned long long nn = n[i], aa = a[i];
     bool r = false;
     if (nn >= 3 && (nn & 1ull)) {
-        if (nn < (1ull << 32)) {
+        if (nn < (1ull << 32) && !CLS32_FP64) {  // the pipeline's arithmetic for each class
             const uint32_t am = (uint32_t)(aa % nn);
             if (am == 2u) r = sprp2_32((uint32_t)nn);
             else { const uint32_t b[1] = {am}; r = sprp_multi32<1>((uint32_t)nn, b); }
@@ -1655,18 +1655,23 @@ __global__ void mulmod_diag_kernel(const unsigned long long* __restrict__ a, con
     if (i >= count) return;
     const unsigned long long mm = m[i];
     if (mm < 3 || !(mm & 1ull)) { out[i] = 0; return; }
-    if (mm < (1ull << 32)) {
-        const Mont32 M = mont32_setup((uint32_t)mm);
-        const uint32_t R2 = mont32_r2(M);
-        const uint32_t am = mmul32((uint32_t)(a[i] % mm), R2, M);
-        const uint32_t bm = mmul32((uint32_t)(b[i] % mm), R2, M);
-        out[i] = mmul32(mmul32(am, bm, M), 1u, M);  // REDC(x * 1) leaves Montgomery form
-    } else {
+    // the product the witness kernels use for m's class
+    if (mm < FP_LIMIT) {  // FP64 lazy signed residue, then the canonical one
+        const ModF M = modf_setup(mm);
+        const double r = fmul_lazy((double)(a[i] % mm), (double)(b[i] % mm), M);
+        out[i] = (unsigned long long)(r < 0.0 ? r + M.n : r);
+    } else if (mm < (1ull << 62)) {  // lazy additive REDC (PTX), representatives < 2m
+        const Mont64 M = mont64_setup(mm);
+        const unsigned long long nn = 0ull - M.ninv, R2 = mont64_r2(M);
+        const unsigned long long am = mmul64_lz_ptx(a[i] % mm, R2, mm, nn);
+        const unsigned long long bm = mmul64_lz_ptx(b[i] % mm, R2, mm, nn);
+        out[i] = mcanon64(mmul64_lz_ptx(mmul64_lz_ptx(am, bm, mm, nn), 1ull, mm, nn), mm);
+    } else {  // subtraction REDC (PTX)
         const Mont64 M = mont64_setup(mm);
         const unsigned long long R2 = mont64_r2(M);
-        const unsigned long long am = mmul64(a[i] % mm, R2, M);
-        const unsigned long long bm = mmul64(b[i] % mm, R2, M);
-        out[i] = mmul64(mmul64(am, bm, M), 1ull, M);
+        const unsigned long long am = mmul64_ptx(a[i] % mm, R2, mm, M.ninv);
+        const unsigned long long bm = mmul64_ptx(b[i] % mm, R2, mm, M.ninv);
+        out[i] = mmul64_ptx(mmul64_ptx(am, bm, mm, M.ninv), 1ull, mm, M.ninv);  // REDC(x * 1) leaves Montgomery form
     }
 }
 

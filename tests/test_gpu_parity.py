@@ -548,10 +548,13 @@ def test_mulmod_device_vs_oracle():
     small = rng.integers(3, 2**32 - 1, size=n // 4, dtype=np.uint64) | np.uint64(1)
     edge = np.array([3, 5, 2**32 - 5, 2**32 + 1, 2**32 - 1, 2**63 - 25, 2**63 + 1, 2**64 - 59, 2**64 - 1],
                     dtype=np.uint64)
-    m = np.concatenate([m, small, np.repeat(edge, 1000)])
+    logu = workloads.loguniform(91, n // 2, 2, 64) | np.uint64(1)  # every class: FP64, lazy and full REDC
+    edge = np.concatenate([edge, np.array([2**51 - 129, 2**51 + 1, 2**62 - 57, 2**62 + 1, 2**50 + 1, 2**49 - 81],
+                                          dtype=np.uint64)])
+    m = np.concatenate([m, small, logu, np.repeat(edge, 1000)])
     a = rng.integers(0, 2**64 - 1, size=m.shape[0], dtype=np.uint64, endpoint=True)
     b = rng.integers(0, 2**64 - 1, size=m.shape[0], dtype=np.uint64, endpoint=True)
-    a[-9000:] = m[-9000:] - np.uint64(1)
+    a[-edge.shape[0] * 1000:] = m[-edge.shape[0] * 1000:] - np.uint64(1)
     t = [torch.from_numpy(x.view(np.int64)).to(DEV) for x in (a, b, m)]
     out = torch.empty_like(t[0])
     isp.isprime_mulmod_device(*t, out)
@@ -563,7 +566,8 @@ def test_mulmod_device_vs_oracle():
 
 @pytest.mark.parametrize("win", [1, 2, 3])
 def test_sprp_device_vs_oracle(win):
-    """The witness step base by base (32-bit and 64-bit Montgomery paths)."""
+    """The witness step base by base, in the arithmetic of each class (FP64
+    below 2^51, 64-bit Montgomery above; window width 1..3)."""
     isp.set_option("win64", win)
     rng = np.random.default_rng(2 + win)
     n32 = rng.integers(3, 2**32 - 1, size=40000, dtype=np.uint64) | np.uint64(1)
