@@ -316,3 +316,29 @@ def test_jaeschke_set_bound_is_tight():
     for a in (2, 13, 23, 1662803):
         passed &= oracle.sprp_array(n, np.full(n.shape[0], a, dtype=np.uint64)).astype(bool)
     assert np.array_equal(passed, oracle.isprime(n).astype(bool))
+
+
+@pytest.mark.slow
+def test_definition_level_64bit_trial_division():
+    """The plain definition above 2^32 ("scale this up in the
+    builder's slow tests"): trial division by every prime below 2^32 -- which
+    decides primality of any n < 2^64 -- against the oracle's Eq 4
+    Miller-Rabin, on the first 64 C3 values (primes exactly at indices 29, 32
+    and 40), 2^64-59, 2^52-47, 3825123056546413051, Chernick
+    numbers and 64-bit C5 values."""
+    sieve = oracle.sieve(1 << 32)
+    primes = np.nonzero(sieve)[0].astype(np.uint64)
+    del sieve
+    c3 = workloads.generate("C3", count=64)
+    c5 = workloads.generate("C5", count=4096)
+    c5 = c5[c5 >= np.uint64(1 << 40)][:24]
+    extra = np.array([2**64 - 59, 2**52 - 47, 3825123056546413051] + workloads.chernick_numbers()[:8], dtype=np.uint64)
+    vals = np.concatenate([c3, c5, extra])
+    by_definition = []
+    for v in vals.tolist():
+        lim = int(np.sqrt(float(v))) + 2
+        p = primes[: np.searchsorted(primes, np.uint64(min(lim, 2**32 - 1)), side="right")]
+        by_definition.append(int(not np.any(np.uint64(v) % p == 0)))
+    assert by_definition == oracle.isprime(vals).tolist()
+    assert [i for i in range(64) if by_definition[i]] == [29, 32, 40]
+    assert by_definition[-11:-8] == [1, 1, 0]
