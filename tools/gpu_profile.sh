@@ -27,3 +27,12 @@ echo "full C3 rc=$?" >> gpurun_out/prof_status.txt
 python tools/explore.py C2 > gpurun_out/ncu_plain_c2.json 2>&1 && \
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:"classify_kernel|mr1_kernel|mr2_kernel" -s 9 -c 3 -o gpurun_out/prof_C2 python tools/explore.py C2 > gpurun_out/ncu_full_c2.log 2>&1
 echo "full C2 rc=$?" >> gpurun_out/prof_status.txt
+# summaries on the box (gpurun copies back at most 64 MiB of gpurun_out/):
+# per-config full_summary.json + the refreshed ncu_kernel_metrics.json; only
+# the C5 report itself is kept for per-line analysis
+TAG=${PROFILE_TAG:-latest}
+for c in C5 C4 C3 C2; do
+  [ -f gpurun_out/prof_$c.ncu-rep ] && python tools/ncu_summary.py gpurun_out/prof_$c.ncu-rep gpurun_out/r1_ncu_${c}_$TAG > /dev/null
+done
+cp profiles/ncu_kernel_metrics.json gpurun_out/ 2>/dev/null
+rm -f gpurun_out/prof_C4.ncu-rep gpurun_out/prof_C3.ncu-rep gpurun_out/prof_C2.ncu-rep
