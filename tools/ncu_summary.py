@@ -89,7 +89,8 @@ def main():
         json.dump(summary, f, indent=1)
     tpath = os.path.join(os.path.dirname(os.path.abspath(__file__)), "..", "profiles", "ncu_kernel_metrics.json")
     old = json.load(open(tpath)) if os.path.exists(tpath) else {}
-    src = os.path.relpath(os.path.join(outdir, "full_summary.json"), os.path.dirname(tpath))
+    # named as it is committed: profiles/<dir>/full_summary.json
+    src = os.path.basename(os.path.normpath(outdir)) + "/full_summary.json"
     # entries are keyed "<short>@<config>" when the output directory names the
     # configuration (r1_ncu_C5_v11 -> C5), which bench.py looks up per config;
     # the plain "<short>" key is refreshed only by launches that did work (a
