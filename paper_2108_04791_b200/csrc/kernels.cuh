@@ -3,12 +3,20 @@
 //   plan_kernel       A0  strided sample of N -> sieve window (cost model)
 //   sieve_kernel      A1  odd-only segmented sieve of Eratosthenes in shared
 //                         memory -> global bitmap for the window [wlo, whi)
+//   dense_kernel      A1+A2 for a dense range N[i] = N0 + i: sieve segments in
+//                         shared memory and classify straight from them
 //   classify_kernel   A2  one streaming pass over N: trivial cases, window
 //                         gather out[i] = bit(N[i]), small-prime trial
 //                         division, ballot/scan compaction of survivors
+//   qscatter_kernel   A2  per-block queue segments -> dense queues, ordered
+//                         by bit length when that pays
 //   mr1_kernel        A3  Miller-Rabin base 2 on the compacted survivors,
 //                         compacting strong probable primes again
 //   mr2_kernel        A4  the remaining bases, lockstep per element, out = 1
+//   small_kernel,     short arrays: the same steps per element in one launch
+//   small_warp_kernel
+// Magnitude classes: n < 2^51 on the FP64 pipe (lazy signed residues), above
+// with 64-bit Montgomery on the FMA-heavy pipe (modmath.cuh, witness.cuh).
 //
 // Cites: PAPER.md:22 / 279 (sieve, membership instead of division), :275-276
 // (shrinking by small primes), :37-56 (Miller-Rabin, Eq 4 bases), :299-330
