@@ -910,9 +910,11 @@ classify_kernel(const unsigned long long* __restrict__ N, uint8_t* __restrict__ 
         for (int e = 0; e < 8; e++) {  // all eight bitmap reads in flight together
             const uint32_t xlo = (uint32_t)v[e], xhi = (uint32_t)(v[e] >> 32);
             dd[e] = xlo - wlo32;
-            const uint32_t in = (uint32_t)(xhi == 0u) & xlo & (uint32_t)(dd[e] <= spanm1w) & 1u;
-            inmask |= in << e;
-            word[e] = in ? __ldg(bitmap + (dd[e] >> 6)) : 0u;
+            // predicate form: one compare chain, a predicated load
+            const bool in = (xlo & 1u) && xhi == 0u && dd[e] <= spanm1w;
+            word[e] = 0u;
+            if (in) word[e] = __ldg(bitmap + (dd[e] >> 6));
+            inmask |= (uint32_t)in << e;
         }
 #pragma unroll
         for (int e = 0; e < 8; e++) {
