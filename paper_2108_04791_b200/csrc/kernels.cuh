@@ -904,11 +904,16 @@ classify_kernel(const unsigned long long* __restrict__ N, uint8_t* __restrict__ 
         uint8_t r[8];
         uint32_t word[8], dd[8];
         uint32_t inmask = 0;
+        // 32-bit halves through a register split the compiler cannot fold back
+        // into 64-bit compares (x >> 32 == 0 otherwise becomes x < 2^32: two ISETPs)
+        uint32_t vlo[8], vhi[8];
+#pragma unroll
+        for (int e = 0; e < 8; e++) asm("mov.b64 {%0, %1}, %2;" : "=r"(vlo[e]), "=r"(vhi[e]) : "l"(v[e]));
         // flags as 0/1 integers combined with bitwise operators: no short-circuit
         // branches and few live predicates
 #pragma unroll
         for (int e = 0; e < 8; e++) {  // all eight bitmap reads in flight together
-            const uint32_t xlo = (uint32_t)v[e], xhi = (uint32_t)(v[e] >> 32);
+            const uint32_t xlo = vlo[e], xhi = vhi[e];
             dd[e] = xlo - wlo32;
             // predicate form: one compare chain, a predicated load
             const bool in = (xlo & 1u) && xhi == 0u && dd[e] <= spanm1w;
@@ -918,7 +923,7 @@ classify_kernel(const unsigned long long* __restrict__ N, uint8_t* __restrict__ 
         }
 #pragma unroll
         for (int e = 0; e < 8; e++) {
-            const uint32_t xlo = (uint32_t)v[e], xhi = (uint32_t)(v[e] >> 32);
+            const uint32_t xlo = vlo[e], xhi = vhi[e];
             const uint32_t big = (uint32_t)(xhi != 0u);
             const uint32_t bit = __funnelshift_r(word[e], word[e], dd[e] >> 1) & 1u;  // 0 outside the window
             r[e] = (uint8_t)(bit | ((uint32_t)(xlo == 2u) & (big ^ 1u)));
