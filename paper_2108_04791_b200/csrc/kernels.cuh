@@ -852,6 +852,11 @@ classify_kernel(const unsigned long long* __restrict__ N, uint8_t* __restrict__ 
                 v[e] = i < len ? N[i] : 0ull;
             }
         }
+        // 32-bit halves through a register split the compiler cannot fold back
+        // into 64-bit compares (x >> 32 == 0 otherwise becomes x < 2^32: two ISETPs)
+        uint32_t vlo[8], vhi[8];
+#pragma unroll
+        for (int e = 0; e < 8; e++) asm("mov.b64 {%0, %1}, %2;" : "=r"(vlo[e]), "=r"(vhi[e]) : "l"(v[e]));
         // ---- window fast path: the whole warp-tile lies below 2^32 and inside
         // the window (a dense or clustered range, config C4).  Then out[i] =
         // bit(N[i]) for odd values and (N[i] == 2) for even ones -- about a
@@ -861,13 +866,13 @@ classify_kernel(const unsigned long long* __restrict__ N, uint8_t* __restrict__ 
         if (full && vec_out && span != 0) {
             uint32_t hor = 0;
 #pragma unroll
-            for (int e = 0; e < 8; e++) hor |= (uint32_t)(v[e] >> 32);
+            for (int e = 0; e < 8; e++) hor |= vhi[e];
             if (__all_sync(0xffffffffu, hor == 0u)) {
                 uint32_t dd[8];
                 bool in = true;
 #pragma unroll
                 for (int e = 0; e < 8; e++) {
-                    dd[e] = (uint32_t)v[e] - wlo32;
+                    dd[e] = vlo[e] - wlo32;
                     in &= dd[e] <= spanm1;
                 }
                 fast = __all_sync(0xffffffffu, in);
@@ -881,7 +886,7 @@ classify_kernel(const unsigned long long* __restrict__ N, uint8_t* __restrict__ 
 #pragma unroll
                         for (int k = 0; k < 2; k++) {
                             const int e = 2 * j + k;
-                            const uint32_t lo = (uint32_t)v[e];
+                            const uint32_t lo = vlo[e];
                             // bit (dd >> 1) & 31 of the word <-> odd value wlo + dd; even values read 0 (lo & 1)
                             uint32_t bit = __funnelshift_r(w[e], w[e], dd[e] >> 1) & lo & 1u;
                             bit = lo == 2u ? 1u : bit;
@@ -904,11 +909,6 @@ classify_kernel(const unsigned long long* __restrict__ N, uint8_t* __restrict__ 
         uint8_t r[8];
         uint32_t word[8], dd[8];
         uint32_t inmask = 0;
-        // 32-bit halves through a register split the compiler cannot fold back
-        // into 64-bit compares (x >> 32 == 0 otherwise becomes x < 2^32: two ISETPs)
-        uint32_t vlo[8], vhi[8];
-#pragma unroll
-        for (int e = 0; e < 8; e++) asm("mov.b64 {%0, %1}, %2;" : "=r"(vlo[e]), "=r"(vhi[e]) : "l"(v[e]));
         // flags as 0/1 integers combined with bitwise operators: no short-circuit
         // branches and few live predicates
 #pragma unroll
