@@ -549,8 +549,9 @@ def test_mulmod_device_vs_oracle():
     edge = np.array([3, 5, 2**32 - 5, 2**32 + 1, 2**32 - 1, 2**63 - 25, 2**63 + 1, 2**64 - 59, 2**64 - 1],
                     dtype=np.uint64)
     logu = workloads.loguniform(91, n // 2, 2, 64) | np.uint64(1)  # every class: FP64, lazy and full REDC
-    edge = np.concatenate([edge, np.array([2**51 - 129, 2**51 + 1, 2**62 - 57, 2**62 + 1, 2**50 + 1, 2**49 - 81],
-                                          dtype=np.uint64)])
+    edge = np.concatenate([edge, np.array([2**51 - 129, 2**51 + 1, 2**62 - 57, 2**62 + 1, 2**50 + 1, 2**49 - 81,
+                                           2**39 + 1, 2**40 - 1, 2**60 - 1, 2**60 + 1, 3 * 2**58 + 1],
+                                          dtype=np.uint64)])  # + the R mod n quotient-estimate range (bit length 40..60)
     m = np.concatenate([m, small, logu, np.repeat(edge, 1000)])
     a = rng.integers(0, 2**64 - 1, size=m.shape[0], dtype=np.uint64, endpoint=True)
     b = rng.integers(0, 2**64 - 1, size=m.shape[0], dtype=np.uint64, endpoint=True)
