@@ -513,9 +513,9 @@ __device__ __forceinline__ uint64_t mont64_r2(const Mont64& M) {
     uint64_t x = M.one;
 #pragma unroll
     for (int i = 0; i < 8; i++) x = mdbl64(x, M.n);
-    x = msqr64(x, M);
-    x = msqr64(x, M);
-    x = msqr64(x, M);
+    x = msqr64_ptx(x, M.n, M.ninv);
+    x = msqr64_ptx(x, M.n, M.ninv);
+    x = msqr64_ptx(x, M.n, M.ninv);
     return x;
 }
 
