@@ -1085,7 +1085,7 @@ classify_kernel(const unsigned long long* __restrict__ N, uint8_t* __restrict__ 
 // lanes carry equal-length exponents.  When the expected gain is small
 // (sort_pays) the same pass only compacts classify's per-block segments.
 constexpr int SORT_THREADS = 256;
-constexpr int SORT_TILE = 2048;
+constexpr int SORT_TILE = 1024;
 
 __device__ __forceinline__ unsigned int bitlen32(uint32_t v) { return 32u - __clz(v); }
 __device__ __forceinline__ unsigned int bitlen64u(unsigned long long v) { return 64u - __clzll((long long)v); }
