@@ -35,9 +35,9 @@ constexpr int PRESIEVE_PERIOD = 3 * 5 * 7 * 11 * 13;  // 15015 (odd-index period
 constexpr int PRESIEVE_COPIES = 16;                   // shifted copies for 16-B loads
 constexpr int PRESIEVE_LEN = ((PRESIEVE_PERIOD + SEG_ODD + 64 + 15) / 16) * 16;
 constexpr int FIRST_CROSS_PRIME_IDX = 5;              // odd primes 3,5,7,11,13 pre-sieved
-constexpr int CLS_THREADS = 256;
+constexpr int CLS_THREADS = 512;
 constexpr int CLS_PAIRS = 4;                          // 2 elements per pair -> 8 per thread
-constexpr int CLS_TILE = CLS_THREADS * 2 * CLS_PAIRS; // 2048 elements per tile
+constexpr int CLS_TILE = CLS_THREADS * 2 * CLS_PAIRS; // 4096 elements per block tile
 constexpr int MR_THREADS = 256;
 constexpr int MAX_SEG = 4096;                         // classify blocks (queue segments) per launch
 
@@ -1323,7 +1323,7 @@ __device__ __forceinline__ void stage_flush(WarpStage<T>& st, unsigned int& n, u
 // rounds while the rest of the GPU idles; claiming 32 at a time from the
 // start costs an atomic round trip per round, which cheap 32-bit entries
 // cannot hide.  div[r] = 0: fixed MR_CHUNK for region r.
-constexpr unsigned int MR_CHUNK = 256;
+constexpr unsigned int MR_CHUNK = 128;
 constexpr unsigned int MR_CHUNK_TAIL = 32;
 
 __device__ __forceinline__ bool next_chunk(const unsigned int (&size)[3], unsigned int* cur, int& r, int& tried,
