@@ -1084,7 +1084,7 @@ classify_kernel(const unsigned long long* __restrict__ N, uint8_t* __restrict__ 
 // queues waste about a quarter of the multiply pipe; sorted, neighbouring
 // lanes carry equal-length exponents.  When the expected gain is small
 // (sort_pays) the same pass only compacts classify's per-block segments.
-constexpr int SORT_THREADS = 256;
+constexpr int SORT_THREADS = 512;
 constexpr int SORT_TILE = 1024;
 
 __device__ __forceinline__ unsigned int bitlen32(uint32_t v) { return 32u - __clz(v); }
