@@ -227,7 +227,9 @@ int init_ctx(Ctx* c) {
     CK(cudaFuncSetAttribute(sieve_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SEG_ODD));
     CK(cudaFuncSetAttribute(dense_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * SEG_ODD));
     c->grid_sieve = c->sms * occupancy((const void*)sieve_kernel, SIEVE_THREADS, SEG_ODD);
-    c->grid_cls = c->sms * occupancy((const void*)classify_kernel<24, 24>, CLS_THREADS, 0);
+    CK(cudaFuncSetAttribute((const void*)classify_kernel<24, 24>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            (int)sizeof(ClsSmem)));
+    c->grid_cls = c->sms * occupancy((const void*)classify_kernel<24, 24>, CLS_THREADS, sizeof(ClsSmem));
     if (c->grid_cls > MAX_SEG) c->grid_cls = MAX_SEG;  // one queue segment per classify block
     c->grid_mr1 = c->sms * occupancy((const void*)mr1_kernel, MR_THREADS, 0);
     c->grid_sort = c->sms * occupancy((const void*)qscatter_kernel, SORT_THREADS, 0);
@@ -309,15 +311,22 @@ bool overlaps(const void* a, size_t an, const void* b, size_t bn) {
 // constant-bank operands then sit in the IMAD instructions themselves).
 int td_round(int v) { return v >= 32 ? 32 : v >= 24 ? 24 : v >= 16 ? 16 : v >= 8 ? 8 : 0; }
 
+template <typename K>
+void launch_cls(K k, int g, cudaStream_t s, const unsigned long long* N, uint8_t* out, uint32_t len, Ctx* c,
+                const TDParams& td, int vin, int vout, uint32_t ss) {
+    cudaFuncSetAttribute((const void*)k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(ClsSmem));
+    launch_k(k, g, CLS_THREADS, sizeof(ClsSmem), s, N, out, len, c->plan, c->bitmap, c->q, td, vin, vout, ss);
+}
+
 template <int A>
 void launch_classify_b(int n64, int g, cudaStream_t s, const unsigned long long* N, uint8_t* out, uint32_t len,
                        Ctx* c, const TDParams& td, int vin, int vout, uint32_t ss) {
     switch (n64) {
-        case 32: launch_k(classify_kernel<A, 32>, g, CLS_THREADS, 0, s, N, out, len, c->plan, c->bitmap, c->q, td, vin, vout, ss); break;
-        case 24: launch_k(classify_kernel<A, 24>, g, CLS_THREADS, 0, s, N, out, len, c->plan, c->bitmap, c->q, td, vin, vout, ss); break;
-        case 16: launch_k(classify_kernel<A, 16>, g, CLS_THREADS, 0, s, N, out, len, c->plan, c->bitmap, c->q, td, vin, vout, ss); break;
-        case 8: launch_k(classify_kernel<A, 8>, g, CLS_THREADS, 0, s, N, out, len, c->plan, c->bitmap, c->q, td, vin, vout, ss); break;
-        default: launch_k(classify_kernel<A, 0>, g, CLS_THREADS, 0, s, N, out, len, c->plan, c->bitmap, c->q, td, vin, vout, ss); break;
+        case 32: launch_cls(classify_kernel<A, 32>, g, s, N, out, len, c, td, vin, vout, ss); break;
+        case 24: launch_cls(classify_kernel<A, 24>, g, s, N, out, len, c, td, vin, vout, ss); break;
+        case 16: launch_cls(classify_kernel<A, 16>, g, s, N, out, len, c, td, vin, vout, ss); break;
+        case 8: launch_cls(classify_kernel<A, 8>, g, s, N, out, len, c, td, vin, vout, ss); break;
+        default: launch_cls(classify_kernel<A, 0>, g, s, N, out, len, c, td, vin, vout, ss); break;
     }
 }
 
@@ -458,7 +467,7 @@ int device_impl(Ctx* c, const unsigned long long* dN, uint8_t* dout, size_t n, c
         }
         {
             KScope ks(K_SORT, s);
-            const int gs = c->grid_sort < gcls ? c->grid_sort : gcls;
+            const int gs = SORT_SPLIT * gcls;  // SORT_SPLIT blocks per classify segment
             launch_k(qscatter_kernel, gs, SORT_THREADS, 0, s, c->plan, c->q, gcls, seg_stride);
             CKL("qscatter_kernel");
         }

@@ -35,9 +35,9 @@ constexpr int PRESIEVE_PERIOD = 3 * 5 * 7 * 11 * 13;  // 15015 (odd-index period
 constexpr int PRESIEVE_COPIES = 16;                   // shifted copies for 16-B loads
 constexpr int PRESIEVE_LEN = ((PRESIEVE_PERIOD + SEG_ODD + 64 + 15) / 16) * 16;
 constexpr int FIRST_CROSS_PRIME_IDX = 5;              // odd primes 3,5,7,11,13 pre-sieved
-constexpr int CLS_THREADS = 512;
+constexpr int CLS_THREADS = 1024;
 constexpr int CLS_PAIRS = 4;                          // 2 elements per pair -> 8 per thread
-constexpr int CLS_TILE = CLS_THREADS * 2 * CLS_PAIRS; // 4096 elements per block tile
+constexpr int CLS_TILE = CLS_THREADS * 2 * CLS_PAIRS; // 8192 elements per block tile
 constexpr int MR_THREADS = 256;
 constexpr int MAX_SEG = 4096;                         // classify blocks (queue segments) per launch
 
@@ -816,7 +816,8 @@ classify_kernel(const unsigned long long* __restrict__ N, uint8_t* __restrict__ 
                 DevPlan* __restrict__ plan, const uint32_t* __restrict__ bitmap, Queues q, TDParams td,
                 int vec_in, int vec_out, uint32_t seg_stride) {
     pdl_wait();
-    __shared__ ClsSmem sm;
+    extern __shared__ __align__(16) unsigned char cls_smem[];  // sizeof(ClsSmem), dynamic (> 48 KB at 1024 threads)
+    ClsSmem& sm = *reinterpret_cast<ClsSmem*>(cls_smem);
     const uint32_t segbase = blockIdx.x * seg_stride;
     // dense_kernel already classified a dense range; if it found a mismatch,
     // this pass redoes the chunk without the window (no global bitmap was sieved)
@@ -1086,6 +1087,9 @@ classify_kernel(const unsigned long long* __restrict__ N, uint8_t* __restrict__ 
 // (sort_pays) the same pass only compacts classify's per-block segments.
 constexpr int SORT_THREADS = 512;
 constexpr int SORT_TILE = 1024;
+#ifndef SORT_SPLIT
+#define SORT_SPLIT 4
+#endif
 
 __device__ __forceinline__ unsigned int bitlen32(uint32_t v) { return 32u - __clz(v); }
 __device__ __forceinline__ unsigned int bitlen64u(unsigned long long v) { return 64u - __clzll((long long)v); }
@@ -1137,10 +1141,12 @@ __device__ __forceinline__ void gather_segments(bool sort, const unsigned int* _
     }
     __syncthreads();
     constexpr int PER = SORT_TILE / SORT_THREADS;
-    for (int g = blockIdx.x; g < nseg; g += gridDim.x) {
+    // SORT_SPLIT blocks share a segment, taking its tiles in turn
+    const int part = blockIdx.x % SORT_SPLIT;
+    for (int g = blockIdx.x / SORT_SPLIT; g < nseg; g += gridDim.x / SORT_SPLIT) {
         const unsigned int count = segcnt[g];
         const size_t sb = (size_t)g * stride;
-        for (unsigned int t0 = 0; t0 < count; t0 += SORT_TILE) {
+        for (unsigned int t0 = part * SORT_TILE; t0 < count; t0 += SORT_SPLIT * SORT_TILE) {
             uint32_t idx[PER];
             T val[PER];
 #pragma unroll
