@@ -231,7 +231,7 @@ int init_ctx(Ctx* c) {
                             (int)sizeof(ClsSmem)));
     c->grid_cls = c->sms * occupancy((const void*)classify_kernel<24, 24>, CLS_THREADS, sizeof(ClsSmem));
     if (c->grid_cls > MAX_SEG) c->grid_cls = MAX_SEG;  // one queue segment per classify block
-    c->grid_mr1 = c->sms * occupancy((const void*)mr1_kernel, MR_THREADS, 0);
+    c->grid_mr1 = c->sms * occupancy((const void*)mr1_kernel, MR1_THREADS, 0);
     c->grid_sort = c->sms * occupancy((const void*)qscatter_kernel, SORT_THREADS, 0);
     c->grid_mr2 = c->sms * occupancy((const void*)mr2_kernel<2, false, 3>, MR_THREADS, 0);
     CK(cudaEventCreateWithFlags(&c->last_done, cudaEventDisableTiming));
@@ -473,7 +473,7 @@ int device_impl(Ctx* c, const unsigned long long* dN, uint8_t* dout, size_t n, c
         }
         {
             KScope ks(K_MR1, s);
-            launch_k(mr1_kernel, mr_grid(c->grid_mr1, len), MR_THREADS, 0, s, c->plan, c->q, g_opt.kernel_timing);
+            launch_k(mr1_kernel, mr_grid(c->grid_mr1, len), MR1_THREADS, 0, s, c->plan, c->q, g_opt.kernel_timing);
             CKL("mr1_kernel");
         }
         {

@@ -38,7 +38,11 @@ constexpr int FIRST_CROSS_PRIME_IDX = 5;              // odd primes 3,5,7,11,13 
 constexpr int CLS_THREADS = 1024;
 constexpr int CLS_PAIRS = 4;                          // 2 elements per pair -> 8 per thread
 constexpr int CLS_TILE = CLS_THREADS * 2 * CLS_PAIRS; // 8192 elements per block tile
-constexpr int MR_THREADS = 256;
+constexpr int MR_THREADS = 256;                       // phase 2 (shared-memory window tables)
+#ifndef MR1_THREADS_DEF
+#define MR1_THREADS_DEF 512
+#endif
+constexpr int MR1_THREADS = MR1_THREADS_DEF;          // phase 1
 constexpr int MAX_SEG = 4096;                         // classify blocks (queue segments) per launch
 
 // Programmatic dependent launch: the pipeline kernels are launched with the
@@ -1376,11 +1380,11 @@ __device__ __forceinline__ unsigned int fp_class_count(const DevPlan* plan) {
     return c;
 }
 
-__global__ void __launch_bounds__(MR_THREADS)
+__global__ void __launch_bounds__(MR1_THREADS)
 mr1_kernel(DevPlan* __restrict__ plan, Queues q, int count_work) {
     pdl_wait();
-    __shared__ WarpStage<uint32_t> st32[MR_THREADS / 32];
-    __shared__ WarpStage<unsigned long long> st64i[MR_THREADS / 32], st64f[MR_THREADS / 32];
+    __shared__ WarpStage<uint32_t> st32[MR1_THREADS / 32];
+    __shared__ WarpStage<unsigned long long> st64i[MR1_THREADS / 32], st64f[MR1_THREADS / 32];
     __shared__ unsigned int s_nf;
     if (threadIdx.x == 0) s_nf = fp_class_count(plan);
     __syncthreads();
@@ -1401,7 +1405,7 @@ mr1_kernel(DevPlan* __restrict__ plan, Queues q, int count_work) {
     // base-2 rounds of 32-bit entries are short: whole chunks (div 0); the
     // 64-bit classes shrink their chunks towards the end
     const unsigned int div[3] = {0u, 2u, 2u};
-    while (next_chunk(size, plan->cur1, r, tried, start, end, gridDim.x * (MR_THREADS / 32), div)) {
+    while (next_chunk(size, plan->cur1, r, tried, start, end, gridDim.x * (MR1_THREADS / 32), div)) {
         for (unsigned int b = start; b < end; b += 32) {
             const unsigned int i = b + lane;
             const bool act = i < end;
