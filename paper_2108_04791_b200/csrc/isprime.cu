@@ -402,6 +402,7 @@ int device_impl(Ctx* c, const unsigned long long* dN, uint8_t* dout, size_t n, c
         const unsigned long long pn = c->hbp[td.n32].x;  // first prime not trial-divided
         const unsigned long long sq = pn * pn;
         td.sq32 = sq > 0xFFFFFFFFull ? 0xFFFFFFFFu : (uint32_t)sq;
+        td.rnd = 6755399441055744.0;  // 1.5 * 2^52
     }
     if ((long long)n <= g_opt.small_max && g_opt.force_path == 0) {
         // short array: one fused launch (small_kernel), latency instead of pipeline stages

@@ -102,6 +102,8 @@ struct Queues {
 struct TDParams {
     int n32, n64;              // primes used for the 32-bit / 64-bit classes
     uint32_t sq32;             // (first prime not tested)^2 capped: v below it with no factor is prime
+    double rnd;                // 1.5 * 2^52 (a parameter, so it sits in a register and the trial
+                               // division's DFMA keeps its constant slot for 1/M)
 };
 
 // Trial-division constants: p, p^-1 mod 2^32 / 2^64, floor((2^k - 1) / p).
@@ -234,7 +236,7 @@ __host__ __device__ constexpr TDGroupConst make_td_group_const() {
 __constant__ TDGroupConst c_tdg = make_td_group_const();
 
 template <int NP, int G>
-__device__ __forceinline__ bool td_groups(double xh, double xl) {
+__device__ __forceinline__ bool td_groups(double xh, double xl, double rnd) {
     if constexpr (G >= group_count(NP)) {
         return false;
     } else {
@@ -243,18 +245,20 @@ __device__ __forceinline__ bool td_groups(double xh, double xl) {
         constexpr double Md = (double)M;
         constexpr double c = (double)(uint32_t)((1ull << 32) % M);
         const double y = fma(xh, c, xl);                                                  // == x (mod M), < 2^53
-        const double q = fma(y, c_tdg.inv[NP / 8 - 1][G], 6755399441055744.0) - 6755399441055744.0;  // round(y / M)
+        // round(y / M); the 1.5 * 2^52 addend comes in a register (rnd), which
+        // leaves the DFMA's constant-bank slot to 1/M (no LDC per group)
+        const double q = fma(y, c_tdg.inv[NP / 8 - 1][G], rnd) - rnd;
         // r = y - q M + M in (0, 2M); adding 2^52 in the same DADD leaves r in the low word
         const uint32_t ri = (uint32_t)__double2loint(fma(-q, Md, y) + c_tdg.mb[NP / 8 - 1][G]);
-        return td_primes<group_start(NP, G), group_start(NP, G + 1)>(ri) | td_groups<NP, G + 1>(xh, xl);
+        return td_primes<group_start(NP, G), group_start(NP, G + 1)>(ri) | td_groups<NP, G + 1>(xh, xl, rnd);
     }
 }
 
 template <int NP>
-__device__ __forceinline__ bool td64_fp(unsigned long long x) {
+__device__ __forceinline__ bool td64_fp(unsigned long long x, double rnd) {
     const double xh = u32_to_f64((uint32_t)(x >> 32));
     const double xl = u32_to_f64((uint32_t)x);
-    return td_groups<NP, 0>(xh, xl);
+    return td_groups<NP, 0>(xh, xl, rnd);
 }
 
 // ------------------------------------------------------------- init kernels
@@ -1011,7 +1015,7 @@ classify_kernel(const unsigned long long* __restrict__ N, uint8_t* __restrict__ 
                     const unsigned long long x = ws.val[255u - k];
                     bool comp = false;
 #pragma unroll
-                    if (N64 > 0) comp = td64_fp<N64>(x);
+                    if (N64 > 0) comp = td64_fp<N64>(x, td.rnd);
                     surv = !comp;
                 }
                 const uint32_t m = __ballot_sync(0xffffffffu, surv);
