@@ -84,7 +84,9 @@ void isprime_shutdown(void);
  *                    Jaeschke; verified over all n < 2^32); 7: the full Eq 4 set.
  * "td_primes32"      number of odd primes (from 3) trial-divided into values
  *                    below 2^32 before Miller-Rabin (0..ISP_MAX_TD)
- * "td_primes64"      same for values >= 2^32
+ * "td_primes64"      same for values >= 2^32.  Both are accepted in 0..ISP_MAX_TD
+ *                    and rounded down to the compiled variants 0, 8, 16, 24, 32
+ *                    (defaults 16 / 32; a v18 sweep found these the fastest).
  * "chunk_log2"       device chunk size (elements) = 2^value, 16..31 (default 30;
  *                    halved while the queues of a chunk do not fit in memory)
  * "win64"            exponent window width for the 64-bit multi-base phase (1..3,
