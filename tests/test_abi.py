@@ -71,6 +71,15 @@ def test_options_validate():
     isp.set_option("win64", 3)
     assert isp.get_option("win64") == 3
     isp.set_option("win64", old)
+    # trial-division counts: 0..ISP_MAX_TD accepted (rounded down to a compiled variant when used)
+    for key in ("td_primes32", "td_primes64"):
+        saved = isp.get_option(key)
+        for bad in (-1, 129):
+            with pytest.raises(isp.IsPrimeError):
+                isp.set_option(key, bad)
+        isp.set_option(key, 128)
+        assert isp.get_option(key) == 128
+        isp.set_option(key, saved)
     for key, bad, good in (("witness", 3, 2), ("small_max", -1, 0), ("warp_max", -1, 64)):
         saved = isp.get_option(key)
         with pytest.raises(isp.IsPrimeError):
