@@ -1014,7 +1014,6 @@ classify_kernel(const unsigned long long* __restrict__ N, uint8_t* __restrict__ 
                 if (k < n64) {
                     const unsigned long long x = ws.val[255u - k];
                     bool comp = false;
-#pragma unroll
                     if (N64 > 0) comp = td64_fp<N64>(x, td.rnd);
                     surv = !comp;
                 }

@@ -119,6 +119,10 @@ __device__ __forceinline__ bool sprp_multi32(uint32_t n, const uint32_t* bases) 
 }
 
 // ---------------------------------------------------------------- 64-bit ----
+#ifndef ISP_MR1_UNROLL
+#define ISP_MR1_UNROLL 2
+#endif
+constexpr int kMr1Unroll = ISP_MR1_UNROLL;  // Montgomery-class base-2 ladders (n >= 2^61); 1 / 2 / 4 measured: C3 phase 1 1.965 / 1.955 / 1.983 ms
 // Phase 1 (base 2).  n odd, n >= 3 (used for n >= 2^32).
 __device__ __forceinline__ bool sprp2_64(uint64_t n) {
     const Mont64 M = mont64_setup(n);
@@ -142,13 +146,13 @@ __device__ __forceinline__ bool sprp2_64(uint64_t n) {
             for_bits_msb(dd, top, [&](uint32_t w) { x = msqr64_shl_lz_ptx(x, n, nn, w >> 31); });
             x = mcanon64(x, n);
         } else if (!__any_sync(act, (unsigned)(n >> 63))) {
-#pragma unroll 2
+#pragma unroll kMr1Unroll
             for (int k = 0; k < top; k++) {
                 x = msqr64_shl_ptx(x, n, M.ninv, (uint32_t)(dd >> 63));
                 dd += dd;
             }
         } else {
-#pragma unroll 2
+#pragma unroll kMr1Unroll
             for (int k = 0; k < top; k++) {
                 x = mdbl64_if_ptx(msqr64_ptx(x, n, M.ninv), n, (uint32_t)(dd >> 63));
                 dd += dd;
