@@ -9,11 +9,18 @@ A step is one isprime_device() call over one batch: plan -> sieve -> classify
 (trial division + compaction) -> Miller-Rabin base 2 -> remaining bases, every
 row of SURVEY.md 8(a).  The headline workload is BASELINE.json configs[4]
 ("C5": n = 2^28 mixed magnitudes with Chernick and 2^64-59 inserts), the one
-configuration that exercises every row in a single step; C1-C4 are reported
-under "per_config".  Multi-GPU is weak scaling: rank r classifies generator
-indices [r n, (r+1) n) with no collective on the path (NCCL only reduces the
-prime count and the max time).  Inputs are 2 GiB per step (> 126 MB L2), so L2
-is not flushed between steps.
+configuration that exercises every row in a single step; the others are
+reported under "per_config".
+
+Multi-GPU: one process per GPU, no collective on the path
+(NCCL only reduces the prime count and the max time, outside the timed
+region).  --scaling weak (default): rank r classifies generator indices
+[r n, (r+1) n); --scaling strong: the fixed array of n elements is split
+contiguously, rank r owning [floor(r n / W), floor((r+1) n / W)).  C4 (the
+dense range 0 .. 2^32-1) is always split by value: rank r classifies the
+device iota [floor(r 2^32 / W), floor((r+1) 2^32 / W)) and sieves only that
+window.  Inputs of C3-C5 are >= 0.5 GiB per step (> 126 MB L2) and are not
+flushed; C1 / C2 are timed with an L2 flush between steps.
 """
 from __future__ import annotations
 
@@ -147,16 +154,61 @@ def load_counts():
     return out
 
 
-def make_input(cfg, rank, torch, dev):
-    """Rank's batch on the device (weak scaling: generator indices [r n, (r+1) n))."""
+def load_weak_counts():
+    """Prime counts of the weak-scaling batches (tests/golden/weak_shard_counts.txt,
+    oracle only): {cfg: {rank: count}}."""
+    out = {}
+    p = os.path.join(ROOT, "tests", "golden", "weak_shard_counts.txt")
+    if os.path.exists(p):
+        with open(p) as f:
+            for line in f:
+                line = line.split("#", 1)[0].split()
+                if line:
+                    out.setdefault(line[0], {})[int(line[1])] = int(line[2])
+    return out
+
+
+def shard_input(cfg, mode, rank, world):
+    """(kind, lo, hi) of rank's batch.  kind "iota": the values lo .. hi-1
+    (C4, split by value); kind "gen": generator indices [lo, hi) of cfg."""
+    from paper_2108_04791_b200 import shard
     n = workloads.CONFIGS[cfg][1]
     if cfg == "C4":
-        if rank != 0:
-            raise SystemExit("C4 is the fixed range 0..2^32-1; run it at --gpus 1")
-        return torch.arange(n, dtype=torch.int64, device=dev), None
-    host = workloads.generate(cfg, start=rank * n, count=n)
-    ht = torch.from_numpy(host.view(np.int64))
-    return ht.to(dev), host
+        a, b = shard.value_range_shard(rank, world, 0, n)
+        return "iota", a, b
+    if mode == "weak":
+        a, b = shard.weak_shard(rank, world, n)
+    else:
+        a, b = shard.strong_shard(rank, world, n)
+    return "gen", a, b
+
+
+def scaling_of(cfg, mode):
+    return "strong" if (cfg == "C4" or mode == "strong") else "weak"
+
+
+def global_units(cfg, mode, world):
+    n = workloads.CONFIGS[cfg][1]
+    return n * world if scaling_of(cfg, mode) == "weak" else n
+
+
+def expected_total(cfg, mode, world, counts, weak_counts):
+    """Prime count over all ranks' batches (None when no golden value exists)."""
+    if scaling_of(cfg, mode) == "strong":
+        return counts[cfg]
+    wc = weak_counts.get(cfg, {})
+    if all(r in wc for r in range(world)):
+        return sum(wc[r] for r in range(world))
+    return counts[cfg] if world == 1 else None
+
+
+def make_input(cfg, mode, rank, world, torch, dev):
+    """Rank's batch on the device, and its host copy (None for an iota)."""
+    kind, a, b = shard_input(cfg, mode, rank, world)
+    if kind == "iota":
+        return torch.arange(a, b, dtype=torch.int64, device=dev), None, (kind, a, b)
+    host = workloads.generate(cfg, start=a, count=b - a)
+    return torch.from_numpy(host.view(np.int64)).to(dev), host, (kind, a, b)
 
 
 L2_BYTES = 126 * 2**20
@@ -168,54 +220,67 @@ def l2_flush_needed(n):
     return n * 8 < 4 * L2_BYTES
 
 
-def time_steps_flushed(isp, torch, dN, dout, n, steps, warmup, stream):
-    """Per-step CUDA events with an L2 flush (a 512 MB write on the same
-    stream) between steps, outside the events: every step starts cold."""
+def time_steps(isp, torch, dN, dout, n, steps, warmup, stream, dist, sampler=None, flush=False):
+    """Per-step device time of isprime_device (ms), the MAX over ranks, and
+    the library's launch count over the timed steps.  W warm-up calls, then
+    barrier + synchronize, CUDA events on the launching stream around the K
+    timed calls, synchronize + barrier.  flush=True (inputs that fit in L2):
+    a 512 MB write on the same stream between steps, outside per-step events,
+    so every step starts from a cold L2."""
     global _flush_buf
-    if _flush_buf is None:
+    if flush and _flush_buf is None:
         _flush_buf = torch.empty(512 * 2**20, dtype=torch.uint8, device=dN.device)
     for _ in range(warmup):
         isp.isprime_device(dN, dout, n, stream)
     torch.cuda.synchronize()
+    if dist is not None:
+        dist.barrier()
+    torch.cuda.synchronize()
     l0 = isp.get_stats()["kernel_launches"]
-    evs = []
-    with torch.cuda.stream(stream):
+    if sampler:
+        sampler.mark()
+    if flush:
+        evs = []
+        with torch.cuda.stream(stream):
+            for _ in range(steps):
+                _flush_buf.fill_(1)
+                e0 = torch.cuda.Event(enable_timing=True)
+                e1 = torch.cuda.Event(enable_timing=True)
+                e0.record(stream)
+                isp.isprime_device(dN, dout, n, stream)
+                e1.record(stream)
+                evs.append((e0, e1))
+        torch.cuda.synchronize()
+        ms = sum(a.elapsed_time(b) for a, b in evs) / steps
+    else:
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
         for _ in range(steps):
-            _flush_buf.fill_(1)
-            e0 = torch.cuda.Event(enable_timing=True)
-            e1 = torch.cuda.Event(enable_timing=True)
-            e0.record(stream)
             isp.isprime_device(dN, dout, n, stream)
-            e1.record(stream)
-            evs.append((e0, e1))
-    torch.cuda.synchronize()
-    launches = isp.get_stats()["kernel_launches"] - l0
-    return sum(a.elapsed_time(b) for a, b in evs) / steps, launches
-
-
-def time_steps(isp, torch, dN, dout, n, steps, warmup, stream, dist, sampler=None):
-    for _ in range(warmup):
-        isp.isprime_device(dN, dout, n, stream)
-    torch.cuda.synchronize()
-    if dist is not None:
-        dist.barrier()
-    torch.cuda.synchronize()
-    e0 = torch.cuda.Event(enable_timing=True)
-    e1 = torch.cuda.Event(enable_timing=True)
-    l0 = isp.get_stats()["kernel_launches"]
+        e1.record(stream)
+        torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1) / steps
     if sampler:
         sampler.mark()
-    e0.record(stream)
-    for _ in range(steps):
-        isp.isprime_device(dN, dout, n, stream)
-    e1.record(stream)
-    torch.cuda.synchronize()
-    if sampler:
-        sampler.mark()
+    launches = isp.get_stats()["kernel_launches"] - l0
     if dist is not None:
         dist.barrier()
-    launches = isp.get_stats()["kernel_launches"] - l0
-    return e0.elapsed_time(e1) / steps, launches
+        t = torch.tensor([ms], dtype=torch.float64, device=dN.device)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    return ms, launches
+
+
+def count_total(isp, torch, dout, n, stream, dist):
+    """(this rank's prime count, NCCL sum over ranks) -- validation only."""
+    dcount = torch.zeros(1, dtype=torch.int64, device=dout.device)
+    isp.isprime_popcount_device(dout, dcount, n, stream)
+    torch.cuda.synchronize()
+    mine = int(dcount.item())
+    if dist is not None:
+        dist.all_reduce(dcount)
+    return mine, int(dcount.item())
 
 
 def kernel_profile(isp, torch, dN, dout, n, steps, stream):
@@ -289,18 +354,53 @@ def roofline(kern_ms, stats, n, steps, peaks, peaks_kind, clocks, cfg=None):
             "work": f"{nbytes:.4g} algorithmic bytes per step", "ms_per_step": round(ms, 4)}
 
 
-def cpu_baseline_run(cfg, host, sample_n):
+def cpu_model():
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def cpu_baseline_run(cfg, host, sample_n, sample1_n):
+    """The oracle as it stands on this host's cores: all threads on the first
+    sample_n elements, and one thread on the first sample1_n."""
     import oracle  # test infrastructure: the cpu_baseline leg only
-    if host is None:
-        sample = np.arange(sample_n, dtype=np.uint64)
-    else:
-        sample = host[:sample_n]
+    sample = np.arange(sample_n, dtype=np.uint64) if host is None else host[:sample_n]
     threads = os.cpu_count() or 1
     t = time.perf_counter()
     out = oracle.isprime(sample, threads=threads)
     dt = time.perf_counter() - t
+    s1 = sample[:sample1_n]
+    t = time.perf_counter()
+    oracle.isprime(s1, threads=1)
+    dt1 = time.perf_counter() - t
     return {"value": round(sample.shape[0] / dt / 1e9, 6), "unit": UNIT, "cores": threads, "kind": "oracle",
-            "sample": f"first {sample.shape[0]} elements of {cfg} ({dt:.2f} s wall, {int(out.sum())} primes)"}
+            "cpu_model": cpu_model(),
+            "sample": f"first {sample.shape[0]} elements of {cfg} ({dt:.2f} s wall on {threads} threads, "
+                      f"{int(out.sum())} primes)",
+            "one_thread": {"value": round(s1.shape[0] / dt1 / 1e9, 6), "unit": UNIT,
+                           "sample": f"first {s1.shape[0]} elements of {cfg} ({dt1:.2f} s wall, 1 thread)",
+                           "ns_per_element": round(dt1 / s1.shape[0] * 1e9, 1)}}
+
+
+def config_block(cfg, mode, world):
+    n = workloads.CONFIGS[cfg][1]
+    sc = scaling_of(cfg, mode)
+    if cfg == "C4":
+        par = f"dp{world}: value-range split, rank r classifies the iota [floor(r 2^32/W), floor((r+1) 2^32/W))"
+    elif sc == "weak":
+        par = f"dp{world}: weak, rank r classifies generator indices [r n, (r+1) n), no collective"
+    else:
+        par = f"dp{world}: strong, contiguous split [floor(r n/W), floor((r+1) n/W)) of the fixed array"
+    return {"workload": f"{cfg}: {workloads.CONFIGS[cfg][2]} (BASELINE.json configs[{int(cfg[1]) - 1}])",
+            "n_per_rank": n if sc == "weak" else n // world, "global_n": global_units(cfg, mode, world),
+            "parallelism": par,
+            "l2": ("flushed between steps (512 MB write outside per-step CUDA events)" if l2_flush_needed(n // world)
+                   else "no flush: inputs larger than L2 (%.2f GiB per rank per step)" % (n * 8 / world / 2**30))}
 
 
 def run_reference(args, rank, world):
@@ -326,19 +426,48 @@ def run_reference(args, rank, world):
     line = {
         "impl": "reference", "metric": METRIC, "value": round(value, 6), "unit": UNIT, "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(dt * 1e3, 3), "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "u64", "data": "synthetic",
-        "config": config_block(cfg, world),
+        "scaling": scaling_of(cfg, args.scaling), "vs_baseline": None, "dtype": "u64", "data": "synthetic",
+        "config": config_block(cfg, args.scaling, 1),
         "cpu_baseline": {"value": round(value, 6), "unit": UNIT, "cores": threads, "kind": "oracle",
-                         "sample": f"first {sample_n} elements of {cfg} per step"},
+                         "cpu_model": cpu_model(),
+                         "sample": f"first {sample_n} elements of {cfg} per step, on rank 0's host only"},
         "e2e": {"value": round(value, 6), "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
 
 
+def measure_config(isp, torch, dev, stream, dist, rank, world, cfg, mode, steps, warmup, counts, weak_counts,
+                   profile=True, peaks=None, peaks_kind=None, clocks=None):
+    """One configuration in one scaling mode across all ranks: value (max over
+    ranks), correctness of the NCCL-summed count, and (optionally) the
+    instrumented pass with the roofline of the dominant kernel (rank-local)."""
+    dN, _, (kind, a, b) = make_input(cfg, mode, rank, world, torch, dev)
+    n = b - a
+    dout = torch.empty(n, dtype=torch.uint8, device=dev)
+    flush = l2_flush_needed(n)
+    csteps = max(steps, 100) if cfg == "C1" else steps
+    ms, launches = time_steps(isp, torch, dN, dout, n, csteps, warmup, stream, dist, flush=flush)
+    mine, total = count_total(isp, torch, dout, n, stream, dist)
+    exp = expected_total(cfg, mode, world, counts, weak_counts)
+    units = global_units(cfg, mode, world)
+    res = {"value": round(units / (ms * 1e-3) / 1e9, 4), "unit": UNIT, "ms_per_step": round(ms, 4),
+           "scaling": scaling_of(cfg, mode), "n_per_rank": n, "global_n": units,
+           "correct": (total == exp) if exp is not None else None, "prime_count_total": total,
+           "gpu_launches_per_step": launches / csteps,
+           "l2": "flushed between steps" if flush else "no flush: inputs larger than L2"}
+    if profile:
+        ckm, cst, _ = kernel_profile(isp, torch, dN, dout, n, csteps, stream)
+        res["kernels_ms_per_step"] = {k: round(v, 4) for k, v in ckm.items()}
+        res["roofline"] = roofline(ckm, cst, n, csteps, peaks, peaks_kind, clocks, cfg)
+    del dN, dout
+    torch.cuda.empty_cache()
+    return res
+
+
 def witness_option(isp, torch, dev, stream, args, counts, mode, cfgs):
     """Another exact witness mode on the same workloads with the same timing;
     the headline above is the paper's Eq 4 method.  mode 1: Baillie-PSW (a
-    strong Lucas test replaces the six remaining Eq 4 bases for n >= 2^49, the
+    strong Lucas test replaces the six remaining Eq 4 bases for n >= 2^51, the
     paper's proposed next step); mode 2: reduced witness sets
     by magnitude (base 2 + one hashed base below 2^32,
     Jaeschke's four bases below 1,122,004,669,633)."""
@@ -346,20 +475,9 @@ def witness_option(isp, torch, dev, stream, args, counts, mode, cfgs):
     isp.set_option("witness", mode)
     try:
         for c in cfgs:
-            cn = workloads.CONFIGS[c][1]
-            cN, _ = make_input(c, 0, torch, dev)
-            cout = torch.empty(cn, dtype=torch.uint8, device=dev)
-            if l2_flush_needed(cn):
-                cms, _ = time_steps_flushed(isp, torch, cN, cout, cn, args.steps, args.warmup, stream)
-            else:
-                cms, _ = time_steps(isp, torch, cN, cout, cn, args.steps, args.warmup, stream, None)
-            dcount = torch.zeros(1, dtype=torch.int64, device=dev)
-            isp.isprime_popcount_device(cout, dcount, cn, stream)
-            torch.cuda.synchronize()
-            res[c] = {"value": round(cn / (cms * 1e-3) / 1e9, 4), "unit": UNIT, "ms_per_step": round(cms, 4),
-                      "correct": int(dcount.item()) == counts[c]}
-            del cN, cout
-            torch.cuda.empty_cache()
+            r = measure_config(isp, torch, dev, stream, None, 0, 1, c, "weak", args.steps, args.warmup, counts, {},
+                               profile=False)
+            res[c] = {k: r[k] for k in ("value", "unit", "ms_per_step", "correct")}
     finally:
         isp.set_option("witness", 0)
     return res
@@ -394,11 +512,31 @@ def scalar_latency(isp, torch, dev, stream):
     return res
 
 
-def config_block(cfg, world):
-    n = workloads.CONFIGS[cfg][1]
-    return {"workload": f"{cfg}: {workloads.CONFIGS[cfg][2]} (BASELINE.json configs[{int(cfg[1]) - 1}])",
-            "n_per_rank": n, "global_n": n * world, "parallelism": f"dp{world} (contiguous shards, no collective)",
-            "l2": "no flush: inputs larger than L2 (%.2f GiB per step)" % (n * 8 / 2**30)}
+def e2e_run(isp, torch, dev, dist, host, shard, dout, steps):
+    """The same metric through the host C-ABI isprime() on pinned buffers:
+    H2D of the batch and D2H of the result inside the timed region (host wall
+    clock around the synchronous call), max over ranks."""
+    kind, a, b = shard
+    n = b - a
+    if host is None:
+        hN = torch.arange(a, b, dtype=torch.int64).pin_memory()
+    else:
+        hN = torch.from_numpy(host.view(np.int64)).pin_memory()
+    hout = torch.empty(n, dtype=torch.uint8).pin_memory()
+    isp.isprime_into(hN, hout)
+    torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    t0 = time.perf_counter()
+    esteps = max(1, min(steps, 5))
+    for _ in range(esteps):
+        isp.isprime_into(hN, hout)
+    et = torch.tensor([(time.perf_counter() - t0) / esteps], dtype=torch.float64, device=dev)
+    if dist:
+        dist.all_reduce(et, op=dist.ReduceOp.MAX)
+    matches = bool(np.array_equal(hout.numpy(), dout.cpu().numpy()))
+    del hN, hout
+    return float(et.item()), matches, n
 
 
 def main():
@@ -407,10 +545,15 @@ def main():
     ap.add_argument("--steps", type=int, default=40)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--config", default="C5", choices=sorted(workloads.CONFIGS))
+    ap.add_argument("--scaling", default="weak", choices=["weak", "strong"],
+                    help="weak: every rank a full batch; strong: the fixed array split across ranks "
+                         "(C4 is always split by value range)")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-per-config", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-extras", action="store_true", help="skip scalar latency and witness-option lines")
     ap.add_argument("--cpu-sample", type=int, default=1 << 24)
+    ap.add_argument("--cpu-sample1", type=int, default=1 << 20)
     ap.add_argument("--ref-sample", type=int, default=1 << 22)
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
@@ -436,111 +579,80 @@ def main():
     stream = torch.cuda.current_stream()
     peaks, peaks_kind = measured_peaks()
     counts = load_counts()
+    weak_counts = load_weak_counts()
 
-    cfg = args.config
-    n = workloads.CONFIGS[cfg][1]
-    dN, host = make_input(cfg, rank, torch, dev)
+    cfg, mode = args.config, args.scaling
+    dN, host, shard = make_input(cfg, mode, rank, world, torch, dev)
+    n = shard[2] - shard[1]
     dout = torch.empty(n, dtype=torch.uint8, device=dev)
+    units = global_units(cfg, mode, world)
 
     sampler = ClockSampler(local)
     sampler.start()
     time.sleep(0.2)
-    ms, launches = time_steps(isp, torch, dN, dout, n, args.steps, args.warmup, stream, dist, sampler)
+    ms_max, launches = time_steps(isp, torch, dN, dout, n, args.steps, args.warmup, stream, dist, sampler,
+                                  flush=l2_flush_needed(n))
     sampler.stop()
     clocks = sampler.summary()
+    value = units / (ms_max * 1e-3) / 1e9
 
-    t = torch.tensor([ms], dtype=torch.float64, device=dev)
-    if dist:
-        dist.all_reduce(t, op=tdist.ReduceOp.MAX)
-    ms_max = float(t.item())
-    value = world * n / (ms_max * 1e-3) / 1e9
-
-    # validation: count per rank -> NCCL sum
-    dcount = torch.zeros(1, dtype=torch.int64, device=dev)
-    isp.isprime_popcount_device(dout, dcount, n, stream)
-    torch.cuda.synchronize()
-    my_count = int(dcount.item())
-    tot = dcount.clone()
-    if dist:
-        dist.all_reduce(tot)
-    total_count = int(tot.item())
-    correct = (my_count == counts[cfg]) if rank == 0 else None
+    # validation: count per rank -> NCCL sum, against the oracle's golden counts
+    my_count, total_count = count_total(isp, torch, dout, n, stream, dist)
+    exp_total = expected_total(cfg, mode, world, counts, weak_counts)
+    # rank 0's own batch has a golden count at W = 1 and in weak scaling (indices [0, n))
+    exp_rank0 = counts[cfg] if (world == 1 or scaling_of(cfg, mode) == "weak") else None
 
     kern_ms, st, inst_ms = kernel_profile(isp, torch, dN, dout, n, args.steps, stream)
     roof = roofline(kern_ms, st, n, args.steps, peaks, peaks_kind, clocks, cfg)
 
     e2e = None
     if not args.no_e2e:
-        if host is None:
-            hN = torch.arange(n, dtype=torch.int64).pin_memory()
-        else:
-            hN = torch.from_numpy(host.view(np.int64)).pin_memory()
-        hout = torch.empty(n, dtype=torch.uint8).pin_memory()
-        for _ in range(1):
-            isp.isprime_into(hN, hout)
-        torch.cuda.synchronize()
-        if dist:
-            dist.barrier()
-        t0 = time.perf_counter()
-        esteps = max(1, min(args.steps, 5))
-        for _ in range(esteps):
-            isp.isprime_into(hN, hout)
-        et = torch.tensor([(time.perf_counter() - t0) / esteps], dtype=torch.float64, device=dev)
-        if dist:
-            dist.all_reduce(et, op=tdist.ReduceOp.MAX)
-        e2e = {"value": round(world * n / float(et.item()) / 1e9, 4), "unit": UNIT,
+        et, matches, _ = e2e_run(isp, torch, dev, dist, host, shard, dout, args.steps)
+        e2e = {"value": round(units / et / 1e9, 4), "unit": UNIT,
                "h2d_bytes_per_step": int(n * 8), "d2h_bytes_per_step": int(n),
-               "ms_per_step": round(float(et.item()) * 1e3, 3),
-               "how": "isprime() host C-ABI on pinned host buffers; host wall clock around the synchronous call",
-               "matches_device": bool(np.array_equal(hout.numpy(), dout.cpu().numpy()))}
-        del hN, hout
+               "ms_per_step": round(et * 1e3, 3),
+               "how": "isprime() host C-ABI on pinned host buffers; host wall clock around the synchronous call, "
+                      "max over ranks; bytes are per rank",
+               "matches_device": matches}
 
     line = {
         "metric": METRIC, "value": round(value, 4), "unit": UNIT, "n_gpus": world, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": round(ms_max, 4), "higher_is_better": True, "scaling": "weak",
-        "vs_baseline": None, "dtype": "u64", "data": "synthetic (seeded generator, SURVEY.md 8(d))",
-        "config": config_block(cfg, world),
+        "warmup": args.warmup, "ms_per_step": round(ms_max, 4), "higher_is_better": True,
+        "scaling": scaling_of(cfg, mode), "vs_baseline": None, "dtype": "u64",
+        "data": "synthetic (seeded generator, SURVEY.md 8(d))",
+        "config": config_block(cfg, mode, world),
         "roofline": roof, "e2e": e2e, "gpu_launches": int(launches), "clocks": clocks,
         "kernels_ms_per_step": {k: round(v, 4) for k, v in kern_ms.items()},
         "instrumented_ms_per_step": round(inst_ms, 4),
-        "prime_count": {"rank0": my_count, "total": total_count, "expected_rank0": counts[cfg], "correct": correct},
+        "prime_count": {"rank0": my_count, "total": total_count, "expected_total": exp_total,
+                        "correct": (total_count == exp_total) if exp_total is not None else None,
+                        "rank0_correct": (my_count == exp_rank0) if exp_rank0 is not None else None},
         "stats_per_step": {k: (v / args.steps if isinstance(v, int) else [x / args.steps for x in v])
                            for k, v in st.items() if k not in ("window_lo", "window_hi", "kernel_launches")},
     }
     del dN, dout
     torch.cuda.empty_cache()
 
+    if not args.no_per_config:
+        per = {}
+        for c in ("C1", "C2", "C3", "C4", "C5"):
+            if c == cfg:
+                continue
+            per[c] = measure_config(isp, torch, dev, stream, dist, rank, world, c, mode, args.steps, args.warmup,
+                                    counts, weak_counts, True, peaks, peaks_kind, clocks)
+        line["per_config"] = per
+        if world > 1:
+            other = "strong" if mode == "weak" else "weak"
+            line[f"per_config_{other}"] = {
+                c: measure_config(isp, torch, dev, stream, dist, rank, world, c, other, args.steps, args.warmup,
+                                  counts, weak_counts, False)
+                for c in ("C1", "C2", "C3", "C5")}
     if rank == 0 and world == 1:
-        line["cpu_baseline"] = cpu_baseline_run(cfg, host, min(n, args.cpu_sample))
-        if not args.no_per_config:
-            per = {}
-            for c in ("C1", "C2", "C3", "C4"):
-                if c == cfg:
-                    continue
-                cn = workloads.CONFIGS[c][1]
-                cN, _ = make_input(c, 0, torch, dev)
-                cout = torch.empty(cn, dtype=torch.uint8, device=dev)
-                csteps = args.steps if c != "C1" else max(args.steps, 100)
-                flushed = l2_flush_needed(cn)
-                if flushed:
-                    cms, cl = time_steps_flushed(isp, torch, cN, cout, cn, csteps, args.warmup, stream)
-                else:
-                    cms, cl = time_steps(isp, torch, cN, cout, cn, csteps, args.warmup, stream, None)
-                isp.isprime_popcount_device(cout, dcount, cn, stream)
-                torch.cuda.synchronize()
-                ckm, cst, _ = kernel_profile(isp, torch, cN, cout, cn, csteps, stream)
-                croof = roofline(ckm, cst, cn, csteps, peaks, peaks_kind, clocks, c)
-                per[c] = {"value": round(cn / (cms * 1e-3) / 1e9, 4), "unit": UNIT, "ms_per_step": round(cms, 4),
-                          "n": cn, "correct": int(dcount.item()) == counts[c], "gpu_launches_per_step": cl / csteps,
-                          "l2": ("flushed between steps (512 MB write outside per-step CUDA events)" if flushed
-                                 else "no flush: inputs larger than L2"),
-                          "kernels_ms_per_step": {k: round(v, 4) for k, v in ckm.items()}, "roofline": croof}
-                del cN, cout
-                torch.cuda.empty_cache()
-            line["per_config"] = per
-        line["scalar_latency"] = scalar_latency(isp, torch, dev, stream)
-        line["witness_bpsw"] = witness_option(isp, torch, dev, stream, args, counts, 1, ("C5", "C3"))
-        line["witness_reduced"] = witness_option(isp, torch, dev, stream, args, counts, 2, ("C5", "C2"))
+        line["cpu_baseline"] = cpu_baseline_run(cfg, host, min(n, args.cpu_sample), min(n, args.cpu_sample1))
+        if not args.no_extras:
+            line["scalar_latency"] = scalar_latency(isp, torch, dev, stream)
+            line["witness_bpsw"] = witness_option(isp, torch, dev, stream, args, counts, 1, ("C5", "C3"))
+            line["witness_reduced"] = witness_option(isp, torch, dev, stream, args, counts, 2, ("C5", "C2"))
     if rank == 0:
         print(json.dumps(line), flush=True)
     if dist:

@@ -109,7 +109,7 @@ void isprime_shutdown(void);
  * "small_max"        arrays with n <= small_max (default 131072) and force_path 0
  *                    take one fused launch (trial division + Miller-Rabin per
  *                    element) instead of the plan / sieve / queue pipeline;
- *                    0 disables it.  Never changes a bit of out.
+ *                    0 disables it; accepted in 0..2^32-1.  Never changes a bit of out.
  * "warp_max"         within the short-array path, n <= warp_max (default 4096)
  *                    runs one warp per element with one Eq 4 base per lane
  *                    (latency of one exponentiation instead of seven)

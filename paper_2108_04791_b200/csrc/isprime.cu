@@ -404,7 +404,7 @@ int device_impl(Ctx* c, const unsigned long long* dN, uint8_t* dout, size_t n, c
         td.sq32 = sq > 0xFFFFFFFFull ? 0xFFFFFFFFu : (uint32_t)sq;
         td.rnd = 6755399441055744.0;  // 1.5 * 2^52
     }
-    if ((long long)n <= g_opt.small_max && g_opt.force_path == 0) {
+    if ((long long)n <= g_opt.small_max && n <= 0xFFFFFFFFull && g_opt.force_path == 0) {
         // short array: one fused launch (small_kernel), latency instead of pipeline stages
         const uint32_t len = (uint32_t)n;
         {
@@ -669,7 +669,7 @@ int isprime_set_option(const char* key, long long v) {
     else if (!strcmp(key, "mr2_group")) { if (v != 3 && v != 6) return ISP_EINVAL; g_opt.mr2_group = (int)v; }
     else if (!strcmp(key, "pdl")) { if (v < 0 || v > 1) return ISP_EINVAL; g_opt.pdl = (int)v; }
     else if (!strcmp(key, "sieve_cache")) { if (v < 0 || v > 1) return ISP_EINVAL; g_opt.sieve_cache = (int)v; }
-    else if (!strcmp(key, "small_max")) { if (v < 0) return ISP_EINVAL; g_opt.small_max = v; }
+    else if (!strcmp(key, "small_max")) { if (v < 0 || v > 0xFFFFFFFFll) return ISP_EINVAL; g_opt.small_max = v; }
     else if (!strcmp(key, "warp_max")) { if (v < 0 || v > (1 << 26)) return ISP_EINVAL; g_opt.warp_max = v; }
     else if (!strcmp(key, "witness")) { if (v < 0 || v > 2) return ISP_EINVAL; g_opt.witness = (int)v; }
     else return ISP_EINVAL;

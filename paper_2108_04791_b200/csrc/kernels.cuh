@@ -536,6 +536,11 @@ __global__ void __launch_bounds__(PLAN_THREADS) plan_kernel(const unsigned long 
         plan->valid_hi = whi;
         plan->sieve_runs += 1;
         plan->sieved_ints += whi - wlo;
+    } else if (whi > wlo) {
+        // inside the held bitmap: classify indexes the bitmap from plan->wlo,
+        // so publish the window the bitmap was sieved for, not the sub-range
+        wlo = vlo;
+        whi = vhi;
     }
     plan->wlo = wlo;
     plan->whi = whi;
@@ -754,7 +759,7 @@ dense_kernel(DevPlan* __restrict__ plan, const unsigned long long* __restrict__ 
             const unsigned long long a1 = a0 < ihi ? a0 + ((ihi - a0) & ~1ull) : a0;
             for (unsigned long long i = ilo + ctid; i < (a0 < ihi ? a0 : ihi); i += NC)
                 out[i] = (uint8_t)one(i, N[i]);
-            for (unsigned long long i = (a1 > a0 ? a1 : ihi) + ctid; i < ihi; i += NC)
+            for (unsigned long long i = (a0 < ihi ? a1 : ihi) + ctid; i < ihi; i += NC)
                 out[i] = (uint8_t)one(i, N[i]);
             constexpr int U = 8;
             for (unsigned long long bb = a0; bb < a1; bb += 2ull * NC * U) {
@@ -769,11 +774,13 @@ dense_kernel(DevPlan* __restrict__ plan, const unsigned long long* __restrict__ 
                     const unsigned long long i = bb + 2ull * (ctid + NC * j);
                     if (i < a1) {
                         // pair (i, i + 1) holds n0 + i and n0 + i + 1: one odd value, whose byte
-                        // index is (n0 + i - seg_lo) >> 1 either way, and one even (prime iff 2)
+                        // index is (n0 + i - seg_lo) >> 1 either way, and one even (prime iff 2:
+                        // the low element when n0 is even, the high one -- e0 = 1 -- when odd)
                         const unsigned long long e0 = n0 + i;
                         fail |= (t[j].x != e0) | (t[j].y != e0 + 1);
                         const uint32_t byte = seg[(uint32_t)(e0 - seg_lo) >> 1];
-                        const uint32_t r = odd0 ? byte : ((uint32_t)(e0 == 2ull) | (byte << 8));
+                        const uint32_t r = odd0 ? (byte | ((uint32_t)(e0 == 1ull) << 8))
+                                                : ((uint32_t)(e0 == 2ull) | (byte << 8));
                         __stcs(reinterpret_cast<unsigned short*>(out + i), (unsigned short)r);
                     }
                 }

@@ -24,6 +24,15 @@ def weak_shard(rank: int, world: int, n_per_rank: int) -> tuple[int, int]:
     return rank * n_per_rank, (rank + 1) * n_per_rank
 
 
+def value_range_shard(rank: int, world: int, lo: int, hi: int) -> tuple[int, int]:
+    """[a, b) of the VALUE range [lo, hi) owned by `rank` when a dense range
+    N = lo, lo+1, ..., hi-1 is split across ranks (config C4):
+    a = lo + floor(r (hi - lo) / W).  Each rank builds its input as a device
+    iota and its plan sieves only its own window [a, b) (2^32 / W values)."""
+    a, b = strong_shard(rank, world, hi - lo)
+    return lo + a, lo + b
+
+
 def reduce_count(count: int, device=None, group=None) -> int:
     """Sum of per-rank prime counts over the process group (validation)."""
     import torch

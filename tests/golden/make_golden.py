@@ -4,6 +4,9 @@ Also checks them against the independent survey values in generator.txt.
 
     python tests/golden/make_golden.py          (C1, C2, C3, C5: about a minute on 8 cores)
     python tests/golden/make_golden.py --c4     (adds pi(2^32) via the plain sieve)
+    python tests/golden/make_golden.py --weak   (writes weak_shard_counts.txt instead: the
+        prime count of generator indices [r n, (r+1) n) for r < 8, the batch rank r of a
+        weak-scaling bench run classifies; a few minutes on 8 cores)
 """
 import os
 import sys
@@ -17,7 +20,25 @@ import workloads  # noqa: E402
 HERE = os.path.dirname(os.path.abspath(__file__))
 
 
+def weak():
+    with open(os.path.join(HERE, "weak_shard_counts.txt"), "w") as f:
+        f.write("# Prime count of generator indices [r n, (r+1) n) per config and rank r < 8 (weak scaling:\n")
+        f.write("# every rank classifies a full batch).  Written by tests/golden/make_golden.py --weak\n")
+        f.write("# (oracle/ only).  Columns: config rank count\n")
+        for cfg in ("C1", "C2", "C3", "C5"):
+            n = workloads.CONFIGS[cfg][1]
+            for r in range(8):
+                t = time.time()
+                c = int(oracle.isprime(workloads.generate(cfg, start=r * n, count=n)).sum())
+                print(cfg, r, c, f"{time.time() - t:.1f}s", flush=True)
+                f.write(f"{cfg} {r} {c}\n")
+                f.flush()
+
+
 def main():
+    if "--weak" in sys.argv:
+        weak()
+        return
     rows = []
     for cfg in ("C1", "C2", "C3", "C5"):
         t = time.time()

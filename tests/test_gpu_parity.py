@@ -52,7 +52,7 @@ def assert_same(got, exp, N=None):
 def _default_options():
     saved = {k: isp.get_option(k) for k in ("force_path", "bases32", "td_primes32", "td_primes64",
                                              "chunk_log2", "win64", "warp_p", "small_max", "warp_max",
-                                             "witness")}
+                                             "witness", "sieve_cache")}
     yield
     for k, v in saved.items():
         isp.set_option(k, v)
@@ -280,6 +280,20 @@ def test_dense_range_path_and_fallback():
     assert_same(gpu(N), oracle.isprime(N), N)
 
 
+def test_sieve_cache_reuses_held_window():
+    """Option sieve_cache = 1 lets a call reuse the bitmap an earlier call
+    sieved; a later window inside the held one must index the bitmap from
+    the held window's start (plan_kernel publishes the held range)."""
+    isp.set_option("sieve_cache", 1)
+    isp.set_option("small_max", 0)
+    rng = np.random.default_rng(12)
+    first = rng.integers(0, 1 << 22, size=1 << 21, dtype=np.uint64)
+    assert_same(gpu(first), oracle.isprime(first), first)
+    for lo, hi in ((700_000, 710_000), (3_000_001, 3_100_000), (1 << 21, 1 << 22)):
+        N = rng.integers(lo, hi, size=1 << 20, dtype=np.uint64)
+        assert_same(gpu(N), oracle.isprime(N), N)
+
+
 def test_c4_shard_window_bit_exact():
     lo = (1 << 32) - (1 << 22) - 99
     N = np.arange(lo, 1 << 32, dtype=np.uint64)
@@ -321,47 +335,98 @@ def _counts():
 @pytest.mark.parametrize("cfg", ["C1", "C2", "C3", "C5"])
 def test_config_full_size(cfg):
     """Full BASELINE.json size through isprime_count_device (the launch
-    configuration bench.py times): prime count equals the oracle's (stored by
-    tests/golden/make_golden.py) and 65,536 sampled elements equal the oracle."""
+    configuration bench.py times): EVERY element equals the oracle's
+    (PAPER.md:11-20 output definition; the oracle runs on all host cores), and
+    the device count equals the oracle's count stored by
+    tests/golden/make_golden.py."""
     N = workloads.generate(cfg)
     dN = torch.from_numpy(N.view(np.int64)).to(DEV)
-    dout = torch.empty(N.shape[0], dtype=torch.uint8, device=DEV)
+    dout = torch.full((N.shape[0],), 7, dtype=torch.uint8, device=DEV)  # poison
     dcount = torch.zeros(1, dtype=torch.int64, device=DEV)
     isp.isprime_count_device(dN, dout, dcount)
     torch.cuda.synchronize()
     assert int(dcount.item()) == _counts()[cfg]
     got = dout.cpu().numpy()
-    assert int(got.sum()) == _counts()[cfg]
-    rng = np.random.default_rng(5)
-    idx = rng.choice(N.shape[0], size=min(65536, N.shape[0]), replace=False)
-    assert_same(got[idx], oracle.isprime(N[idx]), N[idx])
+    del dN, dout
+    exp = oracle.isprime(N)
+    assert_same(got, exp, N)
+    assert int(exp.sum()) == _counts()[cfg]
     if cfg == "C5":
         assert np.all(got[4095::4096] == 1)          # 2^64 - 59
         assert np.all(got[1023::1024][(np.arange(1023, N.shape[0], 1024) & 4095) != 4095] == 0)  # Chernick
+    torch.cuda.empty_cache()
 
 
-def test_c4_full_dense_range_pi_2_32():
-    """Config C4: N = 0 .. 2^32-1; count = pi(2^32) = 203,280,221 and sampled
-    elements equal the oracle."""
+_SIEVE32 = []
+
+
+def _sieve32():
+    """The oracle's plain sieve of [0, 2^32) (one ~1 min single-thread run),
+    kept for every dense-range comparison of this module."""
+    if not _SIEVE32:
+        _SIEVE32.append(oracle.sieve(1 << 32))
+    return _SIEVE32[0]
+
+
+def _compare_dense(dout, lo, n, step=1 << 28):
+    """dout (device) against the oracle's sieve over [lo, lo + n) (lo + n <=
+    2^32), element by element, copied back in slices."""
+    exp = _sieve32()[lo:lo + n]
+    for s0 in range(0, n, step):
+        s1 = min(n, s0 + step)
+        got = dout[s0:s1].cpu().numpy()
+        bad = np.nonzero(got != exp[s0:s1])[0]
+        if bad.size:
+            first = (bad[:8] + s0).tolist()
+            pytest.fail(f"{bad.size} mismatches in [{s0}, {s1}); first idx {first} "
+                        f"values {[lo + i for i in first]} got {got[bad[:8]].tolist()} "
+                        f"expected {exp[first].tolist()}")
+
+
+def test_c4_full_dense_range_every_element():
+    """Config C4: N = 0 .. 2^32-1 in the launch configuration bench.py times.
+    All 2^32 output bytes equal the oracle's plain sieve of [0, 2^32)
+    (PAPER.md:22), and the count is pi(2^32) = 203,280,221."""
     n = 1 << 32
     dN = torch.arange(n, dtype=torch.int64, device=DEV)
-    dout = torch.empty(n, dtype=torch.uint8, device=DEV)
+    dout = torch.full((n,), 7, dtype=torch.uint8, device=DEV)
     dcount = torch.zeros(1, dtype=torch.int64, device=DEV)
     isp.isprime_count_device(dN, dout, dcount)
     torch.cuda.synchronize()
     assert int(dcount.item()) == 203280221
-    rng = np.random.default_rng(9)
-    idx = np.sort(rng.choice(n, size=65536, replace=False)).astype(np.int64)
-    got = dout[torch.from_numpy(idx).to(DEV)].cpu().numpy()
-    assert_same(got, oracle.isprime(idx.astype(np.uint64)), idx.astype(np.uint64))
-    del dN, dout
+    del dN
+    torch.cuda.empty_cache()
+    assert int(_sieve32().sum(dtype=np.int64)) == 203280221
+    _compare_dense(dout, 0, n)
+    del dout
+    torch.cuda.empty_cache()
+
+
+@pytest.mark.parametrize("lo,n", [(0, 1 << 28), (1, (1 << 28) + 7), (3, 553356671), (0, 552977921),
+                                  (1, (1 << 20) + 3), ((1 << 31) + 1, (1 << 28) + 31)])
+def test_dense_kernel_multi_segment_every_element(lo, n):
+    """dense_kernel over many segments per block (2^28 values = ~1366 odd
+    segments, ~9 per block: both shared buffers, the "buffer empty" hand-over
+    at k >= 2), odd and even starts (the pair path's even element is the high
+    byte when lo is odd: lo = 1 makes out[1] the prime 2), and the lengths
+    whose last segment overlaps the range in one or two elements (the tail
+    loop), written into a poisoned buffer and compared element by element."""
+    dN = torch.arange(lo, lo + n, dtype=torch.int64, device=DEV)
+    dout = torch.full((n,), 7, dtype=torch.uint8, device=DEV)
+    isp.set_option("small_max", 0)
+    isp.isprime_device(dN, dout, n)
+    torch.cuda.synchronize()
+    del dN
+    _compare_dense(dout, lo, n)
+    del dout
     torch.cuda.empty_cache()
 
 
 def test_more_than_2_32_elements():
     """n > 2^32 elements (include/isprime.h: "n may exceed 2^32"): N[i] = i mod
     2^32 for i < 2^32 + 2^20, so the count is pi(2^32) + pi(2^20) = 203,280,221
-    + 82,025, and the elements past 2^32 equal the oracle."""
+    + 82,025, and every element equals the oracle (the first 2^32 the sieve of
+    [0, 2^32), the rest the sieve of [0, 2^20))."""
     n = (1 << 32) + (1 << 20)
     # filled 2^30 elements at a time: one torch kernel over more than 2^32
     # elements wrote zeros past 2^32 here (torch 2.11 arange / bitwise_and)
@@ -378,7 +443,9 @@ def test_more_than_2_32_elements():
     assert int(dcount.item()) == 203280221 + 82025
     tail = dout[1 << 32:].cpu().numpy()
     assert_same(tail, oracle.sieve(1 << 20), np.arange(1 << 20, dtype=np.uint64))
-    del dN, dout
+    del dN
+    _compare_dense(dout, 0, 1 << 32)
+    del dout
     torch.cuda.empty_cache()
 
 
@@ -386,8 +453,8 @@ def test_force_path_equivalence_all_32bit():
     """SPEC.md:392 analogue over the ENTIRE 32-bit domain: sieve path vs
     trial-division + Miller-Rabin path ({2,7,61}) vs Miller-Rabin with the full
     Eq 4 base set vs base 2 + one hashed base (option witness = 2).
-    Exhaustive GPU self-consistency; with the C4 count above it ties the
-    reduced base sets to pi(2^32)."""
+    Every path's output equals the oracle's sieve of [0, 2^32) element by
+    element."""
     step = 1 << 28
     outs = {}
     dN = torch.empty(step, dtype=torch.int64, device=DEV)
@@ -408,6 +475,7 @@ def test_force_path_equivalence_all_32bit():
         assert torch.equal(o["sieve"], o["mr3"]), base
         assert torch.equal(o["sieve"], o["mr7"]), base
         assert torch.equal(o["sieve"], o["mrh"]), base
+        _compare_dense(o["sieve"], base, step)
         total += int(o["sieve"].sum(dtype=torch.int64).item())
     assert total == 203280221
 
