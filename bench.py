@@ -267,9 +267,20 @@ def time_steps(isp, torch, dN, dout, n, steps, warmup, stream, dist, sampler=Non
     if dist is not None:
         dist.barrier()
         t = torch.tensor([ms], dtype=torch.float64, device=dN.device)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms = float(t.item())
+        ms = float(allreduce(dist, t, dist.ReduceOp.MAX).item())
     return ms, launches
+
+
+def allreduce(dist, t, op):
+    """all_reduce through the process group (NCCL on GPU tensors; a gloo group,
+    used only by the functional multi-rank check BENCH_DIST_BACKEND=gloo,
+    reduces a host copy)."""
+    if dist.get_backend() == "gloo":
+        h = t.cpu()
+        dist.all_reduce(h, op=op)
+        return h.to(t.device)
+    dist.all_reduce(t, op=op)
+    return t
 
 
 def count_total(isp, torch, dout, n, stream, dist):
@@ -279,7 +290,7 @@ def count_total(isp, torch, dout, n, stream, dist):
     torch.cuda.synchronize()
     mine = int(dcount.item())
     if dist is not None:
-        dist.all_reduce(dcount)
+        dcount = allreduce(dist, dcount, dist.ReduceOp.SUM)
     return mine, int(dcount.item())
 
 
@@ -533,7 +544,7 @@ def e2e_run(isp, torch, dev, dist, host, shard, dout, steps):
         isp.isprime_into(hN, hout)
     et = torch.tensor([(time.perf_counter() - t0) / esteps], dtype=torch.float64, device=dev)
     if dist:
-        dist.all_reduce(et, op=dist.ReduceOp.MAX)
+        et = allreduce(dist, et, dist.ReduceOp.MAX)
     matches = bool(np.array_equal(hout.numpy(), dout.cpu().numpy()))
     del hN, hout
     return float(et.item()), matches, n
@@ -569,11 +580,20 @@ def main():
     import torch.distributed as tdist
     import paper_2108_04791_b200 as isp
 
+    # BENCH_SAME_DEVICE=1 + BENCH_DIST_BACKEND=gloo: every rank on cuda:0 -- a
+    # functional check of the multi-rank code path on a one-GPU box, never a
+    # measurement (the ranks' kernels then share one GPU)
+    if os.environ.get("BENCH_SAME_DEVICE") == "1":
+        local = 0
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     dist = None
     if world > 1:
-        tdist.init_process_group("nccl", device_id=dev)
+        backend = os.environ.get("BENCH_DIST_BACKEND", "nccl")
+        if backend == "nccl":
+            tdist.init_process_group("nccl", device_id=dev)
+        else:
+            tdist.init_process_group(backend)
         dist = tdist
     isp.load(build_if_missing=False)
     stream = torch.cuda.current_stream()
