@@ -265,34 +265,41 @@ int get_ctx(Ctx** out) {
     return ISP_OK;
 }
 
+// Scratch queues for a chunk: two uint32 arrays of `cap` entries (8 bytes per
+// element of the chunk, kernels.cuh Queues), allocated lazily and kept.
 int ensure_queues(Ctx* c, size_t cap) {
     if (cap <= c->qcap) return ISP_OK;
     if (c->qmem) { CK(cudaFree(c->qmem)); c->qmem = nullptr; c->qcap = 0; }
     cap = (cap + 4095) & ~(size_t)4095;
-    // per entry: q32 4+4, q64 4+8, s32 4+4, s64 4+8, p32 4+4, p64 4+8 = 60 bytes
-    const size_t bytes = cap * 60;
+    const size_t bytes = cap * 8;
     if (cudaMalloc(&c->qmem, bytes) != cudaSuccess) {
         cudaGetLastError();
         g_err = "queue allocation of " + std::to_string(bytes) + " bytes failed";
         return ISP_ENOMEM;
     }
-    unsigned char* p = c->qmem;
-    c->q.q64_val = reinterpret_cast<unsigned long long*>(p); p += cap * 8;
-    c->q.p64_val = reinterpret_cast<unsigned long long*>(p); p += cap * 8;
-    c->q.s64_val = reinterpret_cast<unsigned long long*>(p); p += cap * 8;
-    c->q.s32_idx = reinterpret_cast<uint32_t*>(p); p += cap * 4;
-    c->q.s32_val = reinterpret_cast<uint32_t*>(p); p += cap * 4;
-    c->q.s64_idx = reinterpret_cast<uint32_t*>(p); p += cap * 4;
-    c->q.q32_idx = reinterpret_cast<uint32_t*>(p); p += cap * 4;
-    c->q.q32_val = reinterpret_cast<uint32_t*>(p); p += cap * 4;
-    c->q.q64_idx = reinterpret_cast<uint32_t*>(p); p += cap * 4;
-    c->q.p32_idx = reinterpret_cast<uint32_t*>(p); p += cap * 4;
-    c->q.p32_val = reinterpret_cast<uint32_t*>(p); p += cap * 4;
-    c->q.p64_idx = reinterpret_cast<uint32_t*>(p); p += cap * 4;
+    c->q.q = reinterpret_cast<uint32_t*>(c->qmem);
+    c->q.s = reinterpret_cast<uint32_t*>(c->qmem) + cap;
     c->q.cap = (unsigned int)cap;
     c->qcap = cap;
     return ISP_OK;
 }
+
+#if ISP_CHECKS
+// Checked builds (-DISP_CHECKS=1, tools/build_checked.py): wait for the call
+// and turn a failed device-side bounds check into ISP_ECUDA.
+int check_device(cudaStream_t s) {
+    CK(cudaStreamSynchronize(s));
+    unsigned int id = 0;
+    CK(cudaMemcpyFromSymbol(&id, g_isp_check, sizeof(id)));
+    if (id) {
+        const unsigned int zero = 0;
+        CK(cudaMemcpyToSymbol(g_isp_check, &zero, sizeof(zero)));
+        g_err = "device bounds check " + std::to_string(id) + " failed";
+        return ISP_ECUDA;
+    }
+    return ISP_OK;
+}
+#endif
 
 // Persistent MR grids never need more blocks than the chunk could queue.
 int mr_grid(int full, uint32_t len) {
@@ -342,34 +349,35 @@ void launch_classify(int n32, int n64, int g, cudaStream_t s, const unsigned lon
 }
 
 template <int WIN, int G>
-void launch_mr2_w(Ctx* c, cudaStream_t s, uint8_t* out, int grid, bool full, int cw) {
-    if (full) launch_k(mr2_kernel<WIN, true, G>, grid, MR_THREADS, 0, s, c->plan, c->q, out, cw);
-    else launch_k(mr2_kernel<WIN, false, G>, grid, MR_THREADS, 0, s, c->plan, c->q, out, cw);
+void launch_mr2_w(Ctx* c, cudaStream_t s, const unsigned long long* N, uint8_t* out, uint32_t len, int grid, bool full,
+                  int cw) {
+    if (full) launch_k(mr2_kernel<WIN, true, G>, grid, MR_THREADS, 0, s, c->plan, c->q, N, out, len, cw);
+    else launch_k(mr2_kernel<WIN, false, G>, grid, MR_THREADS, 0, s, c->plan, c->q, N, out, len, cw);
 }
 
-int launch_mr2(Ctx* c, cudaStream_t s, uint8_t* out, int grid) {
+int launch_mr2(Ctx* c, cudaStream_t s, const unsigned long long* N, uint8_t* out, uint32_t len, int grid) {
     const bool full = g_opt.bases32 == 7;
     const int cw = g_opt.kernel_timing;
     const int g = g_opt.mr2_group == 6 ? 6 : 3;
     if (g_opt.witness == 1) {  // Baillie-PSW for the 64-bit Montgomery class
-        if (full) launch_k(mr2_kernel<3, true, 3, 1>, grid, MR_THREADS, 0, s, c->plan, c->q, out, cw);
-        else launch_k(mr2_kernel<3, false, 3, 1>, grid, MR_THREADS, 0, s, c->plan, c->q, out, cw);
+        if (full) launch_k(mr2_kernel<3, true, 3, 1>, grid, MR_THREADS, 0, s, c->plan, c->q, N, out, len, cw);
+        else launch_k(mr2_kernel<3, false, 3, 1>, grid, MR_THREADS, 0, s, c->plan, c->q, N, out, len, cw);
         CKL("mr2_kernel");
         return ISP_OK;
     }
     if (g_opt.witness == 2) {  // reduced witness sets by magnitude
-        if (full) launch_k(mr2_kernel<3, true, 3, 2>, grid, MR_THREADS, 0, s, c->plan, c->q, out, cw);
-        else launch_k(mr2_kernel<3, false, 3, 2>, grid, MR_THREADS, 0, s, c->plan, c->q, out, cw);
+        if (full) launch_k(mr2_kernel<3, true, 3, 2>, grid, MR_THREADS, 0, s, c->plan, c->q, N, out, len, cw);
+        else launch_k(mr2_kernel<3, false, 3, 2>, grid, MR_THREADS, 0, s, c->plan, c->q, N, out, len, cw);
         CKL("mr2_kernel");
         return ISP_OK;
     }
     switch (g_opt.win64 * 10 + g) {
-        case 13: launch_mr2_w<1, 3>(c, s, out, grid, full, cw); break;
-        case 16: launch_mr2_w<1, 6>(c, s, out, grid, full, cw); break;
-        case 23: launch_mr2_w<2, 3>(c, s, out, grid, full, cw); break;
-        case 26: launch_mr2_w<2, 6>(c, s, out, grid, full, cw); break;
-        case 33: launch_mr2_w<3, 3>(c, s, out, grid, full, cw); break;
-        default: launch_mr2_w<3, 6>(c, s, out, grid, full, cw); break;
+        case 13: launch_mr2_w<1, 3>(c, s, N, out, len, grid, full, cw); break;
+        case 16: launch_mr2_w<1, 6>(c, s, N, out, len, grid, full, cw); break;
+        case 23: launch_mr2_w<2, 3>(c, s, N, out, len, grid, full, cw); break;
+        case 26: launch_mr2_w<2, 6>(c, s, N, out, len, grid, full, cw); break;
+        case 33: launch_mr2_w<3, 3>(c, s, N, out, len, grid, full, cw); break;
+        default: launch_mr2_w<3, 6>(c, s, N, out, len, grid, full, cw); break;
     }
     CKL("mr2_kernel");
     return ISP_OK;
@@ -378,6 +386,9 @@ int launch_mr2(Ctx* c, cudaStream_t s, uint8_t* out, int grid) {
 // The whole hot path for dN[0..n) on stream s.  Caller holds g_mu.
 int device_impl(Ctx* c, const unsigned long long* dN, uint8_t* dout, size_t n, cudaStream_t s) {
     size_t chunk = (size_t)1 << g_opt.chunk_log2;
+    // packed queue entries hold the tile number within a classify block in
+    // 13 bits (kernels.cuh QE_MAX_TILES)
+    while (chunk > ((size_t)1 << 16) && (chunk / CLS_TILE + c->grid_cls - 1) / c->grid_cls > QE_MAX_TILES) chunk >>= 1;
     // classify's per-block queue segments need up to one tile of slack per block;
     // when the device cannot hold the queues of a full chunk, halve the chunk
     int rc;
@@ -423,7 +434,11 @@ int device_impl(Ctx* c, const unsigned long long* dN, uint8_t* dout, size_t n, c
         CK(cudaEventRecord(c->last_done, s));
         c->has_last = true;
         c->last_stream = (void*)s;
+#if ISP_CHECKS
+        return check_device(s);
+#else
         return ISP_OK;
+#endif
     }
     for (size_t base = 0; base < n; base += chunk) {
         const uint32_t len = (uint32_t)((n - base) < chunk ? (n - base) : chunk);
@@ -474,15 +489,20 @@ int device_impl(Ctx* c, const unsigned long long* dN, uint8_t* dout, size_t n, c
         }
         {
             KScope ks(K_MR1, s);
-            launch_k(mr1_kernel, mr_grid(c->grid_mr1, len), MR1_THREADS, 0, s, c->plan, c->q, g_opt.kernel_timing);
+            launch_k(mr1_kernel, mr_grid(c->grid_mr1, len), MR1_THREADS, 0, s, c->plan, c->q, N, len,
+                     g_opt.kernel_timing);
             CKL("mr1_kernel");
         }
         {
             KScope ks(K_MR2, s);
-            rc = launch_mr2(c, s, out, mr_grid(c->grid_mr2, len));
+            rc = launch_mr2(c, s, N, out, len, mr_grid(c->grid_mr2, len));
         }
         if (rc != ISP_OK) return rc;
     }
+#if ISP_CHECKS
+    rc = check_device(s);
+    if (rc != ISP_OK) return rc;
+#endif
     CK(cudaEventRecord(c->last_done, s));
     c->has_last = true;
     c->last_stream = (void*)s;
@@ -717,7 +737,7 @@ int isprime_get_stats(isprime_stats* st) {
     st->queued32 = p.total[0] + p.counts[0];
     st->queued64 = p.total[1] + p.counts[1];
     st->passed32 = p.total[2] + p.counts[2];
-    st->passed64 = p.total[3] + p.counts[3] + p.pback;
+    st->passed64 = p.total[3] + p.counts[3] + p.pf;
     st->chunks = p.chunks;
     st->kernel_launches = g_launches;
     for (int k = 0; k < 4; k++) st->mulmods[k] = p.work[k];

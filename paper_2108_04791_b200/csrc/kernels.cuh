@@ -52,30 +52,51 @@ constexpr int MAX_SEG = 4096;                         // classify blocks (queue 
 // are visible.  A no-op when the kernel was launched without the attribute.
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 
+// Device-side bounds checks (build with -DISP_CHECKS=1): a failed check
+// records its id in g_isp_check (the first one wins) and the host turns it
+// into ISP_ECUDA after the call.  compute-sanitizer is not available on the
+// GPU pool, so these stand in for its out-of-bounds reports on the queues,
+// the segments and the output.
+#ifndef ISP_CHECKS
+#define ISP_CHECKS 0
+#endif
+#if ISP_CHECKS
+__device__ unsigned int g_isp_check;
+#define ISP_CHECK(cond, id)                                             \
+    do {                                                                \
+        if (!(cond)) atomicCAS(&::isp::g_isp_check, 0u, (unsigned)(id)); \
+    } while (0)
+#else
+#define ISP_CHECK(cond, id) \
+    do {                    \
+    } while (0)
+#endif
+
 // Device-resident plan and counters (one per device context).
 struct DevPlan {
     unsigned long long wlo, whi;            // window for the current chunk
     unsigned long long valid_lo, valid_hi;  // range the bitmap currently holds
     unsigned int sieve_needed;
-    unsigned int counts[4];                 // Q32, Q64, P32, P64 of the current chunk
-    unsigned int pad;
-    unsigned long long total[4];            // accumulated Q32, Q64, P32, P64
+    // survivors of trial division of the current chunk: [0] bit length <= 32,
+    // [1] above; base-2 strong probable primes: [2] 32-bit class, [3]
+    // Montgomery class (pf: FP64 class)
+    unsigned int counts[4];
+    unsigned int pf;
+    unsigned long long total[4];            // accumulated counts (pf goes to total[3])
     unsigned long long sieve_runs, sieved_ints, chunks;
     // algorithmic modular multiplications (square-and-multiply count of the
     // method), accumulated only when work counting is on:
     // [mr1 32-bit, mr1 64-bit, mr2 32-bit, mr2 64-bit]
     unsigned long long work[4];
     // counting sort of the trial-division survivors by bit length (per chunk)
-    unsigned int bins32[33], bins64[65], cur32[33], cur64[65];
-    unsigned int sorted32, sorted64;
-    unsigned int pback;                     // FP64-class entries of P64 (stored from the back)
+    unsigned int bins[65], cur[65];
     unsigned int cur1[3], cur2[3];          // dynamic work cursors of mr1 / mr2 (3 regions)
     unsigned long long work_f[2];           // FP64-class mulmods: mr1, mr2 (work counting)
     unsigned int dense, dense_fail;         // chunk is N[i] = dense_base + i below 2^32 (dense_kernel path)
     unsigned long long dense_base;
     // classify writes survivors into per-block segments (no block barrier):
     // entries used by block b of the last classify launch
-    unsigned int seg32[MAX_SEG], seg64[MAX_SEG];
+    unsigned int seg[MAX_SEG];
 };
 
 // Host -> plan kernel parameters (cost model in picoseconds on a full GPU).
@@ -89,15 +110,22 @@ struct PlanParams {
     int invalidate;            // 1: forget the bitmap held from an earlier call (first chunk of a call)
 };
 
+// Scratch queues of a chunk, 8 bytes per element in all (isprime.cu
+// ensure_queues): classify -> q (packed entries in per-block segments) ->
+// sort -> s (chunk indices ordered by bit length) -> mr1 -> q again (P: the
+// base-2 strong probable primes, indices only; q is dead after the sort) ->
+// mr2.  Values are re-read from N by index (the chunk's own input), so no
+// queue holds a 64-bit value.
+//   packed entry: bits 0..12 offset in the classify tile, 13..25 tile number
+//   within the block (tile = block + k * grid), 26..31 bit length - 1
 struct Queues {
-    uint32_t* q32_idx; uint32_t* q32_val;             // classify -> (sort) -> mr1
-    uint32_t* q64_idx; unsigned long long* q64_val;
-    uint32_t* s32_idx; uint32_t* s32_val;             // the same entries ordered by bit length
-    uint32_t* s64_idx; unsigned long long* s64_val;
-    uint32_t* p32_idx; uint32_t* p32_val;             // base-2 strong probable primes -> mr2
-    uint32_t* p64_idx; unsigned long long* p64_val;   // Montgomery class from the front, FP64 class from the back
-    unsigned int cap;                                  // entries per queue
+    uint32_t* q;
+    uint32_t* s;
+    unsigned int cap;                                  // entries per array
 };
+constexpr int QE_TILE_BITS = 13;                      // CLS_TILE = 2^13
+constexpr uint32_t QE_MAX_TILES = 1u << 13;           // tiles per classify block
+static_assert(CLS_TILE == (1 << QE_TILE_BITS), "packed queue entry: tile offset field");
 
 struct TDParams {
     int n32, n64;              // primes used for the 32-bit / 64-bit classes
@@ -365,8 +393,7 @@ __global__ void __launch_bounds__(PLAN_THREADS) plan_kernel(const unsigned long 
     if (tid == 0) { in_valid = 0; nsamp_small = 0; s_notdense = 0; }
     // per-chunk resets of the sort bins and work cursors (read only by the
     // kernels after this one), spread over the block
-    if (tid < 33) { plan->bins32[tid] = 0; plan->cur32[tid] = 0; }
-    if (tid >= 64 && tid < 64 + 65) { plan->bins64[tid - 64] = 0; plan->cur64[tid - 64] = 0; }
+    if (tid < 65) { plan->bins[tid] = 0; plan->cur[tid] = 0; }
     if (tid >= 160 && tid < 163) { plan->cur1[tid - 160] = 0; plan->cur2[tid - 160] = 0; }
     __syncthreads();
     const unsigned long long n0 = len ? N[0] : 0ull;  // a dense range is N[i] = n0 + i
@@ -546,9 +573,8 @@ __global__ void __launch_bounds__(PLAN_THREADS) plan_kernel(const unsigned long 
     plan->whi = whi;
     plan->sieve_needed = need;
     for (int q = 0; q < 4; q++) { plan->total[q] += plan->counts[q]; plan->counts[q] = 0; }
-    plan->sorted32 = plan->sorted64 = 0;
-    plan->total[3] += plan->pback;  // FP64-class base-2 passes count with the 64-bit ones
-    plan->pback = 0;
+    plan->total[3] += plan->pf;  // FP64-class base-2 passes count with the 64-bit ones
+    plan->pf = 0;
     plan->chunks += 1;
 }
 
@@ -751,6 +777,7 @@ dense_kernel(DevPlan* __restrict__ plan, const unsigned long long* __restrict__ 
             const unsigned long long ilo = seg_lo > n0 ? seg_lo - n0 : 0ull;
             const unsigned long long ihi = seg_hi - n0 < len ? seg_hi - n0 : (unsigned long long)len;
             auto one = [&](unsigned long long i, unsigned long long v) -> uint32_t {
+                ISP_CHECK(i < len && i >= ilo && i < ihi, 501);
                 if (v != n0 + i) { fail = true; return 0u; }
                 return (v & 1ull) ? seg[(uint32_t)(v - seg_lo) >> 1] : (uint32_t)(v == 2ull);
             };
@@ -777,6 +804,7 @@ dense_kernel(DevPlan* __restrict__ plan, const unsigned long long* __restrict__ 
                         // index is (n0 + i - seg_lo) >> 1 either way, and one even (prime iff 2:
                         // the low element when n0 is even, the high one -- e0 = 1 -- when odd)
                         const unsigned long long e0 = n0 + i;
+                        ISP_CHECK(i + 1 < ihi && i >= ilo && ((e0 - seg_lo) >> 1) < seg_len, 502);
                         fail |= (t[j].x != e0) | (t[j].y != e0 + 1);
                         const uint32_t byte = seg[(uint32_t)(e0 - seg_lo) >> 1];
                         const uint32_t r = odd0 ? (byte | ((uint32_t)(e0 == 1ull) << 8))
@@ -821,8 +849,8 @@ struct ClsWarp {
 };
 struct ClsSmem {
     ClsWarp w[CLS_THREADS / 32];
-    unsigned int cur[2];            // entries used in this block's Q32 / Q64 segment
-    unsigned int h32[33], h64[65];  // bit-length histogram of this block's survivors (for the sort)
+    unsigned int cur;     // entries used in this block's queue segment
+    unsigned int h[65];   // bit-length histogram of this block's survivors (for the sort)
 };
 
 template <int N32, int N64>
@@ -846,10 +874,11 @@ classify_kernel(const unsigned long long* __restrict__ N, uint8_t* __restrict__ 
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
     ClsWarp& ws = sm.w[wid];
     const uint32_t ntiles = (len + CLS_TILE - 1) / CLS_TILE;
-    for (int b = tid; b < 65; b += CLS_THREADS) { sm.h64[b] = 0; if (b < 33) sm.h32[b] = 0; }
-    if (tid < 2) sm.cur[tid] = 0;
+    for (int b = tid; b < 65; b += CLS_THREADS) sm.h[b] = 0;
+    if (tid == 0) sm.cur = 0;
     __syncthreads();
-    for (uint32_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    uint32_t tk = 0;  // tile number within this block (packed queue entries)
+    for (uint32_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, tk++) {
         const uint32_t wbase = tile * CLS_TILE + 256u * wid;
         const bool full = wbase + 256u <= len;
         // ---- load, trivial cases, window gather, class
@@ -1031,40 +1060,40 @@ classify_kernel(const unsigned long long* __restrict__ N, uint8_t* __restrict__ 
         }
         }  // !fast
         // ---- queue space from this block's private segment (no block barrier):
-        // block b owns entries [b * seg_stride, (b + 1) * seg_stride) of Q32 and
-        // Q64; seg_stride >= (tiles of the block) * CLS_TILE, so it never fills
+        // block b owns entries [b * seg_stride, (b + 1) * seg_stride) of q;
+        // seg_stride >= (tiles of the block) * CLS_TILE, so it never fills.
+        // An entry packs the element's offset in the tile, the tile number
+        // within the block and the value's bit length (the sort key); the
+        // value itself is re-read from N by the witness kernels.
         if (s32 | s64) {  // warp-uniform
             __syncwarp();    // ws.surv written by lane 0
-            uint32_t o32 = 0, o64 = 0;
-            if (lane == 0) {
-                o32 = s32 ? atomicAdd(&sm.cur[0], s32) : 0u;
-                o64 = s64 ? atomicAdd(&sm.cur[1], s64) : 0u;
-            }
-            o32 = segbase + __shfl_sync(0xffffffffu, o32, 0);
-            o64 = segbase + __shfl_sync(0xffffffffu, o64, 0);
+            uint32_t o = 0;
+            if (lane == 0) o = atomicAdd(&sm.cur, s32 + s64);
+            o = segbase + __shfl_sync(0xffffffffu, o, 0);
+            const uint32_t tag = (tk << QE_TILE_BITS) | (256u * wid);
             for (uint32_t k0 = 0; k0 < n32; k0 += 32) {
                 const uint32_t m = ws.surv[k0 >> 5];
                 const uint32_t k = k0 + lane;
                 if ((m >> lane) & 1u) {
-                    const uint32_t at = o32 + __popc(m & ((1u << lane) - 1u));
-                    const uint32_t v32 = (uint32_t)ws.val[k];
-                    q.q32_idx[at] = wbase + ws.pos[k];
-                    q.q32_val[at] = v32;
-                    atomicAdd(&sm.h32[32u - __clz(v32)], 1u);
+                    const uint32_t at = o + __popc(m & ((1u << lane) - 1u));
+                    const uint32_t bl = 32u - __clz((uint32_t)ws.val[k]);
+                    ISP_CHECK(at < segbase + seg_stride && at < q.cap, 101);
+                    q.q[at] = (tag + ws.pos[k]) | ((bl - 1u) << 26);
+                    atomicAdd(&sm.h[bl], 1u);
                 }
-                o32 += __popc(m);
+                o += __popc(m);
             }
             for (uint32_t k0 = 0; k0 < n64; k0 += 32) {
                 const uint32_t m = ws.surv[8 + (k0 >> 5)];
                 const uint32_t k = k0 + lane;
                 if ((m >> lane) & 1u) {
-                    const uint32_t at = o64 + __popc(m & ((1u << lane) - 1u));
-                    const unsigned long long v64 = ws.val[255u - k];
-                    q.q64_idx[at] = wbase + ws.pos[255u - k];
-                    q.q64_val[at] = v64;
-                    atomicAdd(&sm.h64[64u - __clzll((long long)v64)], 1u);
+                    const uint32_t at = o + __popc(m & ((1u << lane) - 1u));
+                    const uint32_t bl = 64u - __clzll((long long)ws.val[255u - k]);
+                    ISP_CHECK(at < segbase + seg_stride && at < q.cap, 102);
+                    q.q[at] = (tag + ws.pos[255u - k]) | ((bl - 1u) << 26);
+                    atomicAdd(&sm.h[bl], 1u);
                 }
-                o64 += __popc(m);
+                o += __popc(m);
             }
         }
         // ---- results of a warp that took the list path: shared tile -> out
@@ -1080,25 +1109,27 @@ classify_kernel(const unsigned long long* __restrict__ N, uint8_t* __restrict__ 
         }
     }
     __syncthreads();
-    for (int b = tid; b < 65; b += CLS_THREADS) {
-        if (sm.h64[b]) atomicAdd(&plan->bins64[b], sm.h64[b]);
-        if (b < 33 && sm.h32[b]) atomicAdd(&plan->bins32[b], sm.h32[b]);
-    }
+    for (int b = tid; b < 65; b += CLS_THREADS)
+        if (sm.h[b]) atomicAdd(&plan->bins[b], sm.h[b]);
     if (tid == 0) {
-        plan->seg32[blockIdx.x] = sm.cur[0];
-        plan->seg64[blockIdx.x] = sm.cur[1];
-        if (sm.cur[0]) atomicAdd(&plan->counts[0], sm.cur[0]);
-        if (sm.cur[1]) atomicAdd(&plan->counts[1], sm.cur[1]);
+        unsigned int c32 = 0;
+        for (int b = 0; b <= 32; b++) c32 += sm.h[b];
+        plan->seg[blockIdx.x] = sm.cur;
+        ISP_CHECK(sm.cur <= seg_stride, 103);
+        if (c32) atomicAdd(&plan->counts[0], c32);
+        if (sm.cur - c32) atomicAdd(&plan->counts[1], sm.cur - c32);
     }
 }
 
 // ------------------------------------------------------------- A2b: order by magnitude
-// Counting sort of the survivor queues by bit length (33 keys for Q32, 65 for
-// Q64).  A warp runs the exponent loop as long as its longest element, so on
-// mixed magnitudes (config C5: bit lengths 33..64 in every warp) unsorted
-// queues waste about a quarter of the multiply pipe; sorted, neighbouring
-// lanes carry equal-length exponents.  When the expected gain is small
-// (sort_pays) the same pass only compacts classify's per-block segments.
+// Counting sort of the trial-division survivors by bit length (65 keys).  A
+// warp runs the exponent loop as long as its longest element, so on mixed
+// magnitudes (config C5: bit lengths 2..64 in every warp) unsorted entries
+// waste about a quarter of the multiply pipe; sorted, neighbouring lanes carry
+// equal-length exponents, and the three magnitude classes of the witness
+// kernels (32-bit, FP64, Montgomery) become contiguous regions of s.  The
+// pass also gathers classify's per-block segments densely, and unpacks each
+// entry to its index in the chunk (4 bytes moved per survivor).
 constexpr int SORT_THREADS = 512;
 #ifndef SORT_TILE
 #define SORT_TILE 1024
@@ -1110,85 +1141,42 @@ constexpr int SORT_THREADS = 512;
 __device__ __forceinline__ unsigned int bitlen32(uint32_t v) { return 32u - __clz(v); }
 __device__ __forceinline__ unsigned int bitlen64u(unsigned long long v) { return 64u - __clzll((long long)v); }
 
-// Gather the per-block segments of one queue into a dense array: ordered by
-// bit length (counting sort, when `sort`) or in segment order (compaction).
-// Segment g holds segcnt[g] entries at src[g * stride ...].
-template <typename T, int NB>
-__device__ __forceinline__ void gather_segments(bool sort, const unsigned int* __restrict__ gbins, unsigned int* gcur,
-                                                const unsigned int* __restrict__ segcnt, int nseg, uint32_t stride,
-                                                const uint32_t* __restrict__ src_idx, const T* __restrict__ src_val,
-                                                uint32_t* __restrict__ dst_idx, T* __restrict__ dst_val,
-                                                unsigned int* spre, unsigned int* scnt, unsigned int* sbase,
-                                                unsigned int* spfx, unsigned int* swarp) {
-    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
-    if (sort) {
-        // exclusive prefix of the global bins (every block computes it)
-        if (tid == 0) {
-            unsigned int acc = 0;
-            for (int b = 0; b < NB; b++) { spre[b] = acc; acc += gbins[b]; }
-        }
-        for (int b = tid; b < NB; b += SORT_THREADS) scnt[b] = 0;
-    } else {
-        // exclusive prefix of the segment counts: the dense start of each segment
-        constexpr int PERT = MAX_SEG / SORT_THREADS;
-        unsigned int loc[PERT], sum = 0;
-#pragma unroll
-        for (int j = 0; j < PERT; j++) {
-            const int g = tid * PERT + j;
-            loc[j] = g < nseg ? segcnt[g] : 0u;
-            sum += loc[j];
-        }
-        unsigned int incl = sum;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            const unsigned int y = __shfl_up_sync(0xffffffffu, incl, o);
-            if (lane >= o) incl += y;
-        }
-        if (lane == 31) swarp[wid] = incl;
-        __syncthreads();
-        unsigned int wofs = 0;
-        for (int w = 0; w < wid; w++) wofs += swarp[w];
-        unsigned int acc = wofs + incl - sum;
-#pragma unroll
-        for (int j = 0; j < PERT; j++) {
-            spfx[tid * PERT + j] = acc;
-            acc += loc[j];
-        }
+__global__ void __launch_bounds__(SORT_THREADS) qscatter_kernel(DevPlan* __restrict__ plan, Queues q, int nseg,
+                                                                uint32_t seg_stride) {
+    pdl_wait();
+    constexpr int NB = 65;
+    __shared__ unsigned int spre[NB], scnt[NB], sbase[NB];
+    const unsigned int total = plan->counts[0] + plan->counts[1];
+    if (total == 0) return;  // nothing queued (a dense sieve window)
+    const int tid = threadIdx.x, lane = tid & 31;
+    // exclusive prefix of the global bins (every block computes it)
+    if (tid == 0) {
+        unsigned int acc = 0;
+        for (int b = 0; b < NB; b++) { spre[b] = acc; acc += plan->bins[b]; }
     }
+    for (int b = tid; b < NB; b += SORT_THREADS) scnt[b] = 0;
     __syncthreads();
     constexpr int PER = SORT_TILE / SORT_THREADS;
     // SORT_SPLIT blocks share a segment, taking its tiles in turn
     const int part = blockIdx.x % SORT_SPLIT;
     for (int g = blockIdx.x / SORT_SPLIT; g < nseg; g += gridDim.x / SORT_SPLIT) {
-        const unsigned int count = segcnt[g];
-        const size_t sb = (size_t)g * stride;
+        const unsigned int count = plan->seg[g];
+        const size_t sb = (size_t)g * seg_stride;
         for (unsigned int t0 = part * SORT_TILE; t0 < count; t0 += SORT_SPLIT * SORT_TILE) {
-            uint32_t idx[PER];
-            T val[PER];
+            uint32_t ent[PER];
 #pragma unroll
             for (int k = 0; k < PER; k++) {  // all loads in flight before any use
                 const unsigned int i = t0 + tid + k * SORT_THREADS;
-                idx[k] = i < count ? src_idx[sb + i] : 0u;
-                val[k] = i < count ? src_val[sb + i] : (T)0;
-            }
-            if (!sort) {
-                const unsigned int d0 = spfx[g];
-#pragma unroll
-                for (int k = 0; k < PER; k++) {
-                    const unsigned int i = t0 + tid + k * SORT_THREADS;
-                    if (i < count) { dst_idx[d0 + i] = idx[k]; dst_val[d0 + i] = val[k]; }
-                }
-                continue;
+                ent[k] = i < count ? q.q[sb + i] : 0u;
             }
             unsigned int bin[PER], rank[PER];
 #pragma unroll
             for (int k = 0; k < PER; k++) {
                 const unsigned int i = t0 + tid + k * SORT_THREADS;
-                bin[k] = i < count ? ((sizeof(T) == 8) ? bitlen64u((unsigned long long)val[k]) : bitlen32((uint32_t)val[k]))
-                                   : (unsigned int)NB;  // sentinel: no element
+                bin[k] = i < count ? (ent[k] >> 26) + 1u : (unsigned int)NB;  // sentinel: no element
             }
             // warp-aggregated ranks: one shared atomic per distinct bin in the warp
-            // (same-bin lanes would serialise on one address; C3 sort 0.097 -> 0.091 ms)
+            // (same-bin lanes would serialise on one address)
 #pragma unroll
             for (int k = 0; k < PER; k++) {
                 const unsigned int peers = __match_any_sync(0xffffffffu, bin[k]);
@@ -1199,14 +1187,16 @@ __device__ __forceinline__ void gather_segments(bool sort, const unsigned int* _
             }
             __syncthreads();
             for (int b = tid; b < NB; b += SORT_THREADS)
-                if (scnt[b]) sbase[b] = spre[b] + atomicAdd(&gcur[b], scnt[b]);
+                if (scnt[b]) sbase[b] = spre[b] + atomicAdd(&plan->cur[b], scnt[b]);
             __syncthreads();
 #pragma unroll
             for (int k = 0; k < PER; k++) {
                 if (bin[k] < NB) {
                     const unsigned int pos = sbase[bin[k]] + rank[k];
-                    dst_idx[pos] = idx[k];
-                    dst_val[pos] = val[k];
+                    // tile = segment (classify block) + k * classify grid
+                    const uint32_t tile = (uint32_t)g + ((ent[k] >> QE_TILE_BITS) & (QE_MAX_TILES - 1u)) * (uint32_t)nseg;
+                    ISP_CHECK(pos < total && pos < q.cap, 201);
+                    q.s[pos] = tile * (uint32_t)CLS_TILE + (ent[k] & (uint32_t)(CLS_TILE - 1));
                 }
             }
             __syncthreads();
@@ -1216,123 +1206,43 @@ __device__ __forceinline__ void gather_segments(bool sort, const unsigned int* _
     }
 }
 
-// Sort only when it pays: a warp of unsorted entries runs about as long as the
-// longest exponent present, so the expected SIMT efficiency is mean/max bit
-// length.  Below 0.92 (config C5: ~0.76) the sort wins; config C3 (~0.98) and
-// C2 (~0.97) skip it.
-__device__ __forceinline__ bool sort_pays(const unsigned int* bins, int nb) {
-    unsigned long long cnt = 0, sum = 0;
-    int mx = 0;
-    for (int b = 0; b < nb; b++) {
-        cnt += bins[b];
-        sum += (unsigned long long)bins[b] * b;
-        if (bins[b]) mx = b;
-    }
-    if (cnt < 4096) return false;
-    if ((double)sum < 0.92 * (double)mx * (double)cnt) return true;
-    // both sides of the FP64 / Montgomery boundary (bit length FP_BITS | FP_BITS + 1) present
-    if (nb == 65) {
-        unsigned long long lo = 0;
-        for (int b = 0; b <= FP_BITS; b++) lo += bins[b];
-        if (lo > cnt / 64 && lo < cnt - cnt / 64) return true;
-        // both sides of 2^63 (bit length 63 | 64): the base-2 ladder fuses its
-        // doubling into the reduction only below 2^63, chosen per warp
-        lo = 0;
-        for (int b = 0; b <= 63; b++) lo += bins[b];
-        if (lo > cnt / 64 && lo < cnt - cnt / 64) return true;
-    }
-    return false;
-}
-
-__global__ void __launch_bounds__(SORT_THREADS) qscatter_kernel(DevPlan* __restrict__ plan, Queues q, int nseg,
-                                                                uint32_t seg_stride) {
-    pdl_wait();
-    __shared__ unsigned int spre[65], scnt[65], sbase[65], swarp[SORT_THREADS / 32];
-    __shared__ unsigned int spfx[MAX_SEG];
-    __shared__ unsigned int do32, do64;
-    const unsigned int c32 = plan->counts[0], c64 = plan->counts[1];
-    if (c32 == 0 && c64 == 0) return;  // nothing queued (a dense sieve window)
-    if (threadIdx.x == 0) {
-        do32 = sort_pays(plan->bins32, 33);
-        do64 = sort_pays(plan->bins64, 65);
-        if (blockIdx.x == 0) { plan->sorted32 = do32; plan->sorted64 = do64; }
-    }
-    __syncthreads();
-    if (c32)
-        gather_segments<uint32_t, 33>(do32, plan->bins32, plan->cur32, plan->seg32, nseg, seg_stride, q.q32_idx,
-                                      q.q32_val, q.s32_idx, q.s32_val, spre, scnt, sbase, spfx, swarp);
-    __syncthreads();
-    if (c64)
-        gather_segments<unsigned long long, 65>(do64, plan->bins64, plan->cur64, plan->seg64, nseg, seg_stride,
-                                                q.q64_idx, q.q64_val, q.s64_idx, q.s64_val, spre, scnt, sbase, spfx,
-                                                swarp);
-}
-
 // ------------------------------------------------------------- A3: MR phase 1
-// Warp-aggregated append of (idx, val) when `pred`.
-template <typename T>
-__device__ __forceinline__ void warp_append(bool pred, uint32_t idx, T val, unsigned int* counter,
-                                            uint32_t* qidx, T* qval) {
-    const unsigned int mask = __ballot_sync(0xffffffffu, pred);
-    if (!mask) return;
-    const int lane = threadIdx.x & 31;
-    const int leader = __ffs(mask) - 1;
-    unsigned int base = 0;
-    if (lane == leader) base = atomicAdd(counter, (unsigned int)__popc(mask));
-    base = __shfl_sync(0xffffffffu, base, leader);
-    if (pred) {
-        const unsigned int pos = base + __popc(mask & ((1u << lane) - 1u));
-        qidx[pos] = idx;
-        qval[pos] = val;
-    }
-}
-
 // Per-warp staging buffer in shared memory: appends go to the global queue 32
 // at a time (one atomicAdd per 32 entries instead of one per warp iteration).
-template <typename T>
 struct WarpStage {
     uint32_t idx[64];
-    T val[64];
 };
 
-template <typename T>
-__device__ __forceinline__ void stage_append(bool pred, uint32_t idx, T val, WarpStage<T>& st, unsigned int& n,
-                                             unsigned int* counter, uint32_t* qidx, T* qval, unsigned int rev_cap = 0) {
+__device__ __forceinline__ void stage_append(bool pred, uint32_t idx, WarpStage& st, unsigned int& n,
+                                             unsigned int* counter, uint32_t* qidx, unsigned int limit) {
     const int lane = threadIdx.x & 31;
     const unsigned int mask = __ballot_sync(0xffffffffu, pred);
-    if (pred) {
-        const unsigned int pos = n + __popc(mask & ((1u << lane) - 1u));
-        st.idx[pos] = idx;
-        st.val[pos] = val;
-    }
+    if (pred) st.idx[n + __popc(mask & ((1u << lane) - 1u))] = idx;
     n += __popc(mask);
     __syncwarp();
     if (n >= 32) {
         unsigned int base = 0;
         if (lane == 0) base = atomicAdd(counter, 32u);
         base = __shfl_sync(0xffffffffu, base, 0);
-        const unsigned int at = rev_cap ? rev_cap - 1 - (base + lane) : base + lane;
-        qidx[at] = st.idx[lane];
-        qval[at] = st.val[lane];
+        ISP_CHECK(base + lane < limit, 301);
+        qidx[base + lane] = st.idx[lane];
         __syncwarp();
-        if (lane + 32 < n) { st.idx[lane] = st.idx[lane + 32]; st.val[lane] = st.val[lane + 32]; }
+        if (lane + 32 < n) st.idx[lane] = st.idx[lane + 32];
         n -= 32;
         __syncwarp();
     }
 }
 
-template <typename T>
-__device__ __forceinline__ void stage_flush(WarpStage<T>& st, unsigned int& n, unsigned int* counter, uint32_t* qidx,
-                                            T* qval, unsigned int rev_cap = 0) {
+__device__ __forceinline__ void stage_flush(WarpStage& st, unsigned int& n, unsigned int* counter, uint32_t* qidx,
+                                            unsigned int limit) {
     const int lane = threadIdx.x & 31;
     if (!n) return;
     unsigned int base = 0;
     if (lane == 0) base = atomicAdd(counter, n);
     base = __shfl_sync(0xffffffffu, base, 0);
     if ((unsigned int)lane < n) {
-        const unsigned int at = rev_cap ? rev_cap - 1 - (base + lane) : base + lane;
-        qidx[at] = st.idx[lane];
-        qval[at] = st.val[lane];
+        ISP_CHECK(base + lane < limit, 302);
+        qidx[base + lane] = st.idx[lane];
     }
     n = 0;
     __syncwarp();
@@ -1393,74 +1303,76 @@ __device__ __forceinline__ unsigned int modexp_squarings(unsigned long long d) {
 __device__ __forceinline__ unsigned int modexp_mults(unsigned long long d) { return __popcll(d) - 1; }
 __device__ __forceinline__ unsigned long long odd_part(unsigned long long n) { return (n - 1) >> (__ffsll((long long)(n - 1)) - 1); }
 
+// Entries of the FP64 class (bit length 33 .. FP_BITS, i.e. 2^32 <= n <
+// FP_LIMIT): the middle region of the sorted queue s.
 __device__ __forceinline__ unsigned int fp_class_count(const DevPlan* plan) {
-    if (!plan->sorted64) return 0u;
     unsigned int c = 0;
-    for (int b = 0; b <= FP_BITS; b++) c += plan->bins64[b];  // bit length <= FP_BITS <=> n < FP_LIMIT
+    for (int b = 33; b <= FP_BITS; b++) c += plan->bins[b];
     return c;
 }
 
+// Regions of s (sorted by bit length) and of P (q after the sort):
+//   0: n < 2^32 (32-bit class)   s[0, c32)             P32 at q[0 ...)
+//   1: FP64 class                s[c32, c32 + nf)      PF  at q[c32 ...)
+//   2: Montgomery class          s[c32 + nf, total)    PM  at q[c32 + nf ...)
+// Each P region holds at most its s region's entries, so P fits in q.
 __global__ void __launch_bounds__(MR1_THREADS)
-mr1_kernel(DevPlan* __restrict__ plan, Queues q, int count_work) {
+mr1_kernel(DevPlan* __restrict__ plan, Queues q, const unsigned long long* __restrict__ N, uint32_t len,
+           int count_work) {
     pdl_wait();
-    __shared__ WarpStage<uint32_t> st32[MR1_THREADS / 32];
-    __shared__ WarpStage<unsigned long long> st64i[MR1_THREADS / 32], st64f[MR1_THREADS / 32];
+    __shared__ WarpStage st[3][MR1_THREADS / 32];
     __shared__ unsigned int s_nf;
     if (threadIdx.x == 0) s_nf = fp_class_count(plan);
     __syncthreads();
     const unsigned int c32 = plan->counts[0], c64 = plan->counts[1], nf = s_nf;
-    // dense copies written by qscatter_kernel (ordered by bit length when sorted*)
-    const uint32_t* q32i = q.s32_idx;
-    const uint32_t* q32v = q.s32_val;
-    const uint32_t* q64i = q.s64_idx;
-    const unsigned long long* q64v = q.s64_val;
-    // regions: 0 = Q32, 1 = FP64 class = sorted Q64 [0, nf), 2 = the rest of Q64
     const unsigned int size[3] = {c32, nf, c64 - nf};
+
     unsigned long long w32 = 0, w64 = 0, wf = 0;
     const unsigned int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
     const unsigned int gwarp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     int r = (int)(gwarp % 3u), tried = 0;
-    unsigned int start = 0, n32s = 0, n64i = 0, n64f = 0;
-    unsigned int end = 0;
+    unsigned int start = 0, end = 0, n0 = 0, n1 = 0, n2 = 0;  // staged entries per region
     // base-2 rounds of 32-bit entries are short: whole chunks (div 0); the
     // 64-bit classes shrink their chunks towards the end
     const unsigned int div[3] = {0u, 2u, 2u};
     while (next_chunk(size, plan->cur1, r, tried, start, end, gridDim.x * (MR1_THREADS / 32), div)) {
+        const uint32_t* const sr = q.s + (r == 0 ? 0u : r == 1 ? c32 : c32 + nf);  // region of s
+        // values are gathered from N by index; the next round's index and value
+        // are loaded before this round's ladder (one gather latency per claim)
+        unsigned int i = start + lane;
+        uint32_t idx_n = i < end ? sr[i] : 0u;
+        unsigned long long v_n = i < end ? __ldg(N + idx_n) : 0ull;
+#pragma unroll 1
         for (unsigned int b = start; b < end; b += 32) {
-            const unsigned int i = b + lane;
-            const bool act = i < end;
-            if (r == 0) {
-                bool pass = false;
-                uint32_t n = 0, idx = 0;
-                if (act) {
-                    n = q32v[i];
-                    idx = q32i[i];
-                    pass = CLS32_FP64 ? sprp2_f64(n) : sprp2_32(n);
+            const bool act = b + lane < end;
+            const uint32_t idx = idx_n;
+            const unsigned long long n = v_n;
+            ISP_CHECK(!act || idx < len, 303);
+            i = b + 32u + lane;
+            idx_n = i < end ? sr[i] : 0u;
+            v_n = i < end ? __ldg(N + idx_n) : 0ull;
+            bool pass = false;
+            if (act) {
+                if (r == 0) {
+                    pass = CLS32_FP64 ? sprp2_f64(n) : sprp2_32((uint32_t)n);
                     if (count_work) w32 += modexp_squarings(odd_part(n));
-                }
-                stage_append<uint32_t>(pass, idx, n, st32[wib], n32s, &plan->counts[2], q.p32_idx, q.p32_val);
-            } else {
-                const unsigned int k = r == 1 ? i : nf + i;
-                bool pass = false, fp = false;
-                unsigned long long n = 0;
-                uint32_t idx = 0;
-                if (act) {
-                    n = q64v[k];
-                    idx = q64i[k];
-                    // magnitude-class dispatch: below 2^50 on the FP64 pipe, above with
-                    // 64-bit Montgomery (uniform per region when the queue is sorted)
-                    fp = n < FP_LIMIT;
+                } else {
+                    // magnitude-class dispatch: below 2^51 on the FP64 pipe, above
+                    // with 64-bit Montgomery (uniform per region: s is sorted)
+                    const bool fp = n < FP_LIMIT;
                     pass = fp ? sprp2_f64(n) : sprp2_64(n);
                     if (count_work) { if (fp) wf += modexp_squarings(odd_part(n)); else w64 += modexp_squarings(odd_part(n)); }
                 }
-                stage_append<unsigned long long>(pass && !fp, idx, n, st64i[wib], n64i, &plan->counts[3], q.p64_idx, q.p64_val);
-                stage_append<unsigned long long>(pass && fp, idx, n, st64f[wib], n64f, &plan->pback, q.p64_idx, q.p64_val, q.cap);
             }
+            // r is warp-uniform
+            if (r == 0) stage_append(pass, idx, st[0][wib], n0, &plan->counts[2], q.q, size[0]);
+            else if (r == 1) stage_append(pass, idx, st[1][wib], n1, &plan->pf, q.q + c32, nf);
+            else stage_append(pass, idx, st[2][wib], n2, &plan->counts[3], q.q + c32 + nf, c64 - nf);
         }
     }
-    stage_flush<uint32_t>(st32[wib], n32s, &plan->counts[2], q.p32_idx, q.p32_val);
-    stage_flush<unsigned long long>(st64i[wib], n64i, &plan->counts[3], q.p64_idx, q.p64_val);
-    stage_flush<unsigned long long>(st64f[wib], n64f, &plan->pback, q.p64_idx, q.p64_val, q.cap);
+    stage_flush(st[0][wib], n0, &plan->counts[2], q.q, c32);
+    stage_flush(st[1][wib], n1, &plan->pf, q.q + c32, nf);
+    stage_flush(st[2][wib], n2, &plan->counts[3], q.q + c32 + nf, c64 - nf);
     if (count_work) {
         w32 = warp_sum(w32);
         w64 = warp_sum(w64);
@@ -1476,14 +1388,17 @@ mr1_kernel(DevPlan* __restrict__ plan, Queues q, int count_work) {
 // ------------------------------------------------------------- A4: MR phase 2
 template <int WIN, bool FULL32, int G64, int WIT = 0>
 __global__ void __launch_bounds__(MR_THREADS)
-mr2_kernel(DevPlan* __restrict__ plan, Queues q, uint8_t* __restrict__ out, int count_work) {
+mr2_kernel(DevPlan* __restrict__ plan, Queues q, const unsigned long long* __restrict__ N, uint8_t* __restrict__ out,
+           uint32_t len, int count_work) {
     pdl_wait();
+    const unsigned int nf = fp_class_count(plan);  // (static shared memory is full: per thread, L1 hits)
     // window tables of the lockstep bases in shared memory (transposed per thread)
     constexpr bool SM = G64 * (1 << WIN) <= 24;  // <= 48 KB of static shared memory
     __shared__ unsigned long long s_tab[SM ? G64 * (1 << WIN) * MR_THREADS : 1];
     unsigned long long* st = s_tab + threadIdx.x;
-    // regions: 0 = P32, 1 = FP64 class (back of P64), 2 = Montgomery class (front of P64)
-    const unsigned int size[3] = {plan->counts[2], plan->pback, plan->counts[3]};
+    // regions of P (mr1_kernel): 0 = 32-bit class, 1 = FP64 class, 2 = Montgomery class
+    const unsigned int size[3] = {plan->counts[2], plan->pf, plan->counts[3]};
+    const unsigned int c32 = plan->counts[0];
     unsigned long long w32 = 0, w64 = 0, wf = 0;
     const unsigned int lane = threadIdx.x & 31;
     const unsigned int gwarp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
@@ -1493,11 +1408,16 @@ mr2_kernel(DevPlan* __restrict__ plan, Queues q, uint8_t* __restrict__ out, int 
     unsigned int end = 0;
     const unsigned int div[3] = {1u, 2u, 2u};
     while (next_chunk(size, plan->cur2, r, tried, start, end, nw, div)) {
+        const uint32_t* const pr = q.q + (r == 0 ? 0u : r == 1 ? c32 : c32 + nf);  // region of P
+#pragma unroll 1
         for (unsigned int b = start; b < end; b += 32) {
             const unsigned int i = b + lane;
             if (i >= end) continue;
+            const uint32_t idx = pr[i];
+            ISP_CHECK(idx < len, 401);
+            const unsigned long long nv = __ldg(N + idx);  // value gathered by index (the phase is compute-bound)
             if (r == 0) {
-                const uint32_t n = q.p32_val[i];
+                const uint32_t n = (uint32_t)nv;
                 bool prime;
                 if (WIT == 2 && !FULL32) {  // one hashed base after base 2
                     const unsigned long long a = hash_base32(n);
@@ -1507,21 +1427,20 @@ mr2_kernel(DevPlan* __restrict__ plan, Queues q, uint8_t* __restrict__ out, int 
                                    : sprp_multi_f64<2, 2, WIN, SM, MR_THREADS>(n, c_bases32_red64, reinterpret_cast<double*>(st));
                 else
                     prime = FULL32 ? sprp_multi32<6>(n, c_bases32_full) : sprp_multi32<2>(n, c_bases32_red);
-                if (prime) out[q.p32_idx[i]] = 1;
+                if (prime) out[idx] = 1;
                 if (count_work) {
                     const unsigned long long d = odd_part(n);
                     w32 += (unsigned long long)(FULL32 ? 6 : WIT == 2 ? 1 : 2) * (modexp_squarings(d) + modexp_mults(d));
                 }
             } else {
-                const unsigned int k = r == 1 ? q.cap - 1 - i : i;
-                const unsigned long long n = q.p64_val[k];
+                const unsigned long long n = nv;
                 const bool fp = n < FP_LIMIT;
                 const bool j4 = WIT == 2 && n < kJaeschkeBound4;
                 // WIT 1: Baillie-PSW for the Montgomery class (strong Lucas after the base-2 phase)
                 const bool prime = j4 ? sprp_multi_f64<3, 3, WIN, SM, MR_THREADS>(n, c_bases_j4, reinterpret_cast<double*>(st))
                                  : fp ? sprp_multi_f64<6, G64, WIN, SM, MR_THREADS>(n, c_bases64, reinterpret_cast<double*>(st))
                                       : (WIT == 1 ? slprp64(n) : sprp_multi64<6, G64, WIN, SM, MR_THREADS>(n, c_bases64, st));
-                if (prime) out[q.p64_idx[k]] = 1;
+                if (prime) out[idx] = 1;
                 if (count_work) {
                     const unsigned long long d = odd_part(n);
                     const unsigned long long w = (j4 ? 3ull : 6ull) * (modexp_squarings(d) + modexp_mults(d));

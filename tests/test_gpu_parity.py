@@ -480,6 +480,32 @@ def test_force_path_equivalence_all_32bit():
     assert total == 203280221
 
 
+# ------------------------------------------------------------------ scratch memory
+@pytest.mark.parametrize("cfg", ["C5", "C4"])
+def test_scratch_memory_bound(cfg):
+    """The library's device scratch (queues: 8 bytes per element of a chunk,
+    kernels.cuh Queues; the sieve bitmap; tables) stays below 2x the input's
+    bytes on the headline configurations, measured as the drop in free device
+    memory across a first call after isprime_shutdown()."""
+    n = workloads.CONFIGS[cfg][1]
+    if cfg == "C4":
+        dN = torch.arange(n, dtype=torch.int64, device=DEV)
+    else:
+        dN = torch.from_numpy(workloads.generate(cfg).view(np.int64)).to(DEV)
+    dout = torch.empty(n, dtype=torch.uint8, device=DEV)
+    torch.cuda.synchronize()
+    isp.shutdown()
+    free0 = torch.cuda.mem_get_info()[0]
+    isp.isprime_device(dN, dout)
+    torch.cuda.synchronize()
+    used = free0 - torch.cuda.mem_get_info()[0]
+    assert used <= 2 * 8 * n, (cfg, used, 8 * n)
+    if cfg == "C5":
+        assert used <= 1.25 * 8 * n, (cfg, used, 8 * n)
+    del dN, dout
+    torch.cuda.empty_cache()
+
+
 # ------------------------------------------------------------------ streams and threads
 def test_calls_on_two_streams_and_threads():
     """The library keeps one set of queues per device: a call on another

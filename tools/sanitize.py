@@ -11,9 +11,12 @@ that reports 0 hazards also shows the output it watched was correct.
            148-block dense_kernel, both shared buffers and the k >= 2
            "buffer empty" hand-over), then 3 .. 3 + 2^21 + 1
   pipeline C5 prefix of 2^21 elements: plan, sieve, classify (several tiles
-           per block), qscatter (sorted), mr1, mr2
-  c3       C3 prefix of 2^20 (unsorted queues, Montgomery class only)
+           per block), qscatter, mr1, mr2
+  c3       C3 prefix of 2^20 (Montgomery class only)
   small    short-array path (small_kernel, small_warp_kernel)
+  chunks   several device chunks per call, every witness mode, inputs where
+           every element survives to phase 2 (queues at their worst case)
+  full     C2, C3, C5 at full size
 """
 from __future__ import annotations
 
@@ -62,6 +65,17 @@ def main():
     elif what == "small":
         run(isp, torch, workloads.generate("C5", count=3000))
         run(isp, torch, workloads.generate("C5", count=100_000))
+    elif what == "chunks":  # several device chunks per call, every witness mode, all-prime input
+        N = workloads.generate("C5", count=(1 << 22) + 5)
+        for w in (0, 1, 2):
+            run(isp, torch, N, small_max=0, chunk_log2=20, witness=w)
+        cs = np.array(workloads.chernick_numbers(), dtype=np.uint64)
+        primes = np.array([(1 << 64) - 59, (1 << 61) - 1, 4294967291, (1 << 49) - 81], dtype=np.uint64)
+        run(isp, torch, np.tile(np.concatenate([primes, cs]), 300), small_max=0)
+        run(isp, torch, np.tile(primes, 1 << 18), small_max=0)  # every element survives to phase 2
+    elif what == "full":  # the full-size configurations in the bench's launch configuration
+        for cfg in ("C2", "C3", "C5"):
+            run(isp, torch, workloads.generate(cfg))
     else:
         raise SystemExit(f"unknown workload {what}")
     print("sanitize workload ok", what)
