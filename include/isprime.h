@@ -121,6 +121,11 @@ void isprime_shutdown(void);
  *                    tools/costfit.py (the Fig BestFit analogue).
  *                    Path choice only: never changes a bit of out
  * "warp_p"           sieve: primes below this cross off warp-cooperatively
+ * "sched"            witness-kernel work distribution: 0 dynamic guided claims
+ *                    from an atomic cursor per class; 1 static interleaved
+ *                    rounds of 32 queue entries per warp, no atomics; 2
+ *                    (default) static for the 32-bit class, dynamic for the
+ *                    64-bit classes.  Never changes a bit of out
  * "kernel_timing"    1: bracket every launch with CUDA events on its stream and
  *                    accumulate per-kernel device time (isprime_get_kernel_times)
  * Returns ISP_OK or ISP_EINVAL. */

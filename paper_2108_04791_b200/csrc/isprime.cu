@@ -42,6 +42,8 @@ struct Options {
     int mr2_group = 3;       // 64-bit phase-2 bases run G at a time in lockstep (3 or 6)
     long long small_max = 1 << 17;  // n <= small_max (and force_path auto): one fused launch
     long long warp_max = 4096;      // n <= warp_max: one warp per element (one base per lane)
+    int sched = 2;           // witness kernels: 0 dynamic guided claims (atomics), 1 static interleaved rounds,
+                             // 2 static for the 32-bit class then dynamic for the 64-bit classes
     int witness = 0;         // 0: Eq 4 bases; 1: Baillie-PSW for n >= 2^50; 2: reduced sets by magnitude     // 1: a call may reuse the bitmap sieved by an earlier call
 };
 
@@ -351,8 +353,8 @@ void launch_classify(int n32, int n64, int g, cudaStream_t s, const unsigned lon
 template <int WIN, int G>
 void launch_mr2_w(Ctx* c, cudaStream_t s, const unsigned long long* N, uint8_t* out, uint32_t len, int grid, bool full,
                   int cw) {
-    if (full) launch_k(mr2_kernel<WIN, true, G>, grid, MR_THREADS, 0, s, c->plan, c->q, N, out, len, cw);
-    else launch_k(mr2_kernel<WIN, false, G>, grid, MR_THREADS, 0, s, c->plan, c->q, N, out, len, cw);
+    if (full) launch_k(mr2_kernel<WIN, true, G>, grid, MR_THREADS, 0, s, c->plan, c->q, N, out, len, cw, g_opt.sched);
+    else launch_k(mr2_kernel<WIN, false, G>, grid, MR_THREADS, 0, s, c->plan, c->q, N, out, len, cw, g_opt.sched);
 }
 
 int launch_mr2(Ctx* c, cudaStream_t s, const unsigned long long* N, uint8_t* out, uint32_t len, int grid) {
@@ -360,14 +362,14 @@ int launch_mr2(Ctx* c, cudaStream_t s, const unsigned long long* N, uint8_t* out
     const int cw = g_opt.kernel_timing;
     const int g = g_opt.mr2_group == 6 ? 6 : 3;
     if (g_opt.witness == 1) {  // Baillie-PSW for the 64-bit Montgomery class
-        if (full) launch_k(mr2_kernel<3, true, 3, 1>, grid, MR_THREADS, 0, s, c->plan, c->q, N, out, len, cw);
-        else launch_k(mr2_kernel<3, false, 3, 1>, grid, MR_THREADS, 0, s, c->plan, c->q, N, out, len, cw);
+        if (full) launch_k(mr2_kernel<3, true, 3, 1>, grid, MR_THREADS, 0, s, c->plan, c->q, N, out, len, cw, g_opt.sched);
+        else launch_k(mr2_kernel<3, false, 3, 1>, grid, MR_THREADS, 0, s, c->plan, c->q, N, out, len, cw, g_opt.sched);
         CKL("mr2_kernel");
         return ISP_OK;
     }
     if (g_opt.witness == 2) {  // reduced witness sets by magnitude
-        if (full) launch_k(mr2_kernel<3, true, 3, 2>, grid, MR_THREADS, 0, s, c->plan, c->q, N, out, len, cw);
-        else launch_k(mr2_kernel<3, false, 3, 2>, grid, MR_THREADS, 0, s, c->plan, c->q, N, out, len, cw);
+        if (full) launch_k(mr2_kernel<3, true, 3, 2>, grid, MR_THREADS, 0, s, c->plan, c->q, N, out, len, cw, g_opt.sched);
+        else launch_k(mr2_kernel<3, false, 3, 2>, grid, MR_THREADS, 0, s, c->plan, c->q, N, out, len, cw, g_opt.sched);
         CKL("mr2_kernel");
         return ISP_OK;
     }
@@ -490,7 +492,7 @@ int device_impl(Ctx* c, const unsigned long long* dN, uint8_t* dout, size_t n, c
         {
             KScope ks(K_MR1, s);
             launch_k(mr1_kernel, mr_grid(c->grid_mr1, len), MR1_THREADS, 0, s, c->plan, c->q, N, len,
-                     g_opt.kernel_timing);
+                     g_opt.kernel_timing, g_opt.sched);
             CKL("mr1_kernel");
         }
         {
@@ -692,6 +694,7 @@ int isprime_set_option(const char* key, long long v) {
     else if (!strcmp(key, "small_max")) { if (v < 0 || v > 0xFFFFFFFFll) return ISP_EINVAL; g_opt.small_max = v; }
     else if (!strcmp(key, "warp_max")) { if (v < 0 || v > (1 << 26)) return ISP_EINVAL; g_opt.warp_max = v; }
     else if (!strcmp(key, "witness")) { if (v < 0 || v > 2) return ISP_EINVAL; g_opt.witness = (int)v; }
+    else if (!strcmp(key, "sched")) { if (v < 0 || v > 2) return ISP_EINVAL; g_opt.sched = (int)v; }
     else return ISP_EINVAL;
     return ISP_OK;
 }
@@ -718,6 +721,7 @@ long long isprime_get_option(const char* key) {
     if (!strcmp(key, "small_max")) return g_opt.small_max;
     if (!strcmp(key, "warp_max")) return g_opt.warp_max;
     if (!strcmp(key, "witness")) return g_opt.witness;
+    if (!strcmp(key, "sched")) return g_opt.sched;
     return -1;
 }
 

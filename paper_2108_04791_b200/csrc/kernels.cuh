@@ -1291,6 +1291,52 @@ __device__ __forceinline__ bool next_chunk(const unsigned int (&size)[3], unsign
     return false;
 }
 
+// Work of the witness kernels in either scheduling mode.  Dynamic (sched 0):
+// next_chunk's guided claims, rounds of 32 consecutive entries.  Static
+// (sched 1): every warp takes rounds gw, gw + nw, gw + 2 nw, ... of each
+// region in turn (starting at region gw mod 3) -- no atomics.  The queues are
+// sorted by bit length, so neighbouring rounds cost about the same and the
+// interleaved share of every warp is balanced to within a round.
+__device__ __forceinline__ bool next_work(int sched, const unsigned int (&size)[3], unsigned int* cur, int& r,
+                                          int& tried, unsigned int& start, unsigned int& end, unsigned int& step,
+                                          unsigned int nw, unsigned int gw, const unsigned int (&div)[3]) {
+    if (sched == 2) {
+        // static rounds of region 0 (short, uniform 32-bit entries: claims would
+        // cost an atomic per few hundred cycles of work), then dynamic claims
+        // over the 64-bit regions (long rounds, expensive tails)
+        if (!(tried & 1)) {
+            tried |= 1;
+            if (32u * gw < size[0]) {
+                start = 32u * gw;
+                end = size[0];
+                step = 32u * nw;
+                r = 0;
+                return true;
+            }
+        }
+        if (r == 0) r = 1 + (int)(gw & 1u);
+        step = 32u;
+        return next_chunk(size, cur, r, tried, start, end, nw, div);
+    }
+    if (sched) {
+        while (tried != 7) {
+            if (!((tried >> r) & 1)) {
+                tried |= 1 << r;
+                if (32u * gw < size[r]) {
+                    start = 32u * gw;
+                    end = size[r];
+                    step = 32u * nw;
+                    return true;
+                }
+            }
+            r = r == 2 ? 0 : r + 1;
+        }
+        return false;
+    }
+    step = 32u;
+    return next_chunk(size, cur, r, tried, start, end, nw, div);
+}
+
 __device__ __forceinline__ unsigned long long warp_sum(unsigned long long v) {
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
@@ -1318,7 +1364,7 @@ __device__ __forceinline__ unsigned int fp_class_count(const DevPlan* plan) {
 // Each P region holds at most its s region's entries, so P fits in q.
 __global__ void __launch_bounds__(MR1_THREADS)
 mr1_kernel(DevPlan* __restrict__ plan, Queues q, const unsigned long long* __restrict__ N, uint32_t len,
-           int count_work) {
+           int count_work, int sched) {
     pdl_wait();
     __shared__ WarpStage st[3][MR1_THREADS / 32];
     __shared__ unsigned int s_nf;
@@ -1331,11 +1377,12 @@ mr1_kernel(DevPlan* __restrict__ plan, Queues q, const unsigned long long* __res
     const unsigned int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
     const unsigned int gwarp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     int r = (int)(gwarp % 3u), tried = 0;
-    unsigned int start = 0, end = 0, n0 = 0, n1 = 0, n2 = 0;  // staged entries per region
+    unsigned int start = 0, end = 0, step = 32, n0 = 0, n1 = 0, n2 = 0;  // staged entries per region
     // base-2 rounds of 32-bit entries are short: whole chunks (div 0); the
     // 64-bit classes shrink their chunks towards the end
     const unsigned int div[3] = {0u, 2u, 2u};
-    while (next_chunk(size, plan->cur1, r, tried, start, end, gridDim.x * (MR1_THREADS / 32), div)) {
+    const unsigned int nw = gridDim.x * (MR1_THREADS / 32);
+    while (next_work(sched, size, plan->cur1, r, tried, start, end, step, nw, gwarp, div)) {
         const uint32_t* const sr = q.s + (r == 0 ? 0u : r == 1 ? c32 : c32 + nf);  // region of s
         // values are gathered from N by index; the next round's index and value
         // are loaded before this round's ladder (one gather latency per claim)
@@ -1343,12 +1390,12 @@ mr1_kernel(DevPlan* __restrict__ plan, Queues q, const unsigned long long* __res
         uint32_t idx_n = i < end ? sr[i] : 0u;
         unsigned long long v_n = i < end ? __ldg(N + idx_n) : 0ull;
 #pragma unroll 1
-        for (unsigned int b = start; b < end; b += 32) {
+        for (unsigned int b = start; b < end; b += step) {
             const bool act = b + lane < end;
             const uint32_t idx = idx_n;
             const unsigned long long n = v_n;
             ISP_CHECK(!act || idx < len, 303);
-            i = b + 32u + lane;
+            i = b + step + lane;
             idx_n = i < end ? sr[i] : 0u;
             v_n = i < end ? __ldg(N + idx_n) : 0ull;
             bool pass = false;
@@ -1389,7 +1436,7 @@ mr1_kernel(DevPlan* __restrict__ plan, Queues q, const unsigned long long* __res
 template <int WIN, bool FULL32, int G64, int WIT = 0>
 __global__ void __launch_bounds__(MR_THREADS)
 mr2_kernel(DevPlan* __restrict__ plan, Queues q, const unsigned long long* __restrict__ N, uint8_t* __restrict__ out,
-           uint32_t len, int count_work) {
+           uint32_t len, int count_work, int sched) {
     pdl_wait();
     const unsigned int nf = fp_class_count(plan);  // (static shared memory is full: per thread, L1 hits)
     // window tables of the lockstep bases in shared memory (transposed per thread)
@@ -1405,12 +1452,12 @@ mr2_kernel(DevPlan* __restrict__ plan, Queues q, const unsigned long long* __res
     int r = (int)(gwarp % 3u), tried = 0;
     unsigned int start = 0;
     const unsigned int nw = gridDim.x * (MR_THREADS / 32);  // guided chunk sizes
-    unsigned int end = 0;
+    unsigned int end = 0, step = 32;
     const unsigned int div[3] = {1u, 2u, 2u};
-    while (next_chunk(size, plan->cur2, r, tried, start, end, nw, div)) {
+    while (next_work(sched, size, plan->cur2, r, tried, start, end, step, nw, gwarp, div)) {
         const uint32_t* const pr = q.q + (r == 0 ? 0u : r == 1 ? c32 : c32 + nf);  // region of P
 #pragma unroll 1
-        for (unsigned int b = start; b < end; b += 32) {
+        for (unsigned int b = start; b < end; b += step) {
             const unsigned int i = b + lane;
             if (i >= end) continue;
             const uint32_t idx = pr[i];

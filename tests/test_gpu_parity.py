@@ -52,7 +52,7 @@ def assert_same(got, exp, N=None):
 def _default_options():
     saved = {k: isp.get_option(k) for k in ("force_path", "bases32", "td_primes32", "td_primes64",
                                              "chunk_log2", "win64", "warp_p", "small_max", "warp_max",
-                                             "witness", "sieve_cache")}
+                                             "witness", "sieve_cache", "sched")}
     yield
     for k, v in saved.items():
         isp.set_option(k, v)
@@ -556,7 +556,7 @@ def test_options_do_not_change_results():
     exp = oracle.isprime(N)
     for key, vals in (("td_primes32", (0, 1, 5, 128)), ("td_primes64", (0, 3, 128)), ("win64", (1, 2, 3)),
                       ("force_path", (0, 1, 2)), ("chunk_log2", (16, 17, 28)), ("warp_p", (17, 600, 65536)),
-                      ("witness", (1, 2, 0))):
+                      ("witness", (1, 2, 0)), ("sched", (0, 1, 2))):
         saved = isp.get_option(key)
         for v in vals:
             isp.set_option(key, v)
