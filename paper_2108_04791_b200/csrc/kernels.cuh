@@ -92,7 +92,8 @@ struct DevPlan {
     unsigned int bins[65], cur[65];
     unsigned int cur1[3], cur2[3];          // dynamic work cursors of mr1 / mr2 (3 regions)
     unsigned long long work_f[2];           // FP64-class mulmods: mr1, mr2 (work counting)
-    unsigned int dense, dense_fail;         // chunk is N[i] = dense_base + i below 2^32 (dense_kernel path)
+    unsigned int dense, dense_fail;         // chunk is N[i] = dense_base + dense_d i below 2^32 (dense_kernel path)
+    unsigned int dense_d;                   // stride of the dense range (1 or 2)
     unsigned long long dense_base;
     // classify writes survivors into per-block segments (no block barrier):
     // entries used by block b of the last classify launch
@@ -396,7 +397,8 @@ __global__ void __launch_bounds__(PLAN_THREADS) plan_kernel(const unsigned long 
     if (tid < 65) { plan->bins[tid] = 0; plan->cur[tid] = 0; }
     if (tid >= 160 && tid < 163) { plan->cur1[tid - 160] = 0; plan->cur2[tid - 160] = 0; }
     __syncthreads();
-    const unsigned long long n0 = len ? N[0] : 0ull;  // a dense range is N[i] = n0 + i
+    const unsigned long long n0 = len ? N[0] : 0ull;  // a dense range is N[i] = n0 + ds i
+    const unsigned long long ds = len > 1 ? N[1] - n0 : 1ull;  // its candidate stride (dense_kernel: 1 or 2)
     const unsigned long long vlo = P.invalidate ? 0ull : plan->valid_lo;
     const unsigned long long vhi = P.invalidate ? 0ull : plan->valid_hi;
     const unsigned long long S = len < (unsigned long long)PLAN_SAMPLES ? len : (unsigned long long)PLAN_SAMPLES;
@@ -434,7 +436,7 @@ __global__ void __launch_bounds__(PLAN_THREADS) plan_kernel(const unsigned long 
 #pragma unroll
             for (int e = 0; e < PLAN_RUN; e++) {
                 v[PLAN_RUN * r + e] = (unsigned long long)e < avail ? N[at + e] : 0ull;
-                bad |= (unsigned long long)e < avail && v[PLAN_RUN * r + e] != n0 + at + e;
+                bad |= (unsigned long long)e < avail && v[PLAN_RUN * r + e] != n0 + ds * (at + e);
             }
             if (bad) s_notdense = 1;
         }
@@ -543,16 +545,18 @@ __global__ void __launch_bounds__(PLAN_THREADS) plan_kernel(const unsigned long 
     if (lane != 0) return;
     if (whi > wmax) whi = wmax;
     unsigned int need = 0;
-    // a sampled-dense range of at least 2^20 values below 2^32: dense_kernel
-    // sieves and classifies it in one pass (no global bitmap, no classify)
-    const bool dense = P.force == 0 && !s_notdense && len >= (1ull << 20) && n0 + len <= (1ull << 32) &&
-                       n0 + len <= wmax;
+    // a sampled arithmetic progression of stride 1 or 2 and at least 2^20
+    // values below 2^32: dense_kernel sieves and classifies it in one pass (no
+    // global bitmap, no classify)
+    const bool dense = P.force == 0 && !s_notdense && (ds == 1ull || ds == 2ull) && len >= (1ull << 20) &&
+                       n0 < (1ull << 32) && n0 + ds * (len - 1) < (1ull << 32) && n0 + ds * (len - 1) < wmax;
     plan->dense = dense;
     plan->dense_fail = 0;
     plan->dense_base = n0;
+    plan->dense_d = (unsigned int)(dense ? ds : 1ull);
     if (dense) {
         wlo = n0 & ~63ull;
-        whi = (n0 + len + 63) & ~63ull;
+        whi = (n0 + ds * (len - 1) + 64) & ~63ull;
         if (whi > wmax) whi = wmax;
         plan->valid_lo = plan->valid_hi = 0;  // the global bitmap is not written
         plan->sieve_runs += 1;
@@ -721,38 +725,98 @@ sieve_kernel(const DevPlan* __restrict__ plan, uint32_t* __restrict__ bitmap,
 }
 
 // ------------------------------------------------------------- A1 + A2 fused: dense ranges
-// SURVEY.md 8(f) f4.  When the plan finds the chunk to be a contiguous range
-// N[i] = N0 + i below 2^32 (the paper's incrementing sequences, config C4),
-// each block sieves a segment in shared memory and writes out[i] for the
-// indices whose values the segment covers straight from it -- no global
-// bitmap, no separate classify pass, and the sieving of one block overlaps the
-// streaming of another.  Every element is still read and checked against
-// N0 + i; a mismatch (the plan only samples) sets plan->dense_fail, and the
-// classify kernel then redoes the whole chunk without the window.
-constexpr int DENSE_PRODUCERS = 256;              // warps 0-7 sieve
-constexpr int DENSE_THREADS = 1024;                // warps 8-31 stream
+// SURVEY.md 8(f) f4.  When the plan finds the chunk to be an arithmetic
+// progression N[i] = N0 + D i with D = 1 (the paper's incrementing sequences,
+// config C4) or D = 2 (odd numbers in a restricted range)
+// below 2^32, each block sieves a segment in shared memory and writes out[i]
+// for the indices whose values the segment covers straight from it -- no
+// global bitmap, no separate classify pass, and the sieving of one block
+// overlaps the streaming of another.  Every element is still read and
+// checked against N0 + D i; a mismatch (the plan only samples) sets
+// plan->dense_fail, and the classify kernel then redoes the whole chunk
+// without the window.
+constexpr int DENSE_THREADS = 1024;
+// warps that sieve (the rest stream): stride 1 covers one integer per
+// element, stride 2 two, so the stride-2 range gives the sieve twice the warps
+constexpr int DENSE_PRODUCERS1 = 256;
+constexpr int DENSE_PRODUCERS2 = 512;
+
+// The consumer side for one segment [seg_lo, seg_hi) of stride D: scalar head
+// and tail, element pairs (i, i + 1), i even, with 16-byte loads in between.
+// NC consumer threads.
+template <int D, int NC>
+__device__ __forceinline__ void dense_consume(const uint8_t* seg, unsigned long long seg_lo, unsigned long long seg_hi,
+                                              uint32_t seg_len, unsigned long long n0,
+                                              const unsigned long long* __restrict__ N, uint8_t* __restrict__ out,
+                                              uint32_t len, int vec, int ctid, bool& fail) {
+    // indices whose expected values N0 + D i lie in [seg_lo, seg_hi)
+    const unsigned long long ilo = seg_lo > n0 ? (seg_lo - n0 + D - 1) / D : 0ull;
+    const unsigned long long iend = seg_hi > n0 ? (seg_hi - n0 + D - 1) / D : 0ull;
+    const unsigned long long ihi = iend < len ? iend : (unsigned long long)len;
+    if (ilo >= ihi) return;
+    const bool odd0 = n0 & 1ull;  // parity of n0 + D i for even i (the vector path's pairs)
+    auto one = [&](unsigned long long i, unsigned long long v) -> uint32_t {
+        ISP_CHECK(i < len && i >= ilo && i < ihi, 501);
+        if (v != n0 + D * i) { fail = true; return 0u; }
+        return (v & 1ull) ? seg[(uint32_t)(v - seg_lo) >> 1] : (uint32_t)(v == 2ull);
+    };
+    const unsigned long long a0 = vec ? ((ilo + 1) & ~1ull) : ihi;
+    const unsigned long long a1 = a0 < ihi ? a0 + ((ihi - a0) & ~1ull) : a0;
+    for (unsigned long long i = ilo + ctid; i < (a0 < ihi ? a0 : ihi); i += NC) out[i] = (uint8_t)one(i, N[i]);
+    for (unsigned long long i = (a0 < ihi ? a1 : ihi) + ctid; i < ihi; i += NC) out[i] = (uint8_t)one(i, N[i]);
+    constexpr int U = 8;  // eight pairs per thread in flight
+    for (unsigned long long bb = a0; bb < a1; bb += 2ull * NC * U) {
+        ulonglong2 t[U];
+#pragma unroll
+        for (int j = 0; j < U; j++) {
+            const unsigned long long i = bb + 2ull * (ctid + NC * j);
+            if (i < a1) t[j] = __ldcs(reinterpret_cast<const ulonglong2*>(N + i));
+        }
+#pragma unroll
+        for (int j = 0; j < U; j++) {
+            const unsigned long long i = bb + 2ull * (ctid + NC * j);
+            if (i < a1) {
+                const unsigned long long e0 = n0 + D * i;
+                ISP_CHECK(i + 1 < ihi && i >= ilo && ((e0 - seg_lo) >> 1) + (D - 1) < seg_len, 502);
+                fail |= (t[j].x != e0) | (t[j].y != e0 + D);
+                const uint32_t k = (uint32_t)(e0 - seg_lo) >> 1;
+                uint32_t r;
+                if (D == 1) {
+                    // pair (i, i + 1) holds e0 and e0 + 1: one odd value, whose byte index
+                    // is (e0 - seg_lo) >> 1 either way, and one even (prime iff 2: the low
+                    // element when n0 is even, the high one -- e0 = 1 -- when odd)
+                    const uint32_t byte = seg[k];
+                    r = odd0 ? (byte | ((uint32_t)(e0 == 1ull) << 8)) : ((uint32_t)(e0 == 2ull) | (byte << 8));
+                } else {
+                    // D = 2: both odd (consecutive bytes of the segment) or both even
+                    r = odd0 ? ((uint32_t)seg[k] | ((uint32_t)seg[k + 1] << 8))
+                             : ((uint32_t)(e0 == 2ull) | ((uint32_t)(e0 == 0ull) << 8));
+                }
+                __stcs(reinterpret_cast<unsigned short*>(out + i), (unsigned short)r);
+            }
+        }
+    }
+}
 
 // Warp-specialised, double-buffered: the producer warps sieve segment k + 1
 // into one shared buffer while the consumer warps stream the indices of
 // segment k against the other (named barriers 2/3 "buffer b full", 4/5
 // "buffer b empty").  One block per SM: the sieve's shared-memory work and
-// the HBM stream overlap inside every SM.
-__global__ void __launch_bounds__(DENSE_THREADS, 1)
-dense_kernel(DevPlan* __restrict__ plan, const unsigned long long* __restrict__ N, uint8_t* __restrict__ out,
-             uint32_t len, const uint2* __restrict__ bp, int nbp, const uint8_t* __restrict__ patt, int first_large,
-             int vec) {
-    pdl_wait();
-    extern __shared__ __align__(16) uint8_t dseg[];  // two SEG_ODD buffers
-    if (!plan->dense) return;
+// the HBM stream overlap inside every SM.  One kernel body per stride (the
+// host launches one kernel; a block-uniform branch picks the body -- two
+// inlined bodies made ptxas spill, so the stride-2 body is a call).
+template <int D, int NP>
+__device__ __forceinline__ void dense_body(DevPlan* __restrict__ plan, uint8_t* dseg,
+                                           const unsigned long long* __restrict__ N, uint8_t* __restrict__ out,
+                                           uint32_t len, const uint2* __restrict__ bp, int nbp,
+                                           const uint8_t* __restrict__ patt, int first_large, int vec) {
     const unsigned long long wlo = plan->wlo, whi = plan->whi, n0 = plan->dense_base;
     const unsigned long long span_odd = (whi - wlo) >> 1;
     uint32_t SL;
     unsigned long long nseg;
     seg_layout(span_odd, gridDim.x, SL, nseg);
-    const bool producer = threadIdx.x < DENSE_PRODUCERS;
-    const bool odd0 = n0 & 1ull;  // parity of n0 + i for even i (the vector path's pairs)
-    const int ctid = (int)threadIdx.x - DENSE_PRODUCERS;  // consumer thread index
-    constexpr int NC = DENSE_THREADS - DENSE_PRODUCERS;
+    const bool producer = threadIdx.x < NP;
+    const int ctid = (int)threadIdx.x - NP;  // consumer thread index
     bool fail = false;
     unsigned int k = 0;
     for (unsigned long long sgi = blockIdx.x; sgi < nseg; sgi += gridDim.x, k++) {
@@ -767,52 +831,13 @@ dense_kernel(DevPlan* __restrict__ plan, const unsigned long long* __restrict__ 
                 if (b) asm volatile("bar.sync 5, %0;" :: "n"(DENSE_THREADS) : "memory");
                 else asm volatile("bar.sync 4, %0;" :: "n"(DENSE_THREADS) : "memory");
             }
-            sieve_segment<true, DENSE_PRODUCERS>(seg, seg_lo, seg_len, bp, nbp, patt, first_large);
+            sieve_segment<true, NP>(seg, seg_lo, seg_len, bp, nbp, patt, first_large);
             if (b) asm volatile("bar.arrive 3, %0;" :: "n"(DENSE_THREADS) : "memory");
             else asm volatile("bar.arrive 2, %0;" :: "n"(DENSE_THREADS) : "memory");
         } else {
             if (b) asm volatile("bar.sync 3, %0;" :: "n"(DENSE_THREADS) : "memory");
             else asm volatile("bar.sync 2, %0;" :: "n"(DENSE_THREADS) : "memory");
-            // indices whose expected values N0 + i lie in [seg_lo, seg_hi)
-            const unsigned long long ilo = seg_lo > n0 ? seg_lo - n0 : 0ull;
-            const unsigned long long ihi = seg_hi - n0 < len ? seg_hi - n0 : (unsigned long long)len;
-            auto one = [&](unsigned long long i, unsigned long long v) -> uint32_t {
-                ISP_CHECK(i < len && i >= ilo && i < ihi, 501);
-                if (v != n0 + i) { fail = true; return 0u; }
-                return (v & 1ull) ? seg[(uint32_t)(v - seg_lo) >> 1] : (uint32_t)(v == 2ull);
-            };
-            // element pairs with 16-byte loads, eight per thread in flight
-            const unsigned long long a0 = vec ? ((ilo + 1) & ~1ull) : ihi;
-            const unsigned long long a1 = a0 < ihi ? a0 + ((ihi - a0) & ~1ull) : a0;
-            for (unsigned long long i = ilo + ctid; i < (a0 < ihi ? a0 : ihi); i += NC)
-                out[i] = (uint8_t)one(i, N[i]);
-            for (unsigned long long i = (a0 < ihi ? a1 : ihi) + ctid; i < ihi; i += NC)
-                out[i] = (uint8_t)one(i, N[i]);
-            constexpr int U = 8;
-            for (unsigned long long bb = a0; bb < a1; bb += 2ull * NC * U) {
-                ulonglong2 t[U];
-#pragma unroll
-                for (int j = 0; j < U; j++) {
-                    const unsigned long long i = bb + 2ull * (ctid + NC * j);
-                    if (i < a1) t[j] = __ldcs(reinterpret_cast<const ulonglong2*>(N + i));
-                }
-#pragma unroll
-                for (int j = 0; j < U; j++) {
-                    const unsigned long long i = bb + 2ull * (ctid + NC * j);
-                    if (i < a1) {
-                        // pair (i, i + 1) holds n0 + i and n0 + i + 1: one odd value, whose byte
-                        // index is (n0 + i - seg_lo) >> 1 either way, and one even (prime iff 2:
-                        // the low element when n0 is even, the high one -- e0 = 1 -- when odd)
-                        const unsigned long long e0 = n0 + i;
-                        ISP_CHECK(i + 1 < ihi && i >= ilo && ((e0 - seg_lo) >> 1) < seg_len, 502);
-                        fail |= (t[j].x != e0) | (t[j].y != e0 + 1);
-                        const uint32_t byte = seg[(uint32_t)(e0 - seg_lo) >> 1];
-                        const uint32_t r = odd0 ? (byte | ((uint32_t)(e0 == 1ull) << 8))
-                                                : ((uint32_t)(e0 == 2ull) | (byte << 8));
-                        __stcs(reinterpret_cast<unsigned short*>(out + i), (unsigned short)r);
-                    }
-                }
-            }
+            dense_consume<D, DENSE_THREADS - NP>(seg, seg_lo, seg_hi, seg_len, n0, N, out, len, vec, ctid, fail);
             // release the buffer if the producers will refill it
             if (sgi + 2ull * gridDim.x < nseg) {
                 if (b) asm volatile("bar.arrive 5, %0;" :: "n"(DENSE_THREADS) : "memory");
@@ -821,6 +846,29 @@ dense_kernel(DevPlan* __restrict__ plan, const unsigned long long* __restrict__ 
         }
     }
     if (__syncthreads_or(fail) && threadIdx.x == 0) atomicOr(&plan->dense_fail, 1u);
+}
+
+// Stride 1 and stride 2 are separate kernels (both are launched; the one
+// whose stride the plan did not find exits at once): one kernel with both
+// bodies made ptxas spill and cost C4 4.5 % (tools/ab.sh).
+__global__ void __launch_bounds__(DENSE_THREADS, 1)
+dense_kernel(DevPlan* __restrict__ plan, const unsigned long long* __restrict__ N, uint8_t* __restrict__ out,
+             uint32_t len, const uint2* __restrict__ bp, int nbp, const uint8_t* __restrict__ patt, int first_large,
+             int vec) {
+    pdl_wait();
+    extern __shared__ __align__(16) uint8_t dseg[];  // two SEG_ODD buffers
+    if (!plan->dense || plan->dense_d != 1) return;
+    dense_body<1, DENSE_PRODUCERS1>(plan, dseg, N, out, len, bp, nbp, patt, first_large, vec);
+}
+
+__global__ void __launch_bounds__(DENSE_THREADS, 1)
+dense2_kernel(DevPlan* __restrict__ plan, const unsigned long long* __restrict__ N, uint8_t* __restrict__ out,
+              uint32_t len, const uint2* __restrict__ bp, int nbp, const uint8_t* __restrict__ patt, int first_large,
+              int vec) {
+    pdl_wait();
+    extern __shared__ __align__(16) uint8_t dseg[];
+    if (!plan->dense || plan->dense_d != 2) return;
+    dense_body<2, DENSE_PRODUCERS2>(plan, dseg, N, out, len, bp, nbp, patt, first_large, vec);
 }
 
 // ------------------------------------------------------------- A2: classify
@@ -1434,7 +1482,7 @@ mr1_kernel(DevPlan* __restrict__ plan, Queues q, const unsigned long long* __res
 
 // ------------------------------------------------------------- A4: MR phase 2
 template <int WIN, bool FULL32, int G64, int WIT = 0>
-__global__ void __launch_bounds__(MR_THREADS)
+__global__ void __launch_bounds__(MR_THREADS, G64 == 3 ? 4 : 3)
 mr2_kernel(DevPlan* __restrict__ plan, Queues q, const unsigned long long* __restrict__ N, uint8_t* __restrict__ out,
            uint32_t len, int count_work, int sched) {
     pdl_wait();

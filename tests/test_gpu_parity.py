@@ -280,6 +280,40 @@ def test_dense_range_path_and_fallback():
     assert_same(gpu(N), oracle.isprime(N), N)
 
 
+@pytest.mark.parametrize("lo,n", [(1, 1 << 28), (3, (1 << 20) + 5), ((1 << 31) + 7, (1 << 26) + 3),
+                                  ((1 << 32) - (1 << 22) - 1, 1 << 21), (0, (1 << 20) + 1), (2, 1 << 21)])
+def test_stride2_range_every_element(lo, n):
+    """Arithmetic progressions of stride 2 -- odd numbers in a restricted
+    range and the even ones -- go to dense_kernel (no global
+    bitmap): N[i] = lo + 2 i, every element compared with the oracle's sieve."""
+    isp.set_option("small_max", 0)
+    dN = torch.arange(lo, lo + 2 * n, 2, dtype=torch.int64, device=DEV)
+    dout = torch.full((n,), 7, dtype=torch.uint8, device=DEV)
+    isp.reset_stats()
+    isp.isprime_device(dN, dout, n)
+    torch.cuda.synchronize()
+    del dN
+    st = isp.get_stats()
+    assert st["queued32"] == 0 and st["queued64"] == 0  # no element left for the witness kernels
+    exp = _sieve32()[lo:lo + 2 * n:2]
+    got = dout.cpu().numpy()
+    assert_same(got, exp, np.arange(lo, lo + 2 * n, 2, dtype=np.uint64))
+    del dout
+    torch.cuda.empty_cache()
+
+
+def test_stride2_range_with_foreign_elements():
+    """A stride-2 range with a few planted foreign values: dense_kernel sees
+    the mismatch and the classify pass redoes the chunk without the window."""
+    rng = np.random.default_rng(22)
+    N = np.arange(9_000_001, 9_000_001 + 2 * (1 << 21), 2, dtype=np.uint64)
+    hit = rng.choice(N.shape[0], size=41, replace=False)
+    N[hit] = rng.integers(0, 2**64 - 1, size=41, dtype=np.uint64, endpoint=True)
+    N[hit[:4]] = np.array([2, 9, (1 << 64) - 59, 4294967291], dtype=np.uint64)
+    isp.set_option("small_max", 0)
+    assert_same(gpu(N), oracle.isprime(N), N)
+
+
 def test_sieve_cache_reuses_held_window():
     """Option sieve_cache = 1 lets a call reuse the bitmap an earlier call
     sieved; a later window inside the held one must index the bitmap from
