@@ -41,22 +41,24 @@ import workloads  # noqa: E402
 
 METRIC = "Gints/sec classified (1/2/4/8 B200) per magnitude class; % of IMAD or HBM roofline"
 UNIT = "Gints/s"
-# Minimal pipe work of one modular multiplication, in lane-slots of a 16-lane
-# pipe: IMAD.WIDE.U32 and IMAD.HI are half rate on the
-# FMA-heavy pipe (profiles/r1_imad_peak.json: 25.2 / 31.7 vs 63.2 lanes/clk/SM
-# for IMAD), so they count 2 slots.
-#   64-bit Montgomery: 4 WIDE (a*b) + 1 WIDE + 2 IMAD (m) + 4 WIDE (hi(m n)) -> 18 FMA-heavy slots
-#     (a squaring needs 3 WIDE for a^2 -> 16; the multiply count below does not
-#      separate squarings, so 18 is a conservative, i.e. higher, work figure)
-#   32-bit Montgomery: 1 WIDE + 1 IMAD + 1 HI -> 5 FMA-heavy slots
-#   FP64 (n < 2^51), lazy signed residues: DMUL (h), DFMA (l), DFMA + DADD (q), DFMA + DADD (r)
-#     -> 6 FP64 lane-ops (modmath.cuh fmul_lazy)
-# The 32-bit class runs on the FP64 pipe too (csrc/kernels.cuh CLS32_FP64 = 1).
-SLOTS_MULMOD64 = 18
-SLOTS_MULMOD32 = 5
-FP64_OPS_MULMOD = 6
+# Roofline of the witness kernels.  DFMA and IMAD.WIDE share
+# one multiplier pipe on B200 (tools/mont_bench.cu: FP64-product warps and
+# Montgomery warps on the same SMs overlap by ~8 %, profiles/r2/mont_bench.json),
+# so the bound is ONE heavy pipe of 64 lane-slots/clk/SM, and each instruction
+# costs 64 / (its measured lanes/clk/SM) slots (profiles/r1_imad_peak.json):
+LANES_WIDE, LANES_IMAD, LANES_DFMA = 25.12, 63.09, 63.20
+SLOT_WIDE, SLOT_IMAD, SLOT_FP64 = 64 / LANES_WIDE, 64 / LANES_IMAD, 64 / LANES_DFMA
+# heavy-pipe instructions per unit of work, from the SASS of the kernels'
+# arithmetic (tools/sass_counts.py -> profiles/r2/sass_counts.json):
+#   Montgomery product (mr2, msqr64_lz_ptx): 8 IMAD.WIDE + 2 IMAD + 1 IMAD.X
+#   base-2 ladder step (mr1, msqr64_shl_lz_ptx): 8 IMAD.WIDE + 2 IMAD
+#   FP64 lazy product (fmul_lazy; FP64 and 32-bit classes): DMUL + 3 DFMA + 2 DADD
+SLOTS_MONT_PRODUCT = 8 * SLOT_WIDE + 3 * SLOT_IMAD      # 23.4 (predicts 7.95e11/s; measured 7.96e11)
+SLOTS_MONT_LADDER = 8 * SLOT_WIDE + 2 * SLOT_IMAD       # 22.4
+SLOTS_FP64_PRODUCT = 6 * SLOT_FP64                      # 6.1
+SURVEY_IMAD_PER_MULMOD64 = 14                           # 14 IMAD per 64-bit mulmod at 64 lanes/clk
 CLS32_ON_FP64 = True
-LANES_PER_CLK_SM = 64  # FMA-heavy and FP64 pipes: 16 lanes/clk per SMSP x 4 (B300_MICROARCH.md; measured 63.2 / 63.1)
+LANES_PER_CLK_SM = 64
 HBM_BYTES_PER_ELEM = 9      # 8-B value read + 1-B result written
 
 
@@ -331,25 +333,40 @@ def roofline(kern_ms, stats, n, steps, peaks, peaks_kind, clocks, cfg=None):
         except Exception:
             traffic, ncu = None, None
     if name in ("mr1", "mr2"):
+        # units of work: modular multiplications of the method's square-and-multiply
+        # ModExp, counted on the device per magnitude class
         mm, mf = stats["mulmods"], stats["mulmods_fp64"]
         k = 0 if name == "mr1" else 2
-        fma_slots = (0 if CLS32_ON_FP64 else mm[k] * SLOTS_MULMOD32) + mm[k + 1] * SLOTS_MULMOD64
-        fp64_ops = (mf[0 if name == "mr1" else 1] + (mm[k] if CLS32_ON_FP64 else 0)) * FP64_OPS_MULMOD
-        busiest = max(fma_slots, fp64_ops)
-        achieved = busiest / steps / (ms * 1e-3) / 1e12
+        mont = mm[k + 1] / steps
+        fp = (mf[0 if name == "mr1" else 1] + (mm[k] if CLS32_ON_FP64 else 0)) / steps
+        slots = mont * (SLOTS_MONT_LADDER if name == "mr1" else SLOTS_MONT_PRODUCT) + fp * SLOTS_FP64_PRODUCT
+        achieved = slots / (ms * 1e-3) / 1e12
         mhz = peaks.get("sm_max_mhz", 1965.0)
         peak = 148 * LANES_PER_CLK_SM * mhz * 1e6 / 1e12
-        per_pipe = {"fmaheavy": round(fma_slots / steps / (ms * 1e-3) / 1e12 / peak, 4),
-                    "fp64": round(fp64_ops / steps / (ms * 1e-3) / 1e12 / peak, 4)}
+        survey = (mont * SURVEY_IMAD_PER_MULMOD64 + fp * 6) / (ms * 1e-3) / 1e12 / peak
+        ncu_sum = None
+        if ncu and ncu.get("fmaheavy_pipe_pct") is not None and ncu.get("fp64_pipe_pct") is not None:
+            ncu_sum = round((ncu["fmaheavy_pipe_pct"] + ncu["fp64_pipe_pct"]) / 100.0, 4)
         return {"kernel": name, "bound": "alu", "achieved": round(achieved, 4), "peak": round(peak, 3),
-                "unit": "T lane-slots/s (busiest of FMA-heavy / FP64 pipe)", "frac": round(achieved / peak, 4),
-                "frac_per_pipe": per_pipe,
+                "unit": "T heavy-pipe lane-slots/s (IMAD.WIDE and DFMA share one multiplier pipe)",
+                "frac": round(achieved / peak, 4),
+                "ncu_fmaheavy_plus_fp64": ncu_sum,
+                "survey_model_frac": round(survey, 4),
                 "traffic": traffic, "ncu": ncu,
-                "peak_source": f"derived: 148 SMs x {LANES_PER_CLK_SM} lanes/clk x {mhz:.0f} MHz "
-                               "(B300_MICROARCH.md pipe rates; MEASURED_PEAKS sm_max_mhz)",
-                "work": f"per step: {fma_slots / steps:.4g} FMA-heavy slots ({SLOTS_MULMOD64}/64-bit Montgomery mulmod) "
-                        f"and {fp64_ops / steps:.4g} FP64 ops ({FP64_OPS_MULMOD}/mulmod of the FP64 and 32-bit classes); "
-                        "mulmods = square-and-multiply count of ModExp",
+                "peak_source": f"148 SMs x {LANES_PER_CLK_SM} lane-slots/clk x {mhz:.0f} MHz (MEASURED_PEAKS "
+                               f"sm_max_mhz); per-instruction slots 64/measured lanes/clk/SM: IMAD.WIDE "
+                               f"{SLOT_WIDE:.2f}, IMAD {SLOT_IMAD:.2f}, DFMA {SLOT_FP64:.2f} (profiles/r1_imad_peak.json)",
+                "work": f"per step: {mont:.4g} Montgomery {'ladder steps' if name == 'mr1' else 'products'} x "
+                        f"{SLOTS_MONT_LADDER if name == 'mr1' else SLOTS_MONT_PRODUCT:.1f} slots + {fp:.4g} FP64 "
+                        f"products x {SLOTS_FP64_PRODUCT:.1f} slots (SASS: profiles/r2/sass_counts.json); "
+                        f"survey_model_frac: {SURVEY_IMAD_PER_MULMOD64} slots per 64-bit mulmod",
+                "ms_per_step": round(ms, 4)}
+    if name == "small":
+        return {"kernel": name, "bound": "latency", "achieved": None, "peak": None, "unit": None, "frac": None,
+                "traffic": traffic, "ncu": ncu,
+                "work": f"{n} elements in one fused launch ({ms * 1e3:.1f} us): launch- and latency-bound "
+                        f"({9 * n / 1e6:.2f} MB of traffic = {9 * n / (peaks.get('hbm_gbs', 6541.1) * 1e9) * 1e6:.2f} "
+                        "us at HBM peak), SURVEY.md 8(d)",
                 "ms_per_step": round(ms, 4)}
     nbytes = HBM_BYTES_PER_ELEM * n
     if name == "dense":   # fused sieve + gather of a dense range: reads N, writes out
@@ -523,6 +540,29 @@ def scalar_latency(isp, torch, dev, stream):
     return res
 
 
+def stride2_run(isp, torch, dev, stream, args, peaks, clocks):
+    """odd numbers in a restricted range, N[i]
+    = N0 + 2 i, 2^28 elements below 2^32 -- the fused streaming sieve
+    (dense2_kernel, no global bitmap).  Device time per call and the achieved
+    fraction of HBM at 9 algorithmic bytes per element."""
+    res = {}
+    for lo in (1, (1 << 32) - (1 << 29) + 1):
+        n = 1 << 28
+        dN = torch.arange(lo, lo + 2 * n, 2, dtype=torch.int64, device=dev)
+        dout = torch.empty(n, dtype=torch.uint8, device=dev)
+        ms, _ = time_steps(isp, torch, dN, dout, n, args.steps, args.warmup, stream, None)
+        km, st, _ = kernel_profile(isp, torch, dN, dout, n, args.steps, stream)
+        gbs = 9 * n / (ms * 1e-3) / 1e9
+        res[f"N0={lo}"] = {"value": round(n / (ms * 1e-3) / 1e9, 4), "unit": UNIT, "ms_per_step": round(ms, 4),
+                           "hbm_GBps_algorithmic": round(gbs, 1),
+                           "hbm_frac": round(gbs / float(peaks.get("hbm_gbs", 6541.1)), 4),
+                           "queued_for_witness_kernels": st["queued32"] + st["queued64"],
+                           "kernels_ms_per_step": {k: round(v, 4) for k, v in km.items()}}
+        del dN, dout
+        torch.cuda.empty_cache()
+    return res
+
+
 def e2e_run(isp, torch, dev, dist, host, shard, dout, steps):
     """The same metric through the host C-ABI isprime() on pinned buffers:
     H2D of the batch and D2H of the result inside the timed region (host wall
@@ -671,6 +711,7 @@ def main():
         line["cpu_baseline"] = cpu_baseline_run(cfg, host, min(n, args.cpu_sample), min(n, args.cpu_sample1))
         if not args.no_extras:
             line["scalar_latency"] = scalar_latency(isp, torch, dev, stream)
+            line["stride2_odd_range"] = stride2_run(isp, torch, dev, stream, args, peaks, clocks)
             line["witness_bpsw"] = witness_option(isp, torch, dev, stream, args, counts, 1, ("C5", "C3"))
             line["witness_reduced"] = witness_option(isp, torch, dev, stream, args, counts, 2, ("C5", "C2"))
     if rank == 0:

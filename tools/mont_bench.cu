@@ -315,6 +315,49 @@ __global__ void __launch_bounds__(256) k_mixed(unsigned long long* out, unsigned
     out[blockIdx.x * blockDim.x + threadIdx.x] = s;
 }
 
+// the base-2 ladder step of mr1 (square, times 2^bit, lazy REDC): CH
+// independent ladders per thread, n in [2^60, 2^61), bits from a per-thread
+// word (uniform 0/1 mix)
+template <int CH, int THREADS>
+__global__ void __launch_bounds__(THREADS) k_ladder(unsigned long long* out, unsigned long long seed) {
+    unsigned long long n = seed ^ ((unsigned long long)(blockIdx.x * blockDim.x + threadIdx.x) * 0x9E3779B97F4A7C15ull);
+    n = (n & ((1ull << 60) - 1)) | (1ull << 60) | 1ull;
+    const unsigned long long nn = 0ull - inv64(n);
+    uint32_t w = (uint32_t)(n >> 7) * 0x2545F491u;
+    unsigned long long x[CH];
+#pragma unroll
+    for (int c = 0; c < CH; c++) x[c] = ((threadIdx.x + 1) * 0x2545F4914F6CDD1Dull + c * 0x1234567ull) % n;
+#pragma unroll 1
+    for (int i = 0; i < ITERS; i++) {
+#pragma unroll
+        for (int c = 0; c < CH; c++) x[c] = msqr64_shl_lz_ptx(x[c], n, nn, w >> 31);
+        w = (w << 1) | (w >> 31);
+    }
+    unsigned long long s = 0;
+#pragma unroll
+    for (int c = 0; c < CH; c++) s ^= mcanon64(x[c], n);
+    out[blockIdx.x * blockDim.x + threadIdx.x] = s;
+}
+
+template <int CH, int THREADS>
+double ladder_rate(unsigned long long* buf, int sms) {
+    int maxb = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&maxb, k_ladder<CH, THREADS>, THREADS, 0);
+    const int blocks = sms * (maxb > 0 ? maxb : 1);
+    cudaEvent_t a, b;
+    cudaEventCreate(&a);
+    cudaEventCreate(&b);
+    k_ladder<CH, THREADS><<<blocks, THREADS>>>(buf, 3);
+    cudaDeviceSynchronize();
+    cudaEventRecord(a);
+    for (int r = 0; r < 5; r++) k_ladder<CH, THREADS><<<blocks, THREADS>>>(buf, 3);
+    cudaEventRecord(b);
+    cudaEventSynchronize(b);
+    float ms = 0;
+    cudaEventElapsedTime(&ms, a, b);
+    return (double)blocks * THREADS * CH * ITERS / (ms / 5 * 1e-3);
+}
+
 template <typename F>
 float time_ms(F f) {
     cudaEvent_t a, b;
@@ -351,6 +394,10 @@ int main() {
            rate<2, 3>(buf, sms), rate<3, 3>(buf, sms), rate<2, 4>(buf, sms), rate<3, 4>(buf, sms));
     printf(", \"L2_ch3\": %.4e, \"L2_ch4\": %.4e, \"W_ch3\": %.4e, \"W_ch4\": %.4e, \"W_ch6\": %.4e}",
            rate<4, 3>(buf, sms), rate<4, 4>(buf, sms), rate<5, 3>(buf, sms), rate<5, 4>(buf, sms), rate<5, 6>(buf, sms));
+    printf(", \"ladder_shl_lz_per_s\": {\"ch1_t512\": %.4e, \"ch2_t512\": %.4e, \"ch1_t256\": %.4e, \"ch2_t256\": %.4e, "
+           "\"ch3_t256\": %.4e, \"ch4_t256\": %.4e}",
+           ladder_rate<1, 512>(buf, sms), ladder_rate<2, 512>(buf, sms), ladder_rate<1, 256>(buf, sms),
+           ladder_rate<2, 256>(buf, sms), ladder_rate<3, 256>(buf, sms), ladder_rate<4, 256>(buf, sms));
     // agreement
     unsigned long long h[6];
     k_sqr<0, 3><<<1, 64>>>(buf, 12345);
