@@ -35,7 +35,10 @@ constexpr int PRESIEVE_PERIOD = 3 * 5 * 7 * 11 * 13;  // 15015 (odd-index period
 constexpr int PRESIEVE_COPIES = 16;                   // shifted copies for 16-B loads
 constexpr int PRESIEVE_LEN = ((PRESIEVE_PERIOD + SEG_ODD + 64 + 15) / 16) * 16;
 constexpr int FIRST_CROSS_PRIME_IDX = 5;              // odd primes 3,5,7,11,13 pre-sieved
-constexpr int CLS_THREADS = 1024;
+#ifndef CLS_THREADS_DEF
+#define CLS_THREADS_DEF 1024
+#endif
+constexpr int CLS_THREADS = CLS_THREADS_DEF;
 constexpr int CLS_PAIRS = 4;                          // 2 elements per pair -> 8 per thread
 constexpr int CLS_TILE = CLS_THREADS * 2 * CLS_PAIRS; // 8192 elements per block tile
 constexpr int MR_THREADS = 256;                       // phase 2 (shared-memory window tables)
@@ -51,6 +54,12 @@ constexpr int MAX_SEG = 4096;                         // classify blocks (queue 
 // first global access, until the previous grid has completed and its writes
 // are visible.  A no-op when the kernel was launched without the attribute.
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+// Ask the TMA unit to pull [p, p + bytes) into L2 (p 16-B aligned, bytes a
+// multiple of 16): a streaming kernel prefetches its next tile with one
+// instruction instead of holding more loads in flight in registers.
+__device__ __forceinline__ void l2_prefetch_bulk(const void* p, uint32_t bytes) {
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
+}
 
 // Device-side bounds checks (build with -DISP_CHECKS=1): a failed check
 // records its id in g_isp_check (the first one wins) and the host turns it
@@ -124,8 +133,8 @@ struct Queues {
     uint32_t* s;
     unsigned int cap;                                  // entries per array
 };
-constexpr int QE_TILE_BITS = 13;                      // CLS_TILE = 2^13
-constexpr uint32_t QE_MAX_TILES = 1u << 13;           // tiles per classify block
+constexpr int QE_TILE_BITS = CLS_TILE == 8192 ? 13 : CLS_TILE == 4096 ? 12 : 11;  // log2(CLS_TILE)
+constexpr uint32_t QE_MAX_TILES = 1u << (26 - QE_TILE_BITS);  // tiles per classify block
 static_assert(CLS_TILE == (1 << QE_TILE_BITS), "packed queue entry: tile offset field");
 
 struct TDParams {
@@ -738,8 +747,14 @@ sieve_kernel(const DevPlan* __restrict__ plan, uint32_t* __restrict__ bitmap,
 constexpr int DENSE_THREADS = 1024;
 // warps that sieve (the rest stream): stride 1 covers one integer per
 // element, stride 2 two, so the stride-2 range gives the sieve twice the warps
-constexpr int DENSE_PRODUCERS1 = 256;
-constexpr int DENSE_PRODUCERS2 = 512;
+#ifndef DENSE_PRODUCERS1_DEF
+#define DENSE_PRODUCERS1_DEF 256
+#endif
+constexpr int DENSE_PRODUCERS1 = DENSE_PRODUCERS1_DEF;
+#ifndef DENSE_PRODUCERS2_DEF
+#define DENSE_PRODUCERS2_DEF 512
+#endif
+constexpr int DENSE_PRODUCERS2 = DENSE_PRODUCERS2_DEF;
 
 // The consumer side for one segment [seg_lo, seg_hi) of stride D: scalar head
 // and tail, element pairs (i, i + 1), i even, with 16-byte loads in between.
@@ -766,6 +781,16 @@ __device__ __forceinline__ void dense_consume(const uint8_t* seg, unsigned long 
     for (unsigned long long i = (a0 < ihi ? a1 : ihi) + ctid; i < ihi; i += NC) out[i] = (uint8_t)one(i, N[i]);
     constexpr int U = 8;  // eight pairs per thread in flight
     for (unsigned long long bb = a0; bb < a1; bb += 2ull * NC * U) {
+        // the consumers' loads alone keep too few bytes in flight per SM to cover
+        // the HBM latency: one thread asks the TMA unit to pull the next batch
+        // of the segment into L2 (cp.async.bulk.prefetch), so that batch's loads hit L2
+        if (ctid == 0) {
+            const unsigned long long nb = bb + 2ull * NC * U;
+            if (nb < a1) {
+                const unsigned long long ne = nb + 2ull * NC * U < a1 ? nb + 2ull * NC * U : a1;
+                l2_prefetch_bulk(N + nb, (uint32_t)((ne - nb) * 8ull));
+            }
+        }
         ulonglong2 t[U];
 #pragma unroll
         for (int j = 0; j < U; j++) {
@@ -1211,6 +1236,13 @@ __global__ void __launch_bounds__(SORT_THREADS) qscatter_kernel(DevPlan* __restr
         const unsigned int count = plan->seg[g];
         const size_t sb = (size_t)g * seg_stride;
         for (unsigned int t0 = part * SORT_TILE; t0 < count; t0 += SORT_SPLIT * SORT_TILE) {
+            // this block's next tile of the segment into L2 (segments start at
+            // multiples of CLS_TILE entries: 16-B aligned)
+            if (tid == 0 && t0 + SORT_SPLIT * SORT_TILE < count) {
+                const unsigned int nt = t0 + SORT_SPLIT * SORT_TILE;
+                const unsigned int cnt = (count - nt < (unsigned int)SORT_TILE ? count - nt : (unsigned int)SORT_TILE) & ~3u;
+                if (cnt) l2_prefetch_bulk(q.q + sb + nt, cnt * 4u);
+            }
             uint32_t ent[PER];
 #pragma unroll
             for (int k = 0; k < PER; k++) {  // all loads in flight before any use
