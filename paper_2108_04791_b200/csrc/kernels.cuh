@@ -926,30 +926,17 @@ struct ClsSmem {
     unsigned int h[65];   // bit-length histogram of this block's survivors (for the sort)
 };
 
-template <int N32, int N64>
-__global__ void __launch_bounds__(CLS_THREADS)
-classify_kernel(const unsigned long long* __restrict__ N, uint8_t* __restrict__ out, uint32_t len,
-                DevPlan* __restrict__ plan, const uint32_t* __restrict__ bitmap, Queues q, TDParams td,
-                int vec_in, int vec_out, uint32_t seg_stride) {
-    pdl_wait();
-    extern __shared__ __align__(16) unsigned char cls_smem[];  // sizeof(ClsSmem), dynamic (> 48 KB at 1024 threads)
-    ClsSmem& sm = *reinterpret_cast<ClsSmem*>(cls_smem);
-    const uint32_t segbase = blockIdx.x * seg_stride;
-    // dense_kernel already classified a dense range; if it found a mismatch,
-    // this pass redoes the chunk without the window (no global bitmap was sieved)
-    if (plan->dense && !*reinterpret_cast<volatile unsigned int*>(&plan->dense_fail)) return;
-    const unsigned long long wlo = plan->wlo, whi = plan->dense ? plan->wlo : plan->whi;
-    const unsigned long long span = whi - wlo;  // <= 2^32 (0: no window)
-    // 32-bit form of the window test for values below 2^32: (lo - wlo) mod 2^32
-    // <= span - 1 (whi <= 2^32, so values below wlo wrap past the span)
-    const uint32_t wlo32 = (uint32_t)wlo, spanm1 = (uint32_t)(span - 1);
-    const uint32_t spanm1w = span ? spanm1 : 0u;  // no window: only dd == 0 passes, i.e. the even value wlo
-    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
-    ClsWarp& ws = sm.w[wid];
-    const uint32_t ntiles = (len + CLS_TILE - 1) / CLS_TILE;
-    for (int b = tid; b < 65; b += CLS_THREADS) sm.h[b] = 0;
-    if (tid == 0) sm.cur = 0;
-    __syncthreads();
+// The tile loop of classify_kernel.  UNI (the chunk has no sieve window):
+// warp-tiles whose values are all below 2^32 or all at or above take a
+// shorter classification; a separate instantiation keeps the general loop's
+// code unchanged for chunks with a window.
+template <int N32, int N64, bool UNI>
+__device__ __forceinline__ void classify_tiles(const unsigned long long* __restrict__ N, uint8_t* __restrict__ out,
+                                               uint32_t len, const uint32_t* __restrict__ bitmap, const Queues& q,
+                                               const TDParams& td, int vec_in, int vec_out, uint32_t seg_stride,
+                                               uint32_t segbase, unsigned long long span, uint32_t wlo32,
+                                               uint32_t spanm1, uint32_t spanm1w, uint32_t ntiles, ClsSmem& sm,
+                                               ClsWarp& ws, int lane, int wid) {
     uint32_t tk = 0;  // tile number within this block (packed queue entries)
     for (uint32_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, tk++) {
         const uint32_t wbase = tile * CLS_TILE + 256u * wid;
@@ -1025,6 +1012,36 @@ classify_kernel(const unsigned long long* __restrict__ N, uint8_t* __restrict__ 
         // Elements past len were loaded as 0 (even): never a candidate.
         uint32_t m32 = 0, m64 = 0;  // candidate masks by class (bit e)
         uint8_t r[8];
+        // no window and a warp-tile of one class (configs C2: every value below
+        // 2^32, C3: every value at or above): no window test, one class test
+        bool uni = false;
+        if constexpr (UNI) {
+            uint32_t hor = 0, hz = 0;
+#pragma unroll
+            for (int e = 0; e < 8; e++) {
+                hor |= vhi[e];
+                hz |= (uint32_t)(vhi[e] == 0u);
+            }
+            if (__all_sync(0xffffffffu, hor == 0u)) {
+                // odd values other than 1 are candidates, 2 is the only even prime
+#pragma unroll
+                for (int e = 0; e < 8; e++) {
+                    const uint32_t xlo = vlo[e];
+                    r[e] = (uint8_t)(xlo == 2u);
+                    m32 |= (xlo & (uint32_t)(xlo != 1u)) << e;
+                }
+                uni = true;
+            } else if (__all_sync(0xffffffffu, hz == 0u)) {
+                // every value >= 2^32: the odd ones are candidates
+#pragma unroll
+                for (int e = 0; e < 8; e++) {
+                    r[e] = 0;
+                    m64 |= (vlo[e] & 1u) << e;
+                }
+                uni = true;
+            }
+        }
+        if (!uni) {
         uint32_t word[8], dd[8];
         uint32_t inmask = 0;
         // flags as 0/1 integers combined with bitwise operators: no short-circuit
@@ -1050,6 +1067,7 @@ classify_kernel(const unsigned long long* __restrict__ N, uint8_t* __restrict__ 
             m64 |= (cand & big) << e;
             m32 |= (cand & (big ^ 1u)) << e;
         }
+        }  // !uni
         const uint32_t c32 = __popc(m32), c64 = __popc(m64);
         // warp scan of the packed (c32, c64) counts
         const uint32_t packed = c32 | (c64 << 16);
@@ -1181,6 +1199,38 @@ classify_kernel(const unsigned long long* __restrict__ N, uint8_t* __restrict__ 
             __syncwarp();  // the next warp-tile rewrites this warp's lists
         }
     }
+}
+
+template <int N32, int N64>
+__global__ void __launch_bounds__(CLS_THREADS)
+classify_kernel(const unsigned long long* __restrict__ N, uint8_t* __restrict__ out, uint32_t len,
+                DevPlan* __restrict__ plan, const uint32_t* __restrict__ bitmap, Queues q, TDParams td,
+                int vec_in, int vec_out, uint32_t seg_stride) {
+    pdl_wait();
+    extern __shared__ __align__(16) unsigned char cls_smem[];  // sizeof(ClsSmem), dynamic (> 48 KB at 1024 threads)
+    ClsSmem& sm = *reinterpret_cast<ClsSmem*>(cls_smem);
+    const uint32_t segbase = blockIdx.x * seg_stride;
+    // dense_kernel already classified a dense range; if it found a mismatch,
+    // this pass redoes the chunk without the window (no global bitmap was sieved)
+    if (plan->dense && !*reinterpret_cast<volatile unsigned int*>(&plan->dense_fail)) return;
+    const unsigned long long wlo = plan->wlo, whi = plan->dense ? plan->wlo : plan->whi;
+    const unsigned long long span = whi - wlo;  // <= 2^32 (0: no window)
+    // 32-bit form of the window test for values below 2^32: (lo - wlo) mod 2^32
+    // <= span - 1 (whi <= 2^32, so values below wlo wrap past the span)
+    const uint32_t wlo32 = (uint32_t)wlo, spanm1 = (uint32_t)(span - 1);
+    const uint32_t spanm1w = span ? spanm1 : 0u;  // no window: only dd == 0 passes, i.e. the even value wlo
+    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+    ClsWarp& ws = sm.w[wid];
+    const uint32_t ntiles = (len + CLS_TILE - 1) / CLS_TILE;
+    for (int b = tid; b < 65; b += CLS_THREADS) sm.h[b] = 0;
+    if (tid == 0) sm.cur = 0;
+    __syncthreads();
+    if (span == 0)
+        classify_tiles<N32, N64, true>(N, out, len, bitmap, q, td, vec_in, vec_out, seg_stride, segbase, span, wlo32,
+                                       spanm1, spanm1w, ntiles, sm, ws, lane, wid);
+    else
+        classify_tiles<N32, N64, false>(N, out, len, bitmap, q, td, vec_in, vec_out, seg_stride, segbase, span, wlo32,
+                                        spanm1, spanm1w, ntiles, sm, ws, lane, wid);
     __syncthreads();
     for (int b = tid; b < 65; b += CLS_THREADS)
         if (sm.h[b]) atomicAdd(&plan->bins[b], sm.h[b]);
