@@ -918,7 +918,6 @@ struct ClsWarp {
     unsigned long long val[256];  // list32 from the front (low 32 bits used), list64 from the back
     uint8_t pos[256];             // element offset within the warp-tile
     uint8_t res[256];             // results of the warp-tile, element order
-    uint32_t surv[16];            // survivor bit per list slot: [0..8) list32, [8..16) list64 (by back index)
 };
 struct ClsSmem {
     ClsWarp w[CLS_THREADS / 32];
@@ -1005,7 +1004,7 @@ __device__ __forceinline__ void classify_tiles(const unsigned long long* __restr
         // branch-free per element: odd values inside the window read their bit,
         // even values are prime only when equal to 2, other odd values >= 3
         // become trial-division candidates (class 1: < 2^32, class 2: >= 2^32)
-        uint32_t s32 = 0, s64 = 0, wtot = 0, n32 = 0, n64 = 0;
+        uint32_t wtot = 0, n32 = 0, n64 = 0;
         if (!fast) {
         // 32-bit arithmetic throughout: the window lies below 2^32, so an element
         // is inside it iff its high word is 0 and (lo - wlo) mod 2^32 <= span - 1.
@@ -1113,80 +1112,77 @@ __device__ __forceinline__ void classify_tiles(const unsigned long long* __restr
                 p64 -= c64;
             }
             __syncwarp();
-            // ---- trial division over the dense lists
+            // ---- trial division over the dense lists; each group's survivors
+            // go straight to this block's private queue segment (no block
+            // barrier): block b owns entries [b * seg_stride, (b + 1) *
+            // seg_stride) of q, and seg_stride >= (tiles of the block) *
+            // CLS_TILE, so it never fills.  An entry packs the element's offset
+            // in the tile, the tile number within the block and the value's bit
+            // length (the sort key); the value itself is re-read from N by the
+            // witness kernels.
+            const uint32_t tag = (tk << QE_TILE_BITS) | (256u * wid);
             for (uint32_t k0 = 0; k0 < n32; k0 += 32) {
                 const uint32_t k = k0 + lane;
                 bool surv = false;
+                uint32_t x = 0;
                 if (k < n32) {
-                    const uint32_t x = (uint32_t)ws.val[k];
-                    // compile-time primes (immediate operands, 2 instructions each);
-                    // x itself among them is prime, read from a bit mask instead
+                    x = (uint32_t)ws.val[k];
+                    // compile-time primes (immediate operands, 2 instructions each)
                     bool comp = td_primes<0, N32>(x);
                     if constexpr (N32 > 0) {
+                        // x itself among them is prime, read from a bit mask instead
                         constexpr uint32_t kLast = kOddPrimes[N32 - 1];
                         if (x <= kLast) comp = !((kSmallOddPrimeMask[x >> 6] >> ((x >> 1) & 31u)) & 1u);
                     }
-                    if (!comp) {
-                        if (x < td.sq32) ws.res[ws.pos[k]] = 1;
-                        else surv = true;
+                    surv = !comp;
+                }
+                // no factor below the first untested prime p and x < p^2: prime
+                // (rare outside small values: the warp skips the store otherwise)
+                const bool small = surv && x < td.sq32;
+                if (__any_sync(0xffffffffu, small)) {
+                    if (small) ws.res[ws.pos[k]] = 1;
+                }
+                surv &= !small;
+                const uint32_t m = __ballot_sync(0xffffffffu, surv);
+                if (m) {
+                    uint32_t o = 0;
+                    if (lane == 0) o = atomicAdd(&sm.cur, (unsigned int)__popc(m));
+                    o = segbase + __shfl_sync(0xffffffffu, o, 0);
+                    if (surv) {
+                        const uint32_t at = o + __popc(m & ((1u << lane) - 1u));
+                        const uint32_t bl = 32u - __clz(x);
+                        ISP_CHECK(at < segbase + seg_stride && at < q.cap, 101);
+                        q.q[at] = (tag + ws.pos[k]) | ((bl - 1u) << 26);
+                        atomicAdd(&sm.h[bl], 1u);
                     }
                 }
-                const uint32_t m = __ballot_sync(0xffffffffu, surv);
-                if (lane == 0) ws.surv[k0 >> 5] = m;
-                s32 += __popc(m);
             }
             for (uint32_t k0 = 0; k0 < n64; k0 += 32) {
                 const uint32_t k = k0 + lane;  // back index: slot 255 - k
                 bool surv = false;
+                unsigned long long x = 0;
                 if (k < n64) {
-                    const unsigned long long x = ws.val[255u - k];
+                    x = ws.val[255u - k];
                     bool comp = false;
                     if (N64 > 0) comp = td64_fp<N64>(x, td.rnd);
                     surv = !comp;
                 }
                 const uint32_t m = __ballot_sync(0xffffffffu, surv);
-                if (lane == 0) ws.surv[8 + (k0 >> 5)] = m;
-                s64 += __popc(m);
+                if (m) {
+                    uint32_t o = 0;
+                    if (lane == 0) o = atomicAdd(&sm.cur, (unsigned int)__popc(m));
+                    o = segbase + __shfl_sync(0xffffffffu, o, 0);
+                    if (surv) {
+                        const uint32_t at = o + __popc(m & ((1u << lane) - 1u));
+                        const uint32_t bl = 64u - __clzll((long long)x);
+                        ISP_CHECK(at < segbase + seg_stride && at < q.cap, 102);
+                        q.q[at] = (tag + ws.pos[255u - k]) | ((bl - 1u) << 26);
+                        atomicAdd(&sm.h[bl], 1u);
+                    }
+                }
             }
         }
         }  // !fast
-        // ---- queue space from this block's private segment (no block barrier):
-        // block b owns entries [b * seg_stride, (b + 1) * seg_stride) of q;
-        // seg_stride >= (tiles of the block) * CLS_TILE, so it never fills.
-        // An entry packs the element's offset in the tile, the tile number
-        // within the block and the value's bit length (the sort key); the
-        // value itself is re-read from N by the witness kernels.
-        if (s32 | s64) {  // warp-uniform
-            __syncwarp();    // ws.surv written by lane 0
-            uint32_t o = 0;
-            if (lane == 0) o = atomicAdd(&sm.cur, s32 + s64);
-            o = segbase + __shfl_sync(0xffffffffu, o, 0);
-            const uint32_t tag = (tk << QE_TILE_BITS) | (256u * wid);
-            for (uint32_t k0 = 0; k0 < n32; k0 += 32) {
-                const uint32_t m = ws.surv[k0 >> 5];
-                const uint32_t k = k0 + lane;
-                if ((m >> lane) & 1u) {
-                    const uint32_t at = o + __popc(m & ((1u << lane) - 1u));
-                    const uint32_t bl = 32u - __clz((uint32_t)ws.val[k]);
-                    ISP_CHECK(at < segbase + seg_stride && at < q.cap, 101);
-                    q.q[at] = (tag + ws.pos[k]) | ((bl - 1u) << 26);
-                    atomicAdd(&sm.h[bl], 1u);
-                }
-                o += __popc(m);
-            }
-            for (uint32_t k0 = 0; k0 < n64; k0 += 32) {
-                const uint32_t m = ws.surv[8 + (k0 >> 5)];
-                const uint32_t k = k0 + lane;
-                if ((m >> lane) & 1u) {
-                    const uint32_t at = o + __popc(m & ((1u << lane) - 1u));
-                    const uint32_t bl = 64u - __clzll((long long)ws.val[255u - k]);
-                    ISP_CHECK(at < segbase + seg_stride && at < q.cap, 102);
-                    q.q[at] = (tag + ws.pos[255u - k]) | ((bl - 1u) << 26);
-                    atomicAdd(&sm.h[bl], 1u);
-                }
-                o += __popc(m);
-            }
-        }
         // ---- results of a warp that took the list path: shared tile -> out
         if (wtot != 0) {
             __syncwarp();
