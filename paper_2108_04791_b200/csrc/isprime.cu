@@ -62,6 +62,7 @@ struct Ctx {
     uint8_t* patt = nullptr;
     uint32_t* bitmap = nullptr;
     DevPlan* plan = nullptr;
+    unsigned int* segh = nullptr;  // per-classify-block bit-length histograms (the sort's offsets)
     unsigned char* qmem = nullptr;
     size_t qcap = 0;
     Queues q{};
@@ -226,6 +227,8 @@ int init_ctx(Ctx* c) {
     CK(cudaMalloc(&c->bitmap, words * 4));
     CK(cudaMalloc(&c->plan, sizeof(DevPlan)));
     CK(cudaMemset(c->plan, 0, sizeof(DevPlan)));
+    CK(cudaMalloc(&c->segh, (size_t)MAX_SEG * 65 * sizeof(unsigned int)));
+    c->q.segh = c->segh;
     CK(cudaFuncSetAttribute(sieve_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SEG_ODD));
     CK(cudaFuncSetAttribute(dense_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * SEG_ODD));
     CK(cudaFuncSetAttribute(dense2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * SEG_ODD));
@@ -283,6 +286,7 @@ int ensure_queues(Ctx* c, size_t cap) {
     c->q.q = reinterpret_cast<uint32_t*>(c->qmem);
     c->q.s = reinterpret_cast<uint32_t*>(c->qmem) + cap;
     c->q.cap = (unsigned int)cap;
+    c->q.segh = c->segh;
     c->qcap = cap;
     return ISP_OK;
 }
@@ -489,8 +493,7 @@ int device_impl(Ctx* c, const unsigned long long* dN, uint8_t* dout, size_t n, c
         }
         {
             KScope ks(K_SORT, s);
-            const int gs = SORT_SPLIT * gcls;  // SORT_SPLIT blocks per classify segment
-            launch_k(qscatter_kernel, gs, SORT_THREADS, 0, s, c->plan, c->q, gcls, seg_stride);
+            launch_k(qscatter_kernel, gcls, SORT_THREADS, 0, s, c->plan, c->q, gcls, seg_stride);  // one block per segment
             CKL("qscatter_kernel");
         }
         {
@@ -658,7 +661,7 @@ void isprime_shutdown(void) {
         if (!c) continue;
         cudaSetDevice((int)d);
         cudaDeviceSynchronize();
-        cudaFree(c->bp); cudaFree(c->patt); cudaFree(c->bitmap); cudaFree(c->plan);
+        cudaFree(c->bp); cudaFree(c->patt); cudaFree(c->bitmap); cudaFree(c->plan); cudaFree(c->segh);
         if (c->qmem) cudaFree(c->qmem);
         for (int k = 0; k < 2; k++) {
             if (c->din[k]) cudaFree(c->din[k]);

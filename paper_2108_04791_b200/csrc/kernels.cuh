@@ -98,7 +98,7 @@ struct DevPlan {
     // [mr1 32-bit, mr1 64-bit, mr2 32-bit, mr2 64-bit]
     unsigned long long work[4];
     // counting sort of the trial-division survivors by bit length (per chunk)
-    unsigned int bins[65], cur[65];
+    unsigned int bins[65];
     unsigned int cur1[3], cur2[3];          // dynamic work cursors of mr1 / mr2 (3 regions)
     unsigned long long work_f[2];           // FP64-class mulmods: mr1, mr2 (work counting)
     unsigned int dense, dense_fail;         // chunk is N[i] = dense_base + dense_d i below 2^32 (dense_kernel path)
@@ -132,6 +132,7 @@ struct Queues {
     uint32_t* q;
     uint32_t* s;
     unsigned int cap;                                  // entries per array
+    unsigned int* segh;                                // [MAX_SEG][65]: bit-length histogram per classify block
 };
 constexpr int QE_TILE_BITS = CLS_TILE == 8192 ? 13 : CLS_TILE == 4096 ? 12 : 11;  // log2(CLS_TILE)
 constexpr uint32_t QE_MAX_TILES = 1u << (26 - QE_TILE_BITS);  // tiles per classify block
@@ -403,7 +404,7 @@ __global__ void __launch_bounds__(PLAN_THREADS) plan_kernel(const unsigned long 
     if (tid == 0) { in_valid = 0; nsamp_small = 0; s_notdense = 0; }
     // per-chunk resets of the sort bins and work cursors (read only by the
     // kernels after this one), spread over the block
-    if (tid < 65) { plan->bins[tid] = 0; plan->cur[tid] = 0; }
+    if (tid < 65) plan->bins[tid] = 0;
     if (tid >= 160 && tid < 163) { plan->cur1[tid - 160] = 0; plan->cur2[tid - 160] = 0; }
     __syncthreads();
     const unsigned long long n0 = len ? N[0] : 0ull;  // a dense range is N[i] = n0 + ds i
@@ -1229,7 +1230,10 @@ classify_kernel(const unsigned long long* __restrict__ N, uint8_t* __restrict__ 
                                         spanm1, spanm1w, ntiles, sm, ws, lane, wid);
     __syncthreads();
     for (int b = tid; b < 65; b += CLS_THREADS)
+    {
+        q.segh[blockIdx.x * 65 + b] = sm.h[b];  // this segment's bins (the sort's offsets, no atomics there)
         if (sm.h[b]) atomicAdd(&plan->bins[b], sm.h[b]);
+    }
     if (tid == 0) {
         unsigned int c32 = 0;
         for (int b = 0; b <= 32; b++) c32 += sm.h[b];
@@ -1249,85 +1253,82 @@ classify_kernel(const unsigned long long* __restrict__ N, uint8_t* __restrict__ 
 // kernels (32-bit, FP64, Montgomery) become contiguous regions of s.  The
 // pass also gathers classify's per-block segments densely, and unpacks each
 // entry to its index in the chunk (4 bytes moved per survivor).
-constexpr int SORT_THREADS = 512;
-#ifndef SORT_TILE
-#define SORT_TILE 1024
-#endif
-#ifndef SORT_SPLIT
-#define SORT_SPLIT 4
-#endif
+constexpr int SORT_THREADS = 1024;
 
 __device__ __forceinline__ unsigned int bitlen32(uint32_t v) { return 32u - __clz(v); }
 __device__ __forceinline__ unsigned int bitlen64u(unsigned long long v) { return 64u - __clzll((long long)v); }
 
+// One block per classify segment g.  Its entries of bin b go to
+//   s[pre(b) + sum_{g' < g} segh[g'][b] + k],  k = 0 .. segh[g][b] - 1
+// (pre(b): entries of all smaller bins), so the block computes its 65
+// offsets once from the per-segment histograms classify published and then
+// places entries with shared-memory counters only: no global atomics, no
+// block barrier per tile.  Entries of one bin may land in any order (the
+// witness kernels need only the grouping by bit length).
 __global__ void __launch_bounds__(SORT_THREADS) qscatter_kernel(DevPlan* __restrict__ plan, Queues q, int nseg,
                                                                 uint32_t seg_stride) {
     pdl_wait();
     constexpr int NB = 65;
-    __shared__ unsigned int spre[NB], scnt[NB], sbase[NB];
+    __shared__ unsigned int scur[NB];
     const unsigned int total = plan->counts[0] + plan->counts[1];
     if (total == 0) return;  // nothing queued (a dense sieve window)
     const int tid = threadIdx.x, lane = tid & 31;
-    // exclusive prefix of the global bins (every block computes it)
-    if (tid == 0) {
-        unsigned int acc = 0;
-        for (int b = 0; b < NB; b++) { spre[b] = acc; acc += plan->bins[b]; }
-    }
-    for (int b = tid; b < NB; b += SORT_THREADS) scnt[b] = 0;
+    const int g = blockIdx.x;
+    // offsets: sum_{g' < g} segh[g'][b], spread over the block (thread t sums
+    // bin t % 65 over segments t / 65, t / 65 + 15, ...), then the global
+    // prefix of the smaller bins (three warps)
+    __shared__ unsigned int sbefore[NB], wsum[3];
+    if (tid < NB) sbefore[tid] = 0;
     __syncthreads();
-    constexpr int PER = SORT_TILE / SORT_THREADS;
-    // SORT_SPLIT blocks share a segment, taking its tiles in turn
-    const int part = blockIdx.x % SORT_SPLIT;
-    for (int g = blockIdx.x / SORT_SPLIT; g < nseg; g += gridDim.x / SORT_SPLIT) {
-        const unsigned int count = plan->seg[g];
-        const size_t sb = (size_t)g * seg_stride;
-        for (unsigned int t0 = part * SORT_TILE; t0 < count; t0 += SORT_SPLIT * SORT_TILE) {
-            // this block's next tile of the segment into L2 (segments start at
-            // multiples of CLS_TILE entries: 16-B aligned)
-            if (tid == 0 && t0 + SORT_SPLIT * SORT_TILE < count) {
-                const unsigned int nt = t0 + SORT_SPLIT * SORT_TILE;
-                const unsigned int cnt = (count - nt < (unsigned int)SORT_TILE ? count - nt : (unsigned int)SORT_TILE) & ~3u;
-                if (cnt) l2_prefetch_bulk(q.q + sb + nt, cnt * 4u);
-            }
-            uint32_t ent[PER];
+    constexpr int NJ = SORT_THREADS / NB;  // 15
+    if (tid < NJ * NB) {
+        const int b = tid % NB;
+        unsigned int acc = 0;
+        for (int g2 = tid / NB; g2 < g; g2 += NJ) acc += q.segh[g2 * NB + b];
+        if (acc) atomicAdd(&sbefore[b], acc);
+    }
+    __syncthreads();
+    if (tid < 96) {
+        const int b = tid;
+        const unsigned int tot = b < NB ? plan->bins[b] : 0u;
+        unsigned int incl = tot;
 #pragma unroll
-            for (int k = 0; k < PER; k++) {  // all loads in flight before any use
-                const unsigned int i = t0 + tid + k * SORT_THREADS;
-                ent[k] = i < count ? q.q[sb + i] : 0u;
-            }
-            unsigned int bin[PER], rank[PER];
+        for (int o = 1; o < 32; o <<= 1) {
+            const unsigned int y = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= o) incl += y;
+        }
+        if (lane == 31) wsum[tid >> 5] = incl;
+        asm volatile("bar.sync 1, 96;" ::: "memory");  // the three warps only
+        if (b < NB) scur[b] = incl - tot + sbefore[b] + (tid >= 32 ? wsum[0] : 0u) + (tid >= 64 ? wsum[1] : 0u);
+    }
+    __syncthreads();
+    const unsigned int count = plan->seg[g];
+    const size_t sb = (size_t)g * seg_stride;
+    constexpr int PER = 4;  // entries per thread per round, loads first
+    for (unsigned int i0 = 0; i0 < count; i0 += PER * SORT_THREADS) {
+        uint32_t ent[PER];
 #pragma unroll
-            for (int k = 0; k < PER; k++) {
-                const unsigned int i = t0 + tid + k * SORT_THREADS;
-                bin[k] = i < count ? (ent[k] >> 26) + 1u : (unsigned int)NB;  // sentinel: no element
-            }
-            // warp-aggregated ranks: one shared atomic per distinct bin in the warp
-            // (same-bin lanes would serialise on one address)
+        for (int k = 0; k < PER; k++) {
+            const unsigned int i = i0 + tid + k * SORT_THREADS;
+            ent[k] = i < count ? q.q[sb + i] : 0xFFFFFFFFu;
+        }
 #pragma unroll
-            for (int k = 0; k < PER; k++) {
-                const unsigned int peers = __match_any_sync(0xffffffffu, bin[k]);
-                const int leader = __ffs(peers) - 1;
-                unsigned int base = 0;
-                if (lane == leader && bin[k] < NB) base = atomicAdd(&scnt[bin[k]], (unsigned int)__popc(peers));
-                rank[k] = __shfl_sync(0xffffffffu, base, leader) + __popc(peers & ((1u << lane) - 1u));
+        for (int k = 0; k < PER; k++) {
+            const bool act = i0 + tid + k * SORT_THREADS < count;
+            const unsigned int bin = act ? (ent[k] >> 26) + 1u : (unsigned int)NB;  // sentinel: no element
+            // warp-aggregated: one shared atomic per distinct bin in the warp
+            const unsigned int peers = __match_any_sync(0xffffffffu, bin);
+            const int leader = __ffs(peers) - 1;
+            unsigned int base = 0;
+            if (lane == leader && act) base = atomicAdd(&scur[bin], (unsigned int)__popc(peers));
+            base = __shfl_sync(0xffffffffu, base, leader);
+            if (act) {
+                const unsigned int pos = base + __popc(peers & ((1u << lane) - 1u));
+                // tile = segment (classify block) + k * classify grid
+                const uint32_t tile = (uint32_t)g + ((ent[k] >> QE_TILE_BITS) & (QE_MAX_TILES - 1u)) * (uint32_t)nseg;
+                ISP_CHECK(pos < total && pos < q.cap, 201);
+                q.s[pos] = tile * (uint32_t)CLS_TILE + (ent[k] & (uint32_t)(CLS_TILE - 1));
             }
-            __syncthreads();
-            for (int b = tid; b < NB; b += SORT_THREADS)
-                if (scnt[b]) sbase[b] = spre[b] + atomicAdd(&plan->cur[b], scnt[b]);
-            __syncthreads();
-#pragma unroll
-            for (int k = 0; k < PER; k++) {
-                if (bin[k] < NB) {
-                    const unsigned int pos = sbase[bin[k]] + rank[k];
-                    // tile = segment (classify block) + k * classify grid
-                    const uint32_t tile = (uint32_t)g + ((ent[k] >> QE_TILE_BITS) & (QE_MAX_TILES - 1u)) * (uint32_t)nseg;
-                    ISP_CHECK(pos < total && pos < q.cap, 201);
-                    q.s[pos] = tile * (uint32_t)CLS_TILE + (ent[k] & (uint32_t)(CLS_TILE - 1));
-                }
-            }
-            __syncthreads();
-            for (int b = tid; b < NB; b += SORT_THREADS) scnt[b] = 0;
-            __syncthreads();
         }
     }
 }
