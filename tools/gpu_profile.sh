@@ -32,7 +32,7 @@ echo "full C2 rc=$?" >> gpurun_out/prof_status.txt
 # the C5 report itself is kept for per-line analysis
 TAG=${PROFILE_TAG:-latest}
 for c in C5 C4 C3 C2; do
-  [ -f gpurun_out/prof_$c.ncu-rep ] && python tools/ncu_summary.py gpurun_out/prof_$c.ncu-rep gpurun_out/r1_ncu_${c}_$TAG > /dev/null
+  [ -f gpurun_out/prof_$c.ncu-rep ] && python tools/ncu_summary.py gpurun_out/prof_$c.ncu-rep gpurun_out/${PROFILE_PREFIX:-r2}_ncu_${c}_$TAG > /dev/null
 done
 cp profiles/ncu_kernel_metrics.json gpurun_out/ 2>/dev/null
 rm -f gpurun_out/prof_C4.ncu-rep gpurun_out/prof_C3.ncu-rep gpurun_out/prof_C2.ncu-rep
