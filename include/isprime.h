@@ -106,6 +106,12 @@ void isprime_shutdown(void);
  *                    Jaeschke set {2, 13, 23, 1662803}; above, Eq 4.  Exact, so
  *                    it never changes a bit of out.  Applies to the pipeline's
  *                    witness kernels (the short-array path keeps Eq 4)
+ * "fuse_bits"        0, 32 (default) or 51: trial-division survivors below
+ *                    2^fuse_bits are not queued; the classify kernel runs the
+ *                    strong tests (base 2, then the remaining bases of the
+ *                    selected witness set) itself, per warp on rounds of 32, on
+ *                    the FP64 pipe.  0 queues every survivor for the witness
+ *                    kernels.  Same tests, same bases: never changes a bit of out
  * "small_max"        arrays with n <= small_max (default 131072) and force_path 0
  *                    take one fused launch (trial division + Miller-Rabin per
  *                    element) instead of the plan / sieve / queue pipeline;

@@ -44,6 +44,7 @@ struct Options {
     long long warp_max = 4096;      // n <= warp_max: one warp per element (one base per lane)
     int sched = 2;           // witness kernels: 0 dynamic guided claims (atomics), 1 static interleaved rounds,
                              // 2 static for the 32-bit class then dynamic for the 64-bit classes
+    int fuse_bits = 32;      // classify runs the strong tests itself below 2^fuse_bits: 0 (off), 32, 51
     int witness = 0;         // 0: Eq 4 bases; 1: Baillie-PSW for n >= 2^50; 2: reduced sets by magnitude     // 1: a call may reuse the bitmap sieved by an earlier call
 };
 
@@ -140,6 +141,7 @@ void read_env_once() {
     if (const char* e = getenv("ISPRIME_WIN64")) g_opt.win64 = atoi(e);
     if (const char* e = getenv("ISPRIME_CHUNK_LOG2")) g_opt.chunk_log2 = atoi(e);
     if (const char* e = getenv("ISPRIME_SIEVE_MAX")) g_opt.sieve_max = strtoull(e, nullptr, 0);
+    if (const char* e = getenv("ISPRIME_FUSE_BITS")) { const int v = atoi(e); if (v == 0 || v == 32 || v == 51) g_opt.fuse_bits = v; }
 }
 
 int cuda_fail(cudaError_t e, const char* what) {
@@ -329,7 +331,11 @@ template <typename K>
 void launch_cls(K k, int g, cudaStream_t s, const unsigned long long* N, uint8_t* out, uint32_t len, Ctx* c,
                 const TDParams& td, int vin, int vout, uint32_t ss) {
     cudaFuncSetAttribute((const void*)k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(ClsSmem));
-    launch_k(k, g, CLS_THREADS, sizeof(ClsSmem), s, N, out, len, c->plan, c->bitmap, c->q, td, vin, vout, ss);
+    FzParams fz;
+    fz.bits = g_opt.fuse_bits;
+    fz.p2 = (g_opt.witness == 2 && g_opt.bases32 != 7) ? 2 : g_opt.bases32 == 7 ? 1 : 0;
+    fz.wit = g_opt.witness;
+    launch_k(k, g, CLS_THREADS, sizeof(ClsSmem), s, N, out, len, c->plan, c->bitmap, c->q, td, vin, vout, ss, fz);
 }
 
 template <int A>
@@ -702,6 +708,7 @@ int isprime_set_option(const char* key, long long v) {
     else if (!strcmp(key, "warp_max")) { if (v < 0 || v > (1 << 26)) return ISP_EINVAL; g_opt.warp_max = v; }
     else if (!strcmp(key, "witness")) { if (v < 0 || v > 2) return ISP_EINVAL; g_opt.witness = (int)v; }
     else if (!strcmp(key, "sched")) { if (v < 0 || v > 2) return ISP_EINVAL; g_opt.sched = (int)v; }
+    else if (!strcmp(key, "fuse_bits")) { if (v != 0 && v != 32 && v != 51) return ISP_EINVAL; g_opt.fuse_bits = (int)v; }
     else return ISP_EINVAL;
     return ISP_OK;
 }
@@ -729,6 +736,7 @@ long long isprime_get_option(const char* key) {
     if (!strcmp(key, "warp_max")) return g_opt.warp_max;
     if (!strcmp(key, "witness")) return g_opt.witness;
     if (!strcmp(key, "sched")) return g_opt.sched;
+    if (!strcmp(key, "fuse_bits")) return g_opt.fuse_bits;
     return -1;
 }
 
@@ -745,10 +753,10 @@ int isprime_get_stats(isprime_stats* st) {
     st->window_hi = p.whi;
     st->sieve_runs = p.sieve_runs;
     st->sieved_integers = p.sieved_ints;
-    st->queued32 = p.total[0] + p.counts[0];
-    st->queued64 = p.total[1] + p.counts[1];
-    st->passed32 = p.total[2] + p.counts[2];
-    st->passed64 = p.total[3] + p.counts[3] + p.pf;
+    st->queued32 = p.total[0] + p.counts[0] + p.fzt[0];
+    st->queued64 = p.total[1] + p.counts[1] + p.fzt[1];
+    st->passed32 = p.total[2] + p.counts[2] + p.fzt[2];
+    st->passed64 = p.total[3] + p.counts[3] + p.pf + p.fzt[3];
     st->chunks = p.chunks;
     st->kernel_launches = g_launches;
     for (int k = 0; k < 4; k++) st->mulmods[k] = p.work[k];
@@ -765,7 +773,8 @@ int isprime_reset_stats(void) {
     CK(cudaDeviceSynchronize());
     DevPlan p;
     CK(cudaMemcpy(&p, c->plan, sizeof(p), cudaMemcpyDeviceToHost));
-    for (int k = 0; k < 4; k++) { p.total[k] = 0; p.counts[k] = 0; }
+    for (int k = 0; k < 4; k++) { p.total[k] = 0; p.counts[k] = 0; p.fzt[k] = 0; }
+    p.pf = 0;  // FP64-class base-2 passes of the last chunk (added to total[3] by the next plan)
     p.sieve_runs = 0;
     p.sieved_ints = 0;
     p.chunks = 0;

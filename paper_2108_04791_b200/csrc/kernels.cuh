@@ -107,6 +107,9 @@ struct DevPlan {
     // classify writes survivors into per-block segments (no block barrier):
     // entries used by block b of the last classify launch
     unsigned int seg[MAX_SEG];
+    // fused witness tests in classify (option fuse_bits), accumulated: base-2
+    // tests (32-bit class, FP64 class), base-2 passes (32-bit class, FP64 class)
+    unsigned long long fzt[4];
 };
 
 // Host -> plan kernel parameters (cost model in picoseconds on a full GPU).
@@ -920,24 +923,155 @@ struct ClsWarp {
     uint8_t pos[256];             // element offset within the warp-tile
     uint8_t res[256];             // results of the warp-tile, element order
 };
+// Fused witness tests (option "fuse_bits", round 2): trial-division survivors
+// below 2^fuse_bits are not queued; each warp collects them in private
+// shared-memory lists and runs the strong tests itself on full warps of 32
+// -- base 2 on list a, then the remaining bases on the passers, by class (b:
+// n < 2^32, c: the FP64 class 2^32 <= n < 2^51) -- in the FP64 arithmetic of
+// the witness kernels (sprp2_f64 / sprp_multi_f64).  No queue traffic, no
+// sort, no witness-kernel launch for these classes, and the FP64 pipe works
+// beside classify's integer instructions.
+constexpr uint32_t FZ_CAP = 64;
+struct FzWarp {
+    unsigned long long av[FZ_CAP], bv[FZ_CAP], cv[FZ_CAP];
+    uint32_t ai[FZ_CAP], bi[FZ_CAP], ci[FZ_CAP];  // element index in the chunk
+};
+struct FzParams {
+    int bits;     // 0: off (everything queued); 32: n < 2^32; 51: n < FP_LIMIT
+    int p2;       // remaining bases below 2^32: 0 {7, 61}; 1 the six of Eq 4; 2 one hashed base
+    int wit;      // option witness (2: Jaeschke's set below kJaeschkeBound4 in the FP64 class)
+};
 struct ClsSmem {
     ClsWarp w[CLS_THREADS / 32];
+    FzWarp f[CLS_THREADS / 32];
     unsigned int cur;     // entries used in this block's queue segment
     unsigned int h[65];   // bit-length histogram of this block's survivors (for the sort)
+    unsigned int fzc[4];  // fused: base-2 tests (32-bit, FP64 class), base-2 passes (32-bit, FP64 class)
 };
 
-// The tile loop of classify_kernel.  UNI (the chunk has no sieve window):
-// warp-tiles whose values are all below 2^32 or all at or above take a
-// shorter classification; a separate instantiation keeps the general loop's
-// code unchanged for chunks with a window.
+// Append the lanes with pred to list (v, i) of n entries (warp-uniform n).
+__device__ __forceinline__ void fz_push(bool pred, unsigned long long x, uint32_t idx, unsigned long long* v,
+                                        uint32_t* ix, uint32_t& n, int lane) {
+    const uint32_t m = __ballot_sync(0xffffffffu, pred);
+    if (pred) {
+        const uint32_t k = n + __popc(m & ((1u << lane) - 1u));
+        v[k] = x;
+        ix[k] = idx;
+    }
+    n += __popc(m);
+    __syncwarp();
+}
+
+// Take the first min(n, 32) entries of a list (lane l gets entry l), shift the rest down.
+__device__ __forceinline__ bool fz_take(unsigned long long* v, uint32_t* ix, uint32_t& n, int lane,
+                                        unsigned long long& x, uint32_t& idx) {
+    const uint32_t cnt = n < 32u ? n : 32u;
+    const bool act = (uint32_t)lane < cnt;
+    x = act ? v[lane] : 0ull;
+    idx = act ? ix[lane] : 0u;
+    __syncwarp();
+    if ((uint32_t)lane + 32u < n) { v[lane] = v[lane + 32]; ix[lane] = ix[lane + 32]; }
+    n -= cnt;
+    __syncwarp();
+    return act;
+}
+
+// A prime's result: into the warp's result tile while that tile is still to
+// be stored (element indices [tlo, tlo + 256)), straight to out otherwise.
+__device__ __forceinline__ void fz_mark(uint32_t idx, uint32_t tlo, uint8_t* res, uint8_t* __restrict__ out) {
+    if (idx - tlo < 256u) res[idx - tlo] = 1;
+    else out[idx] = 1;
+}
+
+// List lengths of a warp packed in one register (the helpers below are not
+// inlined: counts passed by reference would live in local memory):
+// bits 0-7 list a, 8-15 list b, 16-23 list c (each < FZ_CAP + 32 <= 255).
+__device__ __forceinline__ uint32_t fz_na(uint32_t z) { return z & 0xFFu; }
+__device__ __forceinline__ uint32_t fz_nb(uint32_t z) { return (z >> 8) & 0xFFu; }
+__device__ __forceinline__ uint32_t fz_nc(uint32_t z) { return z >> 16; }
+
+// One round of the remaining bases on list b (n < 2^32) or c (FP64 class).
+__device__ __forceinline__ uint32_t fz_phase2(FzWarp& f, uint32_t z, bool cls_c, FzParams fp, uint32_t tlo,
+                                           uint8_t* res, uint8_t* __restrict__ out) {
+    const int lane = threadIdx.x & 31;
+    unsigned long long n;
+    uint32_t idx, k = cls_c ? fz_nc(z) : fz_nb(z);
+    const bool act = cls_c ? fz_take(f.cv, f.ci, k, lane, n, idx) : fz_take(f.bv, f.bi, k, lane, n, idx);
+    z = cls_c ? ((z & 0xFFFFu) | (k << 16)) : ((z & 0xFFFF00FFu) | (k << 8));
+    if (act) {
+        bool prime;
+        if (!cls_c) {
+            if (fp.p2 == 2) {
+                const unsigned long long a = hash_base32((uint32_t)n);
+                prime = sprp_multi_f64<1, 1, 2>(n, &a);
+            } else if (fp.p2 == 1) {
+                prime = sprp_multi_f64<6, 3, 2>(n, c_bases64);
+            } else {
+                prime = sprp_multi_f64<2, 2, 2>(n, c_bases32_red64);
+            }
+        } else {
+            prime = (fp.wit == 2 && n < kJaeschkeBound4) ? sprp_multi_f64<3, 3, 2>(n, c_bases_j4)
+                                                          : sprp_multi_f64<6, 3, 2>(n, c_bases64);
+        }
+        if (prime) fz_mark(idx, tlo, res, out);
+    }
+    return z;
+}
+
+// One round of base 2 on list a; the passers go to b or c by class.
+__device__ __forceinline__ uint32_t fz_base2(FzWarp& f, uint32_t z, unsigned int* fzc) {
+    const int lane = threadIdx.x & 31;
+    unsigned long long n;
+    uint32_t idx, na = fz_na(z), nb = fz_nb(z), nc = fz_nc(z);
+    const bool act = fz_take(f.av, f.ai, na, lane, n, idx);
+    bool pass = false;
+    if (act) pass = sprp2_f64(n);
+    const bool small = n < (1ull << 32);
+    const uint32_t m32 = __ballot_sync(0xffffffffu, pass && small), mf = __ballot_sync(0xffffffffu, pass && !small);
+    fz_push(pass && small, n, idx, f.bv, f.bi, nb, lane);
+    fz_push(pass && !small, n, idx, f.cv, f.ci, nc, lane);
+    if (lane == 0 && (m32 | mf)) {
+        if (m32) atomicAdd(&fzc[2], (unsigned int)__popc(m32));
+        if (mf) atomicAdd(&fzc[3], (unsigned int)__popc(mf));
+    }
+    return na | (nb << 8) | (nc << 16);
+}
+
+// Run every full round the lists hold.
+__device__ __forceinline__ uint32_t fz_drain(FzWarp& f, uint32_t z, unsigned int* fzc, FzParams fp, uint32_t tlo,
+                                             uint8_t* res, uint8_t* __restrict__ out) {
+    while (fz_na(z) >= 32u) {
+        z = fz_base2(f, z, fzc);
+        while (fz_nb(z) >= 32u) z = fz_phase2(f, z, false, fp, tlo, res, out);
+        while (fz_nc(z) >= 32u) z = fz_phase2(f, z, true, fp, tlo, res, out);
+    }
+    return z;
+}
+
+// Every round left, partial ones too (once per warp, after its last tile:
+// not inlined, so the tile loop's registers are not shaped by a second copy).
+__device__ __noinline__ void fz_flush(FzWarp& f, uint32_t z, unsigned int* fzc, FzParams fp,
+                                      uint8_t* __restrict__ out) {
+    constexpr uint32_t tlo = 0xFFFFFF00u;  // no tile pending: every result goes to out
+    while (fz_na(z)) {
+        z = fz_base2(f, z, fzc);
+        while (fz_nb(z) >= 32u) z = fz_phase2(f, z, false, fp, tlo, nullptr, out);
+        while (fz_nc(z) >= 32u) z = fz_phase2(f, z, true, fp, tlo, nullptr, out);
+    }
+    while (fz_nb(z)) z = fz_phase2(f, z, false, fp, tlo, nullptr, out);
+    while (fz_nc(z)) z = fz_phase2(f, z, true, fp, tlo, nullptr, out);
+}
+
 template <int N32, int N64, bool UNI>
 __device__ __forceinline__ void classify_tiles(const unsigned long long* __restrict__ N, uint8_t* __restrict__ out,
                                                uint32_t len, const uint32_t* __restrict__ bitmap, const Queues& q,
                                                const TDParams& td, int vec_in, int vec_out, uint32_t seg_stride,
                                                uint32_t segbase, unsigned long long span, uint32_t wlo32,
                                                uint32_t spanm1, uint32_t spanm1w, uint32_t ntiles, ClsSmem& sm,
-                                               ClsWarp& ws, int lane, int wid) {
+                                               ClsWarp& ws, int lane, int wid, FzParams fz) {
     uint32_t tk = 0;  // tile number within this block (packed queue entries)
+    FzWarp& fw = sm.f[wid];
+    uint32_t z = 0;   // fused lists' lengths (fz_na / fz_nb / fz_nc)
     for (uint32_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, tk++) {
         const uint32_t wbase = tile * CLS_TILE + 256u * wid;
         const bool full = wbase + 256u <= len;
@@ -1122,6 +1256,11 @@ __device__ __forceinline__ void classify_tiles(const unsigned long long* __restr
             // length (the sort key); the value itself is re-read from N by the
             // witness kernels.
             const uint32_t tag = (tk << QE_TILE_BITS) | (256u * wid);
+            uint32_t s32 = 0, s64 = 0;  // fused: survivors compacted in list32 / list64
+            // fused 32-bit class only for warp-tiles with at least a round of
+            // candidates (config C2: ~128); a few per tile (C5: the window takes
+            // most small values) cost classify more than the queue round trip
+            const bool fz32 = fz.bits && n32 >= 32u;
             for (uint32_t k0 = 0; k0 < n32; k0 += 32) {
                 const uint32_t k = k0 + lane;
                 bool surv = false;
@@ -1145,7 +1284,19 @@ __device__ __forceinline__ void classify_tiles(const unsigned long long* __restr
                 }
                 surv &= !small;
                 const uint32_t m = __ballot_sync(0xffffffffu, surv);
-                if (m) {
+                if (fz32) {
+                    // fused: survivors compacted to the front of list32 (in
+                    // place: slot s32 + rank <= k), tested at the end of the tile
+                    if (surv) {
+                        const uint32_t j = s32 + __popc(m & ((1u << lane) - 1u));
+                        const uint8_t pk = ws.pos[k];
+                        __syncwarp(m);
+                        ws.val[j] = x;
+                        ws.pos[j] = pk;
+                    }
+                    s32 += __popc(m);
+                    __syncwarp();
+                } else if (m) {
                     uint32_t o = 0;
                     if (lane == 0) o = atomicAdd(&sm.cur, (unsigned int)__popc(m));
                     o = segbase + __shfl_sync(0xffffffffu, o, 0);
@@ -1162,11 +1313,25 @@ __device__ __forceinline__ void classify_tiles(const unsigned long long* __restr
                 const uint32_t k = k0 + lane;  // back index: slot 255 - k
                 bool surv = false;
                 unsigned long long x = 0;
+                const uint8_t pk = ws.pos[255u - k];  // read before the fused compaction below rewrites slots
                 if (k < n64) {
                     x = ws.val[255u - k];
                     bool comp = false;
                     if (N64 > 0) comp = td64_fp<N64>(x, td.rnd);
                     surv = !comp;
+                }
+                if (fz.bits > 32) {
+                    // fused FP64 class: compacted to the back of list64 (slot 255 - s64)
+                    const bool tofz = surv && x < FP_LIMIT;
+                    const uint32_t mf = __ballot_sync(0xffffffffu, tofz);
+                    if (tofz) {
+                        const uint32_t j = 255u - (s64 + __popc(mf & ((1u << lane) - 1u)));
+                        ws.val[j] = x;
+                        ws.pos[j] = pk;
+                    }
+                    s64 += __popc(mf);
+                    __syncwarp();
+                    surv &= !tofz;
                 }
                 const uint32_t m = __ballot_sync(0xffffffffu, surv);
                 if (m) {
@@ -1177,9 +1342,31 @@ __device__ __forceinline__ void classify_tiles(const unsigned long long* __restr
                         const uint32_t at = o + __popc(m & ((1u << lane) - 1u));
                         const uint32_t bl = 64u - __clzll((long long)x);
                         ISP_CHECK(at < segbase + seg_stride && at < q.cap, 102);
-                        q.q[at] = (tag + ws.pos[255u - k]) | ((bl - 1u) << 26);
+                        q.q[at] = (tag + pk) | ((bl - 1u) << 26);
                         atomicAdd(&sm.h[bl], 1u);
                     }
+                }
+            }
+            // fused: this tile's survivors join list a (< 32 entries between
+            // rounds), full rounds run at once; results of this tile's elements
+            // land in ws.res before the tile is stored below
+            const uint32_t ns = s32 + s64;
+            if (ns) {
+                if (lane == 0) {
+                    if (s32) atomicAdd(&sm.fzc[0], s32);
+                    if (s64) atomicAdd(&sm.fzc[1], s64);
+                }
+                for (uint32_t k0 = 0; k0 < ns; k0 += 32) {
+                    const uint32_t k = k0 + lane;
+                    const bool valid = k < ns;
+                    const uint32_t j = k < s32 ? k : 255u - (k - s32);
+                    unsigned long long x = 0;
+                    uint32_t idx = 0;
+                    if (valid) { x = ws.val[j]; idx = wbase + ws.pos[j]; }
+                    uint32_t na = fz_na(z);
+                    fz_push(valid, x, idx, fw.av, fw.ai, na, lane);
+                    z = (z & ~0xFFu) | na;
+                    if (na >= 32u) z = fz_drain(fw, z, sm.fzc, fz, wbase, ws.res, out);
                 }
             }
         }
@@ -1196,13 +1383,15 @@ __device__ __forceinline__ void classify_tiles(const unsigned long long* __restr
             __syncwarp();  // the next warp-tile rewrites this warp's lists
         }
     }
+    // fused lists: the partial rounds left (every tile is stored: results go to out)
+    if (z) fz_flush(fw, z, sm.fzc, fz, out);
 }
 
 template <int N32, int N64>
 __global__ void __launch_bounds__(CLS_THREADS)
 classify_kernel(const unsigned long long* __restrict__ N, uint8_t* __restrict__ out, uint32_t len,
                 DevPlan* __restrict__ plan, const uint32_t* __restrict__ bitmap, Queues q, TDParams td,
-                int vec_in, int vec_out, uint32_t seg_stride) {
+                int vec_in, int vec_out, uint32_t seg_stride, FzParams fz) {
     pdl_wait();
     extern __shared__ __align__(16) unsigned char cls_smem[];  // sizeof(ClsSmem), dynamic (> 48 KB at 1024 threads)
     ClsSmem& sm = *reinterpret_cast<ClsSmem*>(cls_smem);
@@ -1221,19 +1410,21 @@ classify_kernel(const unsigned long long* __restrict__ N, uint8_t* __restrict__ 
     const uint32_t ntiles = (len + CLS_TILE - 1) / CLS_TILE;
     for (int b = tid; b < 65; b += CLS_THREADS) sm.h[b] = 0;
     if (tid == 0) sm.cur = 0;
+    if (tid < 4) sm.fzc[tid] = 0;
     __syncthreads();
     if (span == 0)
         classify_tiles<N32, N64, true>(N, out, len, bitmap, q, td, vec_in, vec_out, seg_stride, segbase, span, wlo32,
-                                       spanm1, spanm1w, ntiles, sm, ws, lane, wid);
+                                       spanm1, spanm1w, ntiles, sm, ws, lane, wid, fz);
     else
         classify_tiles<N32, N64, false>(N, out, len, bitmap, q, td, vec_in, vec_out, seg_stride, segbase, span, wlo32,
-                                        spanm1, spanm1w, ntiles, sm, ws, lane, wid);
+                                        spanm1, spanm1w, ntiles, sm, ws, lane, wid, fz);
     __syncthreads();
     for (int b = tid; b < 65; b += CLS_THREADS)
     {
         q.segh[blockIdx.x * 65 + b] = sm.h[b];  // this segment's bins (the sort's offsets, no atomics there)
         if (sm.h[b]) atomicAdd(&plan->bins[b], sm.h[b]);
     }
+    if (tid < 4 && sm.fzc[tid]) atomicAdd(&plan->fzt[tid], (unsigned long long)sm.fzc[tid]);
     if (tid == 0) {
         unsigned int c32 = 0;
         for (int b = 0; b <= 32; b++) c32 += sm.h[b];

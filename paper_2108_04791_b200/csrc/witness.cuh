@@ -288,9 +288,45 @@ __device__ __forceinline__ bool sprp_multi64(uint64_t n, const unsigned long lon
 }
 
 // ------------------------------------------------------- FP64 class ----
-// The same two phases on the FP64 pipe for odd n < 2^50 (modmath.cuh, ModF):
+// The same two phases on the FP64 pipe for odd n < 2^51 (modmath.cuh, ModF):
 // plain residues (no Montgomery form) kept as signed lazy representatives
 // |x| < n, so 1 is 1.0 or 1 - n and -1 is -1.0 or n - 1.
+//
+// Base-2 ladder in K-bit windows (round 2).  2^d = prod over the windows of d
+// (MSB first) of x <- x^(2^K) * 2^digit, and the factor 2^digit folds into
+// the window's last squaring as an exact power-of-two scaling of one factor
+// (an exponent-field add, fscale2): fmul_lazy(2^digit x, x).  fmul_lazy's
+// bound (modmath.cuh) holds for |a| < 2^e n, |b| < n when e + bitlen(n) <= 51:
+// |h / n| < 2^(e + bitlen n) <= 2^51 keeps the rounding addend valid, and
+// (h / n) 2^-53 and |l| / n stay <= 2^(e + bitlen n - 53) <= 1/4, so
+// |q - ab/n| < 1 and |r| < n.  With digits up to 2^K - 1, K = 4 serves
+// bitlen(n) <= 36, K = 3 <= 44, K = 2 <= 48; above, one bit per step as
+// before.  Per exponent bit: one product (6 FP64-pipe instructions) and 1/K of
+// the window bookkeeping, instead of a product and a scaling every bit.
+__device__ __forceinline__ double fscale2(double x, uint32_t e) {
+    return __hiloint2double(__double2hiint(x) + (int)(e << 20), __double2loint(x));
+}
+
+template <int K>
+__device__ __forceinline__ double f2_pow_win(unsigned long long d, const ModF& M) {
+    const int nb = 64 - __clzll((long long)d);  // d odd >= 1
+    const int nw = (nb + K - 1) / K;
+    const uint32_t top = (uint32_t)(d >> (K * (nw - 1)));  // 1 .. 2^K - 1
+    double x = __hiloint2double((int)((1023u + top) << 20), 0);  // 2^top, exact
+    {  // 2^top may exceed a small n: one exact reduction, |x| <= n / 2 + 1 < n
+        const double q = fma(x, M.ninv, FP_RND) - FP_RND;
+        x = fma(-q, M.n, x);
+    }
+#pragma unroll 1
+    for (int w = nw - 2; w >= 0; w--) {
+        const uint32_t dig = (uint32_t)(d >> (K * w)) & ((1u << K) - 1u);
+#pragma unroll
+        for (int j = 0; j < K - 1; j++) x = fmul_lazy(x, x, M);
+        x = fmul_lazy(fscale2(x, dig), x, M);
+    }
+    return x;
+}
+
 __device__ __forceinline__ bool sprp2_f64(unsigned long long n) {
     const ModF M = modf_setup(n);
     unsigned long long d = n - 1;
@@ -299,9 +335,17 @@ __device__ __forceinline__ bool sprp2_f64(unsigned long long n) {
     const int top = 63 - __clzll((long long)d);
     // signed lazy residues (fmul_lazy): |x| < n throughout, no per-step correction
     double x = 2.0;  // top bit of d
-    if (top > 0) {
+    // window width from the warp's largest n (warp-uniform: no divergence)
+    const int bmax = (int)__reduce_max_sync(__activemask(), (unsigned)(64 - __clzll((long long)n)));
+    if (bmax <= 36) {
+        x = f2_pow_win<4>(d, M);
+    } else if (bmax <= 44) {
+        x = f2_pow_win<3>(d, M);
+    } else if (bmax <= 48) {
+        x = f2_pow_win<2>(d, M);
+    } else if (top > 0) {
         unsigned long long dd = d << (64 - top);  // remaining bits, MSB first
-        if (!__any_sync(__activemask(), (unsigned)(n >> 50))) {
+        if (bmax <= 50) {
             // n < 2^50: the doubling folded into the product (|2x| < 2n is allowed)
             for_bits_msb(dd, top, [&](uint32_t w) { x = fsqr_dbl_lazy(x, w, M); });
         } else {

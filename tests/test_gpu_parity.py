@@ -52,7 +52,7 @@ def assert_same(got, exp, N=None):
 def _default_options():
     saved = {k: isp.get_option(k) for k in ("force_path", "bases32", "td_primes32", "td_primes64",
                                              "chunk_log2", "win64", "warp_p", "small_max", "warp_max",
-                                             "witness", "sieve_cache", "sched")}
+                                             "witness", "sieve_cache", "sched", "fuse_bits")}
     yield
     for k, v in saved.items():
         isp.set_option(k, v)
@@ -590,12 +590,60 @@ def test_options_do_not_change_results():
     exp = oracle.isprime(N)
     for key, vals in (("td_primes32", (0, 1, 5, 128)), ("td_primes64", (0, 3, 128)), ("win64", (1, 2, 3)),
                       ("force_path", (0, 1, 2)), ("chunk_log2", (16, 17, 28)), ("warp_p", (17, 600, 65536)),
-                      ("witness", (1, 2, 0)), ("sched", (0, 1, 2))):
+                      ("witness", (1, 2, 0)), ("sched", (0, 1, 2)), ("fuse_bits", (0, 51, 32))):
         saved = isp.get_option(key)
         for v in vals:
             isp.set_option(key, v)
             assert_same(gpu(N), exp, N)
         isp.set_option(key, saved)
+
+
+# ------------------------------------------------------------------ fused witness tests in classify
+@pytest.mark.parametrize("fuse_bits", [0, 32, 51])
+@pytest.mark.parametrize("witness,bases32", [(0, 3), (0, 7), (1, 3), (2, 3), (2, 7)])
+def test_fused_classes_every_witness_mode(fuse_bits, witness, bases32):
+    """Option fuse_bits: classify runs base 2 and the remaining bases itself
+    for trial-division survivors below 2^fuse_bits (per-warp lists, rounds of
+    32, kernels.cuh FzWarp).  Every element against the oracle on a C5 / C2
+    mix, the class boundaries 2^32 and 2^51, the strong pseudoprimes and
+    Chernick numbers (base-2 passers that must fail a later base), and runs of
+    consecutive primes -- every list slot a survivor, so a warp-tile carries
+    more survivors than one round and rounds straddle tiles."""
+    isp.set_option("small_max", 0)
+    isp.set_option("fuse_bits", fuse_bits)
+    isp.set_option("witness", witness)
+    isp.set_option("bases32", bases32)
+    sp2 = np.array([int(r[0]) for r in _rows("special_values.txt")], dtype=np.uint64)
+    cs = np.array(workloads.chernick_numbers(), dtype=np.uint64)
+    s32 = oracle.sieve(1 << 22)
+    primes_small = np.nonzero(s32)[0].astype(np.uint64)[-40_000:]  # consecutive primes below 2^22
+    near = np.concatenate([np.arange(c - 20_001, c + 20_001, 2, dtype=np.uint64) for c in (2**32, 2**51)])
+    N = np.concatenate([workloads.generate("C5", count=200_003), workloads.generate("C2", count=100_000),
+                        np.tile(np.concatenate([sp2, cs]), 9), primes_small, near])
+    exp = oracle.isprime(N)
+    assert_same(gpu(N), exp, N)
+    st0 = isp.get_stats()
+    assert st0["passed32"] <= st0["queued32"] and st0["passed64"] <= st0["queued64"]
+    # every element a prime below 2^32 (no window for the tail: force the MR path)
+    isp.set_option("force_path", 2)
+    P = np.tile(primes_small, 3)
+    assert_same(gpu(P), np.ones(P.shape[0], dtype=np.uint8), P)
+
+
+def test_fused_stats_count_like_the_queues():
+    """fuse_bits moves the witness tests, not the counts: trial-division
+    survivors and base-2 passes per class are the same numbers with the lists
+    in classify as with the queues and witness kernels."""
+    isp.set_option("small_max", 0)
+    N = np.concatenate([workloads.generate("C5", count=1 << 20), workloads.generate("C2", count=1 << 18)])
+    res = {}
+    for fb in (0, 32, 51):
+        isp.set_option("fuse_bits", fb)
+        isp.reset_stats()
+        gpu(N)
+        st = isp.get_stats()
+        res[fb] = tuple(st[k] for k in ("queued32", "queued64", "passed32", "passed64"))
+    assert res[0] == res[32] == res[51], res
 
 
 # ------------------------------------------------------------------ boundary edge cases
