@@ -181,6 +181,13 @@ cudaError_t launch_k(void (*k)(KArgs...), unsigned grid, unsigned block, size_t 
     return cudaLaunchKernelEx(&cfg, k, static_cast<KArgs>(args)...);
 }
 
+// mr2_kernel's small-base table lives in dynamic shared memory beside 48 KB of
+// static tables: the launch needs the opt-in attribute.
+template <typename K>
+void mr2_attr(K k) {
+    cudaFuncSetAttribute((const void*)k, cudaFuncAttributeMaxDynamicSharedMemorySize, MR2_DYN_SMEM);
+}
+
 int occupancy(const void* fn, int threads, size_t smem) {
     int b = 0;
     if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, fn, threads, smem) != cudaSuccess || b < 1) b = 1;
@@ -241,7 +248,8 @@ int init_ctx(Ctx* c) {
     if (c->grid_cls > MAX_SEG) c->grid_cls = MAX_SEG;  // one queue segment per classify block
     c->grid_mr1 = c->sms * occupancy((const void*)mr1_kernel, MR1_THREADS, 0);
     c->grid_sort = c->sms * occupancy((const void*)qscatter_kernel, SORT_THREADS, 0);
-    c->grid_mr2 = c->sms * occupancy((const void*)mr2_kernel<2, false, 3>, MR_THREADS, 0);
+    mr2_attr(mr2_kernel<2, false, 3>);
+    c->grid_mr2 = c->sms * occupancy((const void*)mr2_kernel<2, false, 3>, MR_THREADS, MR2_DYN_SMEM);
     CK(cudaEventCreateWithFlags(&c->last_done, cudaEventDisableTiming));
     for (int k = 0; k < 2; k++) {
         CK(cudaStreamCreateWithFlags(&c->hs[k], cudaStreamNonBlocking));
@@ -364,8 +372,13 @@ void launch_classify(int n32, int n64, int g, cudaStream_t s, const unsigned lon
 template <int WIN, int G>
 void launch_mr2_w(Ctx* c, cudaStream_t s, const unsigned long long* N, uint8_t* out, uint32_t len, int grid, bool full,
                   int cw) {
-    if (full) launch_k(mr2_kernel<WIN, true, G>, grid, MR_THREADS, 0, s, c->plan, c->q, N, out, len, cw, g_opt.sched);
-    else launch_k(mr2_kernel<WIN, false, G>, grid, MR_THREADS, 0, s, c->plan, c->q, N, out, len, cw, g_opt.sched);
+    if (full) {
+        mr2_attr(mr2_kernel<WIN, true, G>);
+        launch_k(mr2_kernel<WIN, true, G>, grid, MR_THREADS, MR2_DYN_SMEM, s, c->plan, c->q, N, out, len, cw, g_opt.sched);
+    } else {
+        mr2_attr(mr2_kernel<WIN, false, G>);
+        launch_k(mr2_kernel<WIN, false, G>, grid, MR_THREADS, MR2_DYN_SMEM, s, c->plan, c->q, N, out, len, cw, g_opt.sched);
+    }
 }
 
 int launch_mr2(Ctx* c, cudaStream_t s, const unsigned long long* N, uint8_t* out, uint32_t len, int grid) {
@@ -373,14 +386,18 @@ int launch_mr2(Ctx* c, cudaStream_t s, const unsigned long long* N, uint8_t* out
     const int cw = g_opt.kernel_timing;
     const int g = g_opt.mr2_group == 6 ? 6 : 3;
     if (g_opt.witness == 1) {  // Baillie-PSW for the 64-bit Montgomery class
-        if (full) launch_k(mr2_kernel<3, true, 3, 1>, grid, MR_THREADS, 0, s, c->plan, c->q, N, out, len, cw, g_opt.sched);
-        else launch_k(mr2_kernel<3, false, 3, 1>, grid, MR_THREADS, 0, s, c->plan, c->q, N, out, len, cw, g_opt.sched);
+        mr2_attr(mr2_kernel<3, true, 3, 1>);
+        mr2_attr(mr2_kernel<3, false, 3, 1>);
+        if (full) launch_k(mr2_kernel<3, true, 3, 1>, grid, MR_THREADS, MR2_DYN_SMEM, s, c->plan, c->q, N, out, len, cw, g_opt.sched);
+        else launch_k(mr2_kernel<3, false, 3, 1>, grid, MR_THREADS, MR2_DYN_SMEM, s, c->plan, c->q, N, out, len, cw, g_opt.sched);
         CKL("mr2_kernel");
         return ISP_OK;
     }
     if (g_opt.witness == 2) {  // reduced witness sets by magnitude
-        if (full) launch_k(mr2_kernel<3, true, 3, 2>, grid, MR_THREADS, 0, s, c->plan, c->q, N, out, len, cw, g_opt.sched);
-        else launch_k(mr2_kernel<3, false, 3, 2>, grid, MR_THREADS, 0, s, c->plan, c->q, N, out, len, cw, g_opt.sched);
+        mr2_attr(mr2_kernel<3, true, 3, 2>);
+        mr2_attr(mr2_kernel<3, false, 3, 2>);
+        if (full) launch_k(mr2_kernel<3, true, 3, 2>, grid, MR_THREADS, MR2_DYN_SMEM, s, c->plan, c->q, N, out, len, cw, g_opt.sched);
+        else launch_k(mr2_kernel<3, false, 3, 2>, grid, MR_THREADS, MR2_DYN_SMEM, s, c->plan, c->q, N, out, len, cw, g_opt.sched);
         CKL("mr2_kernel");
         return ISP_OK;
     }
@@ -463,7 +480,8 @@ int device_impl(Ctx* c, const unsigned long long* dN, uint8_t* dout, size_t n, c
             launch_k(plan_kernel, 1, PLAN_THREADS, 0, s, N, (unsigned long long)len, c->plan, P);
             CKL("plan_kernel");
         }
-        {
+        static const int exp_skip = getenv("ISPRIME_EXP_SKIP") ? atoi(getenv("ISPRIME_EXP_SKIP")) : 0;  // TEMP experiment
+        if (!(exp_skip & 1)) {
             KScope ks(K_SIEVE, s);
             // first base prime >= warp_p (the warp-cooperative / per-thread split)
             int first_large = FIRST_CROSS_PRIME_IDX;
@@ -472,7 +490,7 @@ int device_impl(Ctx* c, const unsigned long long* dN, uint8_t* dout, size_t n, c
                      first_large);
             CKL("sieve_kernel");
         }
-        {
+        if (!(exp_skip & 2)) {
             KScope ks(K_DENSE, s);
             int first_large = FIRST_CROSS_PRIME_IDX;
             while (first_large < c->nbp && c->hbp[first_large].x < (uint32_t)g_opt.warp_p) first_large++;
@@ -497,18 +515,18 @@ int device_impl(Ctx* c, const unsigned long long* dN, uint8_t* dout, size_t n, c
             launch_classify(td.n32, td.n64, gcls, s, N, out, len, c, td, vin, vout, seg_stride);
             CKL("classify_kernel");
         }
-        {
+        if (!(exp_skip & 4)) {
             KScope ks(K_SORT, s);
             launch_k(qscatter_kernel, gcls, SORT_THREADS, 0, s, c->plan, c->q, gcls, seg_stride);  // one block per segment
             CKL("qscatter_kernel");
         }
-        {
+        if (!(exp_skip & 4)) {
             KScope ks(K_MR1, s);
             launch_k(mr1_kernel, mr_grid(c->grid_mr1, len), MR1_THREADS, 0, s, c->plan, c->q, N, len,
                      g_opt.kernel_timing, g_opt.sched);
             CKL("mr1_kernel");
         }
-        {
+        if (!(exp_skip & 4)) {
             KScope ks(K_MR2, s);
             rc = launch_mr2(c, s, N, out, len, mr_grid(c->grid_mr2, len));
         }

@@ -947,6 +947,7 @@ struct ClsSmem {
     unsigned int cur;     // entries used in this block's queue segment
     unsigned int h[65];   // bit-length histogram of this block's survivors (for the sort)
     unsigned int fzc[4];  // fused: base-2 tests (32-bit, FP64 class), base-2 passes (32-bit, FP64 class)
+    double p2tab[8];      // {1, a, a^2, a^3} for a = 7, 61 (sprp_small32_f64)
 };
 
 // Append the lanes with pred to list (v, i) of n entries (warp-uniform n).
@@ -992,7 +993,7 @@ __device__ __forceinline__ uint32_t fz_nc(uint32_t z) { return z >> 16; }
 
 // One round of the remaining bases on list b (n < 2^32) or c (FP64 class).
 __device__ __forceinline__ uint32_t fz_phase2(FzWarp& f, uint32_t z, bool cls_c, FzParams fp, uint32_t tlo,
-                                           uint8_t* res, uint8_t* __restrict__ out) {
+                                           uint8_t* res, uint8_t* __restrict__ out, const double* p2tab) {
     const int lane = threadIdx.x & 31;
     unsigned long long n;
     uint32_t idx, k = cls_c ? fz_nc(z) : fz_nb(z);
@@ -1006,6 +1007,8 @@ __device__ __forceinline__ uint32_t fz_phase2(FzWarp& f, uint32_t z, bool cls_c,
                 prime = sprp_multi_f64<1, 1, 2>(n, &a);
             } else if (fp.p2 == 1) {
                 prime = sprp_multi_f64<6, 3, 2>(n, c_bases64);
+            } else if (!__any_sync(__activemask(), n < kSmallBaseMinN)) {
+                prime = sprp_small32_f64<2>(n, p2tab);
             } else {
                 prime = sprp_multi_f64<2, 2, 2>(n, c_bases32_red64);
             }
@@ -1039,11 +1042,11 @@ __device__ __forceinline__ uint32_t fz_base2(FzWarp& f, uint32_t z, unsigned int
 
 // Run every full round the lists hold.
 __device__ __forceinline__ uint32_t fz_drain(FzWarp& f, uint32_t z, unsigned int* fzc, FzParams fp, uint32_t tlo,
-                                             uint8_t* res, uint8_t* __restrict__ out) {
+                                             uint8_t* res, uint8_t* __restrict__ out, const double* p2tab) {
     while (fz_na(z) >= 32u) {
         z = fz_base2(f, z, fzc);
-        while (fz_nb(z) >= 32u) z = fz_phase2(f, z, false, fp, tlo, res, out);
-        while (fz_nc(z) >= 32u) z = fz_phase2(f, z, true, fp, tlo, res, out);
+        while (fz_nb(z) >= 32u) z = fz_phase2(f, z, false, fp, tlo, res, out, p2tab);
+        while (fz_nc(z) >= 32u) z = fz_phase2(f, z, true, fp, tlo, res, out, p2tab);
     }
     return z;
 }
@@ -1051,15 +1054,15 @@ __device__ __forceinline__ uint32_t fz_drain(FzWarp& f, uint32_t z, unsigned int
 // Every round left, partial ones too (once per warp, after its last tile:
 // not inlined, so the tile loop's registers are not shaped by a second copy).
 __device__ __noinline__ void fz_flush(FzWarp& f, uint32_t z, unsigned int* fzc, FzParams fp,
-                                      uint8_t* __restrict__ out) {
+                                      uint8_t* __restrict__ out, const double* p2tab) {
     constexpr uint32_t tlo = 0xFFFFFF00u;  // no tile pending: every result goes to out
     while (fz_na(z)) {
         z = fz_base2(f, z, fzc);
-        while (fz_nb(z) >= 32u) z = fz_phase2(f, z, false, fp, tlo, nullptr, out);
-        while (fz_nc(z) >= 32u) z = fz_phase2(f, z, true, fp, tlo, nullptr, out);
+        while (fz_nb(z) >= 32u) z = fz_phase2(f, z, false, fp, tlo, nullptr, out, p2tab);
+        while (fz_nc(z) >= 32u) z = fz_phase2(f, z, true, fp, tlo, nullptr, out, p2tab);
     }
-    while (fz_nb(z)) z = fz_phase2(f, z, false, fp, tlo, nullptr, out);
-    while (fz_nc(z)) z = fz_phase2(f, z, true, fp, tlo, nullptr, out);
+    while (fz_nb(z)) z = fz_phase2(f, z, false, fp, tlo, nullptr, out, p2tab);
+    while (fz_nc(z)) z = fz_phase2(f, z, true, fp, tlo, nullptr, out, p2tab);
 }
 
 template <int N32, int N64, bool UNI>
@@ -1366,7 +1369,7 @@ __device__ __forceinline__ void classify_tiles(const unsigned long long* __restr
                     uint32_t na = fz_na(z);
                     fz_push(valid, x, idx, fw.av, fw.ai, na, lane);
                     z = (z & ~0xFFu) | na;
-                    if (na >= 32u) z = fz_drain(fw, z, sm.fzc, fz, wbase, ws.res, out);
+                    if (na >= 32u) z = fz_drain(fw, z, sm.fzc, fz, wbase, ws.res, out, sm.p2tab);
                 }
             }
         }
@@ -1384,7 +1387,7 @@ __device__ __forceinline__ void classify_tiles(const unsigned long long* __restr
         }
     }
     // fused lists: the partial rounds left (every tile is stored: results go to out)
-    if (z) fz_flush(fw, z, sm.fzc, fz, out);
+    if (z) fz_flush(fw, z, sm.fzc, fz, out, sm.p2tab);
 }
 
 template <int N32, int N64>
@@ -1411,6 +1414,7 @@ classify_kernel(const unsigned long long* __restrict__ N, uint8_t* __restrict__ 
     for (int b = tid; b < 65; b += CLS_THREADS) sm.h[b] = 0;
     if (tid == 0) sm.cur = 0;
     if (tid < 4) sm.fzc[tid] = 0;
+    small_base_table<2>(sm.p2tab, c_bases32_red64);
     __syncthreads();
     if (span == 0)
         classify_tiles<N32, N64, true>(N, out, len, bitmap, q, td, vec_in, vec_out, seg_stride, segbase, span, wlo32,
@@ -1751,12 +1755,18 @@ mr1_kernel(DevPlan* __restrict__ plan, Queues q, const unsigned long long* __res
 }
 
 // ------------------------------------------------------------- A4: MR phase 2
+constexpr int MR2_DYN_SMEM = 8 * sizeof(double);
 template <int WIN, bool FULL32, int G64, int WIT = 0>
 __global__ void __launch_bounds__(MR_THREADS, G64 == 3 ? 4 : 3)
 mr2_kernel(DevPlan* __restrict__ plan, Queues q, const unsigned long long* __restrict__ N, uint8_t* __restrict__ out,
            uint32_t len, int count_work, int sched) {
     pdl_wait();
     const unsigned int nf = fp_class_count(plan);  // (static shared memory is full: per thread, L1 hits)
+    // {1, a, a^2, a^3} for a = 7, 61 (sprp_small32_f64): dynamic shared memory
+    // (MR2_DYN_SMEM bytes; the static tables fill the 48 KB static limit)
+    extern __shared__ double s_p2tab[];
+    small_base_table<2>(s_p2tab, c_bases32_red64);
+    __syncthreads();
     // window tables of the lockstep bases in shared memory (transposed per thread)
     constexpr bool SM = G64 * (1 << WIN) <= 24;  // <= 48 KB of static shared memory
     __shared__ unsigned long long s_tab[SM ? G64 * (1 << WIN) * MR_THREADS : 1];
@@ -1787,9 +1797,14 @@ mr2_kernel(DevPlan* __restrict__ plan, Queues q, const unsigned long long* __res
                 if (WIT == 2 && !FULL32) {  // one hashed base after base 2
                     const unsigned long long a = hash_base32(n);
                     prime = sprp_multi_f64<1, 1, WIN, SM, MR_THREADS>(n, &a, reinterpret_cast<double*>(st));
-                } else if (CLS32_FP64)  // the 32-bit class on the FP64 pipe (exact below 2^50)
-                    prime = FULL32 ? sprp_multi_f64<6, 3, WIN, SM, MR_THREADS>(n, c_bases64, reinterpret_cast<double*>(st))
-                                   : sprp_multi_f64<2, 2, WIN, SM, MR_THREADS>(n, c_bases32_red64, reinterpret_cast<double*>(st));
+                } else if (CLS32_FP64) {  // the 32-bit class on the FP64 pipe (exact below 2^50)
+                    if (FULL32)
+                        prime = sprp_multi_f64<6, 3, WIN, SM, MR_THREADS>(n, c_bases64, reinterpret_cast<double*>(st));
+                    else if (!__any_sync(__activemask(), n < kSmallBaseMinN))
+                        prime = sprp_small32_f64<2>(n, s_p2tab);
+                    else
+                        prime = sprp_multi_f64<2, 2, WIN, SM, MR_THREADS>(n, c_bases32_red64, reinterpret_cast<double*>(st));
+                }
                 else
                     prime = FULL32 ? sprp_multi32<6>(n, c_bases32_full) : sprp_multi32<2>(n, c_bases32_red);
                 if (prime) out[idx] = 1;
@@ -1844,6 +1859,8 @@ __global__ void __launch_bounds__(256) small_kernel(const unsigned long long* __
     __shared__ unsigned long long s_v[256];
     __shared__ uint32_t s_i[256];
     __shared__ unsigned int s_n[2];  // FP64-pipe classes from the front, 64-bit Montgomery from the back
+    __shared__ double s_p2tab[8];    // {1, a, a^2, a^3} for a = 7, 61 (sprp_small32_f64)
+    small_base_table<2>(s_p2tab, c_bases32_red64);
     if (threadIdx.x < 2) s_n[threadIdx.x] = 0;
     __syncthreads();
     const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
@@ -1878,8 +1895,12 @@ __global__ void __launch_bounds__(256) small_kernel(const unsigned long long* __
         const unsigned long long v = s_v[at];
         bool r;
         if (v < FP_LIMIT) {  // 32-bit and FP64 classes on the FP64 pipe (lazy residues)
-            r = sprp2_f64(v) && (v < (1ull << 32) && !FULL32 ? sprp_multi_f64<2, 2, 2>(v, c_bases32_red64)
-                                                             : sprp_multi_f64<6, 3, 2>(v, c_bases64));
+            r = sprp2_f64(v);
+            if (v < (1ull << 32) && !FULL32) {
+                if (r) r = v >= kSmallBaseMinN ? sprp_small32_f64<2>(v, s_p2tab) : sprp_multi_f64<2, 2, 2>(v, c_bases32_red64);
+            } else if (r) {
+                r = sprp_multi_f64<6, 3, 2>(v, c_bases64);
+            }
         } else {
             r = sprp2_64(v) && sprp_multi64<6, 3, 2>(v, c_bases64);
         }

@@ -123,6 +123,30 @@ __device__ __forceinline__ bool sprp_multi32(uint32_t n, const uint32_t* bases) 
 #define ISP_MR1_UNROLL 2
 #endif
 constexpr int kMr1Unroll = ISP_MR1_UNROLL;  // Montgomery-class base-2 ladders (n >= 2^61); 1 / 2 / 4 measured: C3 phase 1 1.965 / 1.955 / 1.983 ms
+// Base-2 ladder in K-bit windows on lazy Montgomery residues (round 2):
+// 2^d R mod n (< 2n), d odd.  Each window is K - 1 plain squares and one
+// square whose REDC input is shifted left by the window's digit:
+// REDC(x^2 2^dig) = x^2 2^dig R^-1, so the multiplication by 2^dig costs the
+// shift the one-bit ladder already pays.  The REDC bound T = x^2 2^dig <
+// 4 n^2 2^dig <= n R holds for n <= 2^(62 - dig): digits up to 2^K - 1 need
+// n < 2^55 for K = 3 and n < 2^59 for K = 2.  The top window starts from
+// mont(1) (its square is itself).  Per bit: 8 IMAD.WIDE + 2 IMAD as before,
+// the shift and the exponent bookkeeping once per window instead of per bit.
+template <int K>
+__device__ __forceinline__ uint64_t m2_pow_win(uint64_t d, uint64_t n, uint64_t nn, uint64_t one) {
+    const int nb = 64 - __clzll((long long)d);
+    const int nw = (nb + K - 1) / K;
+    uint64_t x = msqr64_shl_lz_ptx(one, n, nn, (uint32_t)(d >> (K * (nw - 1))));
+#pragma unroll 1
+    for (int w = nw - 2; w >= 0; w--) {
+        const uint32_t dig = (uint32_t)(d >> (K * w)) & ((1u << K) - 1u);
+#pragma unroll
+        for (int j = 0; j < K - 1; j++) x = msqr64_lz_ptx(x, n, nn);
+        x = msqr64_shl_lz_ptx(x, n, nn, dig);
+    }
+    return mcanon64(x, n);
+}
+
 // Phase 1 (base 2).  n odd, n >= 3 (used for n >= 2^32).
 __device__ __forceinline__ bool sprp2_64(uint64_t n) {
     const Mont64 M = mont64_setup(n);
@@ -131,7 +155,13 @@ __device__ __forceinline__ bool sprp2_64(uint64_t n) {
     d >>= s;
     const int top = 63 - __clzll((long long)d);
     uint64_t x = mdbl64(M.one, n);  // mont(2): the leading bit of d
-    if (top > 0) {
+    const unsigned int act0 = __activemask();
+    const int bmax = (int)__reduce_max_sync(act0, (unsigned)(64 - __clzll((long long)n)));
+    if (bmax <= 59) {
+        // windowed ladder (warp-uniform width from the warp's largest n)
+        const uint64_t nn = 0ull - M.ninv;
+        x = bmax <= 55 ? m2_pow_win<3>(d, n, nn, M.one) : m2_pow_win<2>(d, n, nn, M.one);
+    } else if (top > 0) {
         // remaining bits of d, most significant first, from the top of dd
         uint64_t dd = d << (64 - top);
         // warp-uniform choice (queues are ordered by bit length, so warps
@@ -445,6 +475,75 @@ __device__ __forceinline__ bool sprp_multi_f64(unsigned long long n, const unsig
     for (int g = 0; g < NB; g += G)
         if (!sprp_lockstep_f64<G, WIN, SM, TS>(M, n, d, s, bases + g, st)) return false;
     return true;
+}
+
+// Remaining bases of the 32-bit class ({7, 61}, reading of Eq 4 by magnitude)
+// in 2-bit windows whose digit multiply folds into the window's last square
+// (round 2): a^dig < 2^18 for a <= 61, dig <= 3, and x a^dig (|x| < n < 2^32)
+// is an exact DMUL below 2^50, so fmul_lazy(a^dig x, x) = x^2 a^dig with the
+// bound of sprp2_f64's windows (e + bitlen(n) <= 18 + 33 <= 51).  Per two
+// exponent bits: two products and one DMUL, instead of two products, a table
+// product and a select chain.  tbl (shared memory): NB rows of {1, a, a^2, a^3}.
+// Needs n > 61 (every base below n); the caller sends smaller n elsewhere.
+constexpr unsigned long long kSmallBaseMinN = 62;
+template <int NB>
+__device__ __forceinline__ bool sprp_small32_f64(unsigned long long n, const double* tbl) {
+    const ModF M = modf_setup(n);
+    uint32_t d = (uint32_t)n - 1u;  // n < 2^32
+    const int s = __ffs(d) - 1;
+    d >>= s;
+    const int nb = 32 - __clz(d);
+    const int nw = (nb + 1) >> 1;
+    const uint32_t top = d >> (2 * (nw - 1));  // 1 .. 3
+    double x[NB];
+#pragma unroll
+    for (int i = 0; i < NB; i++) {
+        x[i] = tbl[4 * i + top];  // a^top < 2^18: one exact reduction below n
+        const double q = fma(x[i], M.ninv, FP_RND) - FP_RND;
+        x[i] = fma(-q, M.n, x[i]);
+    }
+#pragma unroll 1
+    for (int w = nw - 2; w >= 0; w--) {
+        const uint32_t dig = (d >> (2 * w)) & 3u;
+#pragma unroll
+        for (int i = 0; i < NB; i++) {
+            const double c = tbl[4 * i + dig];
+            x[i] = fmul_lazy(x[i], x[i], M);
+            x[i] = fmul_lazy(x[i] * c, x[i], M);
+        }
+    }
+    bool done[NB], pass[NB];
+#pragma unroll
+    for (int i = 0; i < NB; i++) done[i] = pass[i] = f_is_one(x[i], M) || f_is_mone(x[i], M);
+    for (int r = 1; r < s; r++) {
+        bool all = true;
+#pragma unroll
+        for (int i = 0; i < NB; i++) {
+            if (!done[i]) {
+                x[i] = fmul_lazy(x[i], x[i], M);
+                if (f_is_mone(x[i], M)) done[i] = pass[i] = true;
+                else if (f_is_one(x[i], M)) done[i] = true;
+            }
+            all &= done[i];
+        }
+        if (all) break;
+    }
+    bool ok = true;
+#pragma unroll
+    for (int i = 0; i < NB; i++) ok &= pass[i];
+    return ok;
+}
+
+// Fill tbl[4 i + k] = bases[i]^k (k < 4) -- threads 0 .. 4 NB - 1 of a block.
+template <int NB>
+__device__ __forceinline__ void small_base_table(double* tbl, const unsigned long long* bases) {
+    const int t = threadIdx.x;
+    if (t < 4 * NB) {
+        const double a = (double)bases[t >> 2];
+        double v = 1.0;
+        for (int k = 0; k < (t & 3); k++) v *= a;
+        tbl[t] = v;
+    }
 }
 
 // ------------------------------------------------- strong Lucas (BPSW) ----
