@@ -556,6 +556,14 @@ __global__ void __launch_bounds__(PLAN_THREADS) plan_kernel(const unsigned long 
         whi = chi;
     }
     if (lane != 0) return;
+    // the accumulated statistics, read up front: loads issued after the
+    // stores below would each wait out an L2 round trip (plan may alias)
+    unsigned int cnt[4];
+    unsigned long long tot[4];
+#pragma unroll
+    for (int q = 0; q < 4; q++) { cnt[q] = plan->counts[q]; tot[q] = plan->total[q]; }
+    const unsigned int pf0 = plan->pf;
+    const unsigned long long runs0 = plan->sieve_runs, ints0 = plan->sieved_ints, chunks0 = plan->chunks;
     if (whi > wmax) whi = wmax;
     unsigned int need = 0;
     // a sampled arithmetic progression of stride 1 or 2 and at least 2^20
@@ -572,14 +580,14 @@ __global__ void __launch_bounds__(PLAN_THREADS) plan_kernel(const unsigned long 
         whi = (n0 + ds * (len - 1) + 64) & ~63ull;
         if (whi > wmax) whi = wmax;
         plan->valid_lo = plan->valid_hi = 0;  // the global bitmap is not written
-        plan->sieve_runs += 1;
-        plan->sieved_ints += whi - wlo;
+        plan->sieve_runs = runs0 + 1;
+        plan->sieved_ints = ints0 + (whi - wlo);
     } else if (whi > wlo && !(wlo >= vlo && whi <= vhi)) {
         need = 1;
         plan->valid_lo = wlo;
         plan->valid_hi = whi;
-        plan->sieve_runs += 1;
-        plan->sieved_ints += whi - wlo;
+        plan->sieve_runs = runs0 + 1;
+        plan->sieved_ints = ints0 + (whi - wlo);
     } else if (whi > wlo) {
         // inside the held bitmap: classify indexes the bitmap from plan->wlo,
         // so publish the window the bitmap was sieved for, not the sub-range
@@ -589,10 +597,14 @@ __global__ void __launch_bounds__(PLAN_THREADS) plan_kernel(const unsigned long 
     plan->wlo = wlo;
     plan->whi = whi;
     plan->sieve_needed = need;
-    for (int q = 0; q < 4; q++) { plan->total[q] += plan->counts[q]; plan->counts[q] = 0; }
-    plan->total[3] += plan->pf;  // FP64-class base-2 passes count with the 64-bit ones
+#pragma unroll
+    for (int q = 0; q < 4; q++) {
+        // FP64-class base-2 passes count with the 64-bit ones
+        plan->total[q] = tot[q] + cnt[q] + (q == 3 ? pf0 : 0u);
+        plan->counts[q] = 0;
+    }
     plan->pf = 0;
-    plan->chunks += 1;
+    plan->chunks = chunks0 + 1;
 }
 
 // ------------------------------------------------------------- A1: sieve
@@ -880,24 +892,17 @@ __device__ __forceinline__ void dense_body(DevPlan* __restrict__ plan, uint8_t* 
 // Stride 1 and stride 2 are separate kernels (both are launched; the one
 // whose stride the plan did not find exits at once): one kernel with both
 // bodies made ptxas spill and cost C4 4.5 % (tools/ab.sh).
+// One launch for both strides (a chunk that is not a dense range costs one
+// early-exit launch instead of two).
 __global__ void __launch_bounds__(DENSE_THREADS, 1)
 dense_kernel(DevPlan* __restrict__ plan, const unsigned long long* __restrict__ N, uint8_t* __restrict__ out,
              uint32_t len, const uint2* __restrict__ bp, int nbp, const uint8_t* __restrict__ patt, int first_large,
              int vec) {
     pdl_wait();
     extern __shared__ __align__(16) uint8_t dseg[];  // two SEG_ODD buffers
-    if (!plan->dense || plan->dense_d != 1) return;
-    dense_body<1, DENSE_PRODUCERS1>(plan, dseg, N, out, len, bp, nbp, patt, first_large, vec);
-}
-
-__global__ void __launch_bounds__(DENSE_THREADS, 1)
-dense2_kernel(DevPlan* __restrict__ plan, const unsigned long long* __restrict__ N, uint8_t* __restrict__ out,
-              uint32_t len, const uint2* __restrict__ bp, int nbp, const uint8_t* __restrict__ patt, int first_large,
-              int vec) {
-    pdl_wait();
-    extern __shared__ __align__(16) uint8_t dseg[];
-    if (!plan->dense || plan->dense_d != 2) return;
-    dense_body<2, DENSE_PRODUCERS2>(plan, dseg, N, out, len, bp, nbp, patt, first_large, vec);
+    if (!plan->dense) return;
+    if (plan->dense_d == 1) dense_body<1, DENSE_PRODUCERS1>(plan, dseg, N, out, len, bp, nbp, patt, first_large, vec);
+    else dense_body<2, DENSE_PRODUCERS2>(plan, dseg, N, out, len, bp, nbp, patt, first_large, vec);
 }
 
 // ------------------------------------------------------------- A2: classify
@@ -1688,6 +1693,7 @@ __global__ void __launch_bounds__(MR1_THREADS)
 mr1_kernel(DevPlan* __restrict__ plan, Queues q, const unsigned long long* __restrict__ N, uint32_t len,
            int count_work, int sched) {
     pdl_wait();
+    if (plan->counts[0] + plan->counts[1] == 0) return;  // nothing queued (dense window, fused classes)
     __shared__ WarpStage st[3][MR1_THREADS / 32];
     __shared__ unsigned int s_nf;
     if (threadIdx.x == 0) s_nf = fp_class_count(plan);
@@ -1761,6 +1767,7 @@ __global__ void __launch_bounds__(MR_THREADS, G64 == 3 ? 4 : 3)
 mr2_kernel(DevPlan* __restrict__ plan, Queues q, const unsigned long long* __restrict__ N, uint8_t* __restrict__ out,
            uint32_t len, int count_work, int sched) {
     pdl_wait();
+    if (plan->counts[2] + plan->pf + plan->counts[3] == 0) return;  // no base-2 strong probable prime queued
     const unsigned int nf = fp_class_count(plan);  // (static shared memory is full: per thread, L1 hits)
     // {1, a, a^2, a^3} for a = 7, 61 (sprp_small32_f64): dynamic shared memory
     // (MR2_DYN_SMEM bytes; the static tables fill the 48 KB static limit)
