@@ -361,6 +361,30 @@ def roofline(kern_ms, stats, n, steps, peaks, peaks_kind, clocks, cfg=None):
                         f"products x {SLOTS_FP64_PRODUCT:.1f} slots (SASS: profiles/r2/sass_counts.json); "
                         f"survey_model_frac: {SURVEY_IMAD_PER_MULMOD64} slots per 64-bit mulmod",
                 "ms_per_step": round(ms, 4)}
+    fused = stats.get("mulmods_fused", [0, 0])
+    if name == "classify" and sum(fused) > 0:
+        # classify with the fused witness tests (option fuse_bits): the strong
+        # tests of the 32-bit class run on the FP64 pipe inside the streaming
+        # pass, so the multiplier pipe is its roofline; the HBM side is reported
+        # beside it
+        fp = sum(fused) / steps
+        slots = fp * SLOTS_FP64_PRODUCT
+        achieved = slots / (ms * 1e-3) / 1e12
+        mhz = peaks.get("sm_max_mhz", 1965.0)
+        peak = 148 * LANES_PER_CLK_SM * mhz * 1e6 / 1e12
+        hbm = HBM_BYTES_PER_ELEM * n / (ms * 1e-3) / 1e9
+        ncu_sum = None
+        if ncu and ncu.get("fmaheavy_pipe_pct") is not None and ncu.get("fp64_pipe_pct") is not None:
+            ncu_sum = round((ncu["fmaheavy_pipe_pct"] + ncu["fp64_pipe_pct"]) / 100.0, 4)
+        return {"kernel": name, "bound": "alu", "achieved": round(achieved, 4), "peak": round(peak, 3),
+                "unit": "T heavy-pipe lane-slots/s (IMAD.WIDE and DFMA share one multiplier pipe)",
+                "frac": round(achieved / peak, 4), "ncu_fmaheavy_plus_fp64": ncu_sum,
+                "hbm_gbs": round(hbm, 1), "hbm_frac": round(hbm / float(peaks.get("hbm_gbs", 6650.0)), 4),
+                "traffic": traffic, "ncu": ncu,
+                "work": f"per step: {fused[0] / steps:.4g} base-2 + {fused[1] / steps:.4g} remaining-base FP64 "
+                        f"products x {SLOTS_FP64_PRODUCT:.1f} slots in the streaming pass (trial division, "
+                        f"classification and {HBM_BYTES_PER_ELEM} B/element of traffic besides: issue-bound)",
+                "ms_per_step": round(ms, 4)}
     if name == "small":
         return {"kernel": name, "bound": "latency", "achieved": None, "peak": None, "unit": None, "frac": None,
                 "traffic": traffic, "ncu": ncu,

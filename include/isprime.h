@@ -153,6 +153,8 @@ typedef struct {
                                         mr2 32-bit, mr2 64-bit (square-and-multiply count);
                                         the 64-bit entries count the Montgomery class only */
     uint64_t mulmods_fp64[2];        /* same for the FP64 class (odd 2^32 <= n < 2^51): mr1, mr2 */
+    uint64_t mulmods_fused[2];       /* same for the strong tests classify runs itself (option
+                                        "fuse_bits"): base 2, remaining bases (FP64 pipe) */
 } isprime_stats;
 
 /* Synchronises the current device, copies the accumulated statistics. */

@@ -44,12 +44,14 @@ class Stats(ctypes.Structure):
     _fields_ = [(name, ctypes.c_uint64) for name in (
         "window_lo", "window_hi", "sieve_runs", "sieved_integers", "queued32", "queued64",
         "passed32", "passed64", "chunks", "kernel_launches")] + [
-        ("mulmods", ctypes.c_uint64 * 4), ("mulmods_fp64", ctypes.c_uint64 * 2)]
+        ("mulmods", ctypes.c_uint64 * 4), ("mulmods_fp64", ctypes.c_uint64 * 2),
+        ("mulmods_fused", ctypes.c_uint64 * 2)]
 
     def as_dict(self) -> dict:
         d = {name: int(getattr(self, name)) for name, _ in self._fields_ if not name.startswith("mulmods")}
         d["mulmods"] = [int(x) for x in self.mulmods]
         d["mulmods_fp64"] = [int(x) for x in self.mulmods_fp64]
+        d["mulmods_fused"] = [int(x) for x in self.mulmods_fused]
         return d
 
 

@@ -342,6 +342,7 @@ void launch_cls(K k, int g, cudaStream_t s, const unsigned long long* N, uint8_t
     fz.bits = g_opt.fuse_bits;
     fz.p2 = (g_opt.witness == 2 && g_opt.bases32 != 7) ? 2 : g_opt.bases32 == 7 ? 1 : 0;
     fz.wit = g_opt.witness;
+    fz.count_work = g_opt.kernel_timing;
     launch_k(k, g, CLS_THREADS, sizeof(ClsSmem), s, N, out, len, c->plan, c->bitmap, c->q, td, vin, vout, ss, fz);
 }
 
@@ -776,6 +777,8 @@ int isprime_get_stats(isprime_stats* st) {
     for (int k = 0; k < 4; k++) st->mulmods[k] = p.work[k];
     st->mulmods_fp64[0] = p.work_f[0];
     st->mulmods_fp64[1] = p.work_f[1];
+    st->mulmods_fused[0] = p.fzw[0];
+    st->mulmods_fused[1] = p.fzw[1];
     return ISP_OK;
 }
 
@@ -794,6 +797,7 @@ int isprime_reset_stats(void) {
     p.chunks = 0;
     for (int k = 0; k < 4; k++) p.work[k] = 0;
     p.work_f[0] = p.work_f[1] = 0;
+    p.fzw[0] = p.fzw[1] = 0;
     p.valid_lo = p.valid_hi = 0;  // forget the bitmap: the next call sieves again
     CK(cudaMemcpy(c->plan, &p, sizeof(p), cudaMemcpyHostToDevice));
     g_launches = 0;

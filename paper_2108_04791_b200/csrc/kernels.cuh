@@ -110,6 +110,7 @@ struct DevPlan {
     // fused witness tests in classify (option fuse_bits), accumulated: base-2
     // tests (32-bit class, FP64 class), base-2 passes (32-bit class, FP64 class)
     unsigned long long fzt[4];
+    unsigned long long fzw[2];  // fused algorithmic products (work counting): base 2, remaining bases
 };
 
 // Host -> plan kernel parameters (cost model in picoseconds on a full GPU).
@@ -945,6 +946,7 @@ struct FzParams {
     int bits;     // 0: off (everything queued); 32: n < 2^32; 51: n < FP_LIMIT
     int p2;       // remaining bases below 2^32: 0 {7, 61}; 1 the six of Eq 4; 2 one hashed base
     int wit;      // option witness (2: Jaeschke's set below kJaeschkeBound4 in the FP64 class)
+    int count_work;  // accumulate the algorithmic products (plan->fzw), kernel_timing runs only
 };
 struct ClsSmem {
     ClsWarp w[CLS_THREADS / 32];
@@ -953,6 +955,7 @@ struct ClsSmem {
     unsigned int h[65];   // bit-length histogram of this block's survivors (for the sort)
     unsigned int fzc[4];  // fused: base-2 tests (32-bit, FP64 class), base-2 passes (32-bit, FP64 class)
     double p2tab[8];      // {1, a, a^2, a^3} for a = 7, 61 (sprp_small32_f64)
+    unsigned long long fzw[2];  // fused algorithmic products (work counting)
 };
 
 // Append the lanes with pred to list (v, i) of n entries (warp-uniform n).
@@ -998,7 +1001,8 @@ __device__ __forceinline__ uint32_t fz_nc(uint32_t z) { return z >> 16; }
 
 // One round of the remaining bases on list b (n < 2^32) or c (FP64 class).
 __device__ __forceinline__ uint32_t fz_phase2(FzWarp& f, uint32_t z, bool cls_c, FzParams fp, uint32_t tlo,
-                                           uint8_t* res, uint8_t* __restrict__ out, const double* p2tab) {
+                                           uint8_t* res, uint8_t* __restrict__ out, const double* p2tab,
+                                           unsigned long long* fzw) {
     const int lane = threadIdx.x & 31;
     unsigned long long n;
     uint32_t idx, k = cls_c ? fz_nc(z) : fz_nb(z);
@@ -1022,18 +1026,31 @@ __device__ __forceinline__ uint32_t fz_phase2(FzWarp& f, uint32_t z, bool cls_c,
                                                           : sprp_multi_f64<6, 3, 2>(n, c_bases64);
         }
         if (prime) fz_mark(idx, tlo, res, out);
+        if (fp.count_work) {  // square-and-multiply count per base
+            const unsigned long long d = (n - 1) >> (__ffsll((long long)(n - 1)) - 1);
+            const unsigned long long nb = !cls_c ? (fp.p2 == 1 ? 6 : fp.p2 == 2 ? 1 : 2)
+                                                 : ((fp.wit == 2 && n < kJaeschkeBound4) ? 3 : 6);
+            atomicAdd(fzw + 1, nb * (unsigned long long)(63 - __clzll((long long)d) + __popcll(d) - 1));
+        }
     }
     return z;
 }
 
 // One round of base 2 on list a; the passers go to b or c by class.
-__device__ __forceinline__ uint32_t fz_base2(FzWarp& f, uint32_t z, unsigned int* fzc) {
+__device__ __forceinline__ uint32_t fz_base2(FzWarp& f, uint32_t z, unsigned int* fzc, FzParams fp,
+                                            unsigned long long* fzw) {
     const int lane = threadIdx.x & 31;
     unsigned long long n;
     uint32_t idx, na = fz_na(z), nb = fz_nb(z), nc = fz_nc(z);
     const bool act = fz_take(f.av, f.ai, na, lane, n, idx);
     bool pass = false;
-    if (act) pass = sprp2_f64(n);
+    if (act) {
+        pass = sprp2_f64(n);
+        if (fp.count_work) {
+            const unsigned long long d = (n - 1) >> (__ffsll((long long)(n - 1)) - 1);
+            atomicAdd(fzw, (unsigned long long)(63 - __clzll((long long)d)));
+        }
+    }
     const bool small = n < (1ull << 32);
     const uint32_t m32 = __ballot_sync(0xffffffffu, pass && small), mf = __ballot_sync(0xffffffffu, pass && !small);
     fz_push(pass && small, n, idx, f.bv, f.bi, nb, lane);
@@ -1047,11 +1064,12 @@ __device__ __forceinline__ uint32_t fz_base2(FzWarp& f, uint32_t z, unsigned int
 
 // Run every full round the lists hold.
 __device__ __forceinline__ uint32_t fz_drain(FzWarp& f, uint32_t z, unsigned int* fzc, FzParams fp, uint32_t tlo,
-                                             uint8_t* res, uint8_t* __restrict__ out, const double* p2tab) {
+                                             uint8_t* res, uint8_t* __restrict__ out, const double* p2tab,
+                                             unsigned long long* fzw) {
     while (fz_na(z) >= 32u) {
-        z = fz_base2(f, z, fzc);
-        while (fz_nb(z) >= 32u) z = fz_phase2(f, z, false, fp, tlo, res, out, p2tab);
-        while (fz_nc(z) >= 32u) z = fz_phase2(f, z, true, fp, tlo, res, out, p2tab);
+        z = fz_base2(f, z, fzc, fp, fzw);
+        while (fz_nb(z) >= 32u) z = fz_phase2(f, z, false, fp, tlo, res, out, p2tab, fzw);
+        while (fz_nc(z) >= 32u) z = fz_phase2(f, z, true, fp, tlo, res, out, p2tab, fzw);
     }
     return z;
 }
@@ -1059,15 +1077,15 @@ __device__ __forceinline__ uint32_t fz_drain(FzWarp& f, uint32_t z, unsigned int
 // Every round left, partial ones too (once per warp, after its last tile:
 // not inlined, so the tile loop's registers are not shaped by a second copy).
 __device__ __noinline__ void fz_flush(FzWarp& f, uint32_t z, unsigned int* fzc, FzParams fp,
-                                      uint8_t* __restrict__ out, const double* p2tab) {
+                                      uint8_t* __restrict__ out, const double* p2tab, unsigned long long* fzw) {
     constexpr uint32_t tlo = 0xFFFFFF00u;  // no tile pending: every result goes to out
     while (fz_na(z)) {
-        z = fz_base2(f, z, fzc);
-        while (fz_nb(z) >= 32u) z = fz_phase2(f, z, false, fp, tlo, nullptr, out, p2tab);
-        while (fz_nc(z) >= 32u) z = fz_phase2(f, z, true, fp, tlo, nullptr, out, p2tab);
+        z = fz_base2(f, z, fzc, fp, fzw);
+        while (fz_nb(z) >= 32u) z = fz_phase2(f, z, false, fp, tlo, nullptr, out, p2tab, fzw);
+        while (fz_nc(z) >= 32u) z = fz_phase2(f, z, true, fp, tlo, nullptr, out, p2tab, fzw);
     }
-    while (fz_nb(z)) z = fz_phase2(f, z, false, fp, tlo, nullptr, out, p2tab);
-    while (fz_nc(z)) z = fz_phase2(f, z, true, fp, tlo, nullptr, out, p2tab);
+    while (fz_nb(z)) z = fz_phase2(f, z, false, fp, tlo, nullptr, out, p2tab, fzw);
+    while (fz_nc(z)) z = fz_phase2(f, z, true, fp, tlo, nullptr, out, p2tab, fzw);
 }
 
 template <int N32, int N64, bool UNI>
@@ -1374,7 +1392,7 @@ __device__ __forceinline__ void classify_tiles(const unsigned long long* __restr
                     uint32_t na = fz_na(z);
                     fz_push(valid, x, idx, fw.av, fw.ai, na, lane);
                     z = (z & ~0xFFu) | na;
-                    if (na >= 32u) z = fz_drain(fw, z, sm.fzc, fz, wbase, ws.res, out, sm.p2tab);
+                    if (na >= 32u) z = fz_drain(fw, z, sm.fzc, fz, wbase, ws.res, out, sm.p2tab, sm.fzw);
                 }
             }
         }
@@ -1392,7 +1410,7 @@ __device__ __forceinline__ void classify_tiles(const unsigned long long* __restr
         }
     }
     // fused lists: the partial rounds left (every tile is stored: results go to out)
-    if (z) fz_flush(fw, z, sm.fzc, fz, out, sm.p2tab);
+    if (z) fz_flush(fw, z, sm.fzc, fz, out, sm.p2tab, sm.fzw);
 }
 
 template <int N32, int N64>
@@ -1419,6 +1437,7 @@ classify_kernel(const unsigned long long* __restrict__ N, uint8_t* __restrict__ 
     for (int b = tid; b < 65; b += CLS_THREADS) sm.h[b] = 0;
     if (tid == 0) sm.cur = 0;
     if (tid < 4) sm.fzc[tid] = 0;
+    if (tid < 2) sm.fzw[tid] = 0;
     small_base_table<2>(sm.p2tab, c_bases32_red64);
     __syncthreads();
     if (span == 0)
@@ -1434,6 +1453,7 @@ classify_kernel(const unsigned long long* __restrict__ N, uint8_t* __restrict__ 
         if (sm.h[b]) atomicAdd(&plan->bins[b], sm.h[b]);
     }
     if (tid < 4 && sm.fzc[tid]) atomicAdd(&plan->fzt[tid], (unsigned long long)sm.fzc[tid]);
+    if (tid < 2 && sm.fzw[tid]) atomicAdd(&plan->fzw[tid], sm.fzw[tid]);
     if (tid == 0) {
         unsigned int c32 = 0;
         for (int b = 0; b <= 32; b++) c32 += sm.h[b];
