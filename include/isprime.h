@@ -134,6 +134,9 @@ void isprime_shutdown(void);
  *                    64-bit classes.  Never changes a bit of out
  * "kernel_timing"    1: bracket every launch with CUDA events on its stream and
  *                    accumulate per-kernel device time (isprime_get_kernel_times)
+ * "count_work"       1: the witness tests count their algorithmic modular
+ *                    multiplications (isprime_stats.mulmods*); separate
+ *                    instantiations, so timings are taken with it off
  * Returns ISP_OK or ISP_EINVAL. */
 #define ISP_MAX_TD 128
 int isprime_set_option(const char* key, long long value);
@@ -149,7 +152,7 @@ typedef struct {
     uint64_t chunks;                 /* device chunks processed */
     uint64_t kernel_launches;        /* kernels launched by the library (host count) */
     uint64_t mulmods[4];             /* algorithmic modular multiplications counted while
-                                        "kernel_timing" is 1: mr1 32-bit, mr1 64-bit,
+                                        "count_work" is 1: mr1 32-bit, mr1 64-bit,
                                         mr2 32-bit, mr2 64-bit (square-and-multiply count);
                                         the 64-bit entries count the Montgomery class only */
     uint64_t mulmods_fp64[2];        /* same for the FP64 class (odd 2^32 <= n < 2^51): mr1, mr2 */

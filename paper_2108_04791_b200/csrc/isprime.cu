@@ -37,6 +37,7 @@ struct Options {
     long long mr_fixed_ns = 24486;        // witness kernels' latency floor
     unsigned long long sieve_max = 1ull << 32;
     int kernel_timing = 0;
+    int count_work = 0;      // witness tests count their algorithmic products (isprime_stats.mulmods*)
     int sieve_cache = 0;
     int pdl = 1;             // programmatic dependent launch of the pipeline kernels
     int mr2_group = 3;       // 64-bit phase-2 bases run G at a time in lockstep (3 or 6)
@@ -342,7 +343,6 @@ void launch_cls(K k, int g, cudaStream_t s, const unsigned long long* N, uint8_t
     fz.bits = g_opt.fuse_bits;
     fz.p2 = (g_opt.witness == 2 && g_opt.bases32 != 7) ? 2 : g_opt.bases32 == 7 ? 1 : 0;
     fz.wit = g_opt.witness;
-    fz.count_work = g_opt.kernel_timing;
     launch_k(k, g, CLS_THREADS, sizeof(ClsSmem), s, N, out, len, c->plan, c->bitmap, c->q, td, vin, vout, ss, fz);
 }
 
@@ -360,6 +360,10 @@ void launch_classify_b(int n64, int g, cudaStream_t s, const unsigned long long*
 
 void launch_classify(int n32, int n64, int g, cudaStream_t s, const unsigned long long* N, uint8_t* out,
                      uint32_t len, Ctx* c, const TDParams& td, int vin, int vout, uint32_t ss) {
+    if (g_opt.count_work && n32 == 16 && n64 == 32) {  // the work-counting instantiation (default TD only)
+        launch_cls(classify_kernel<16, 32, true>, g, s, N, out, len, c, td, vin, vout, ss);
+        return;
+    }
     switch (n32) {
         case 32: launch_classify_b<32>(n64, g, s, N, out, len, c, td, vin, vout, ss); break;
         case 24: launch_classify_b<24>(n64, g, s, N, out, len, c, td, vin, vout, ss); break;
@@ -383,7 +387,7 @@ void launch_mr2_w(Ctx* c, cudaStream_t s, const unsigned long long* N, uint8_t* 
 
 int launch_mr2(Ctx* c, cudaStream_t s, const unsigned long long* N, uint8_t* out, uint32_t len, int grid) {
     const bool full = g_opt.bases32 == 7;
-    const int cw = g_opt.kernel_timing;
+    const int cw = g_opt.count_work;
     const int g = g_opt.mr2_group == 6 ? 6 : 3;
     if (g_opt.witness == 1) {  // Baillie-PSW for the 64-bit Montgomery class
         mr2_attr(mr2_kernel<3, true, 3, 1>);
@@ -520,7 +524,7 @@ int device_impl(Ctx* c, const unsigned long long* dN, uint8_t* dout, size_t n, c
         if (!(exp_skip & 4)) {
             KScope ks(K_MR1, s);
             launch_k(mr1_kernel, mr_grid(c->grid_mr1, len), MR1_THREADS, 0, s, c->plan, c->q, N, len,
-                     g_opt.kernel_timing, g_opt.sched);
+                     g_opt.count_work, g_opt.sched);
             CKL("mr1_kernel");
         }
         if (!(exp_skip & 4)) {
@@ -716,6 +720,7 @@ int isprime_set_option(const char* key, long long v) {
     else if (!strcmp(key, "mr32_fs_per_bit")) { if (v < 0) return ISP_EINVAL; g_opt.mr32_fs_per_bit = v; }
     else if (!strcmp(key, "mr_fixed_ns")) { if (v < 0) return ISP_EINVAL; g_opt.mr_fixed_ns = v; }
     else if (!strcmp(key, "kernel_timing")) { if (v < 0 || v > 1) return ISP_EINVAL; g_opt.kernel_timing = (int)v; }
+    else if (!strcmp(key, "count_work")) { if (v < 0 || v > 1) return ISP_EINVAL; g_opt.count_work = (int)v; }
     else if (!strcmp(key, "mr2_group")) { if (v != 3 && v != 6) return ISP_EINVAL; g_opt.mr2_group = (int)v; }
     else if (!strcmp(key, "pdl")) { if (v < 0 || v > 1) return ISP_EINVAL; g_opt.pdl = (int)v; }
     else if (!strcmp(key, "sieve_cache")) { if (v < 0 || v > 1) return ISP_EINVAL; g_opt.sieve_cache = (int)v; }
@@ -744,6 +749,7 @@ long long isprime_get_option(const char* key) {
     if (!strcmp(key, "mr32_fs_per_bit")) return g_opt.mr32_fs_per_bit;
     if (!strcmp(key, "mr_fixed_ns")) return g_opt.mr_fixed_ns;
     if (!strcmp(key, "kernel_timing")) return g_opt.kernel_timing;
+    if (!strcmp(key, "count_work")) return g_opt.count_work;
     if (!strcmp(key, "sieve_cache")) return g_opt.sieve_cache;
     if (!strcmp(key, "mr2_group")) return g_opt.mr2_group;
     if (!strcmp(key, "pdl")) return g_opt.pdl;

@@ -946,7 +946,6 @@ struct FzParams {
     int bits;     // 0: off (everything queued); 32: n < 2^32; 51: n < FP_LIMIT
     int p2;       // remaining bases below 2^32: 0 {7, 61}; 1 the six of Eq 4; 2 one hashed base
     int wit;      // option witness (2: Jaeschke's set below kJaeschkeBound4 in the FP64 class)
-    int count_work;  // accumulate the algorithmic products (plan->fzw), kernel_timing runs only
 };
 struct ClsSmem {
     ClsWarp w[CLS_THREADS / 32];
@@ -1000,6 +999,9 @@ __device__ __forceinline__ uint32_t fz_nb(uint32_t z) { return (z >> 8) & 0xFFu;
 __device__ __forceinline__ uint32_t fz_nc(uint32_t z) { return z >> 16; }
 
 // One round of the remaining bases on list b (n < 2^32) or c (FP64 class).
+// CW: count the algorithmic products (kernel_timing runs; a separate
+// instantiation, so the counting costs the timed kernel no registers).
+template <bool CW>
 __device__ __forceinline__ uint32_t fz_phase2(FzWarp& f, uint32_t z, bool cls_c, FzParams fp, uint32_t tlo,
                                            uint8_t* res, uint8_t* __restrict__ out, const double* p2tab,
                                            unsigned long long* fzw) {
@@ -1026,17 +1028,23 @@ __device__ __forceinline__ uint32_t fz_phase2(FzWarp& f, uint32_t z, bool cls_c,
                                                           : sprp_multi_f64<6, 3, 2>(n, c_bases64);
         }
         if (prime) fz_mark(idx, tlo, res, out);
-        if (fp.count_work) {  // square-and-multiply count per base
+    }
+    if (CW) {  // square-and-multiply count per base, one atomic per warp
+        uint32_t w = 0;
+        if (act) {
             const unsigned long long d = (n - 1) >> (__ffsll((long long)(n - 1)) - 1);
-            const unsigned long long nb = !cls_c ? (fp.p2 == 1 ? 6 : fp.p2 == 2 ? 1 : 2)
-                                                 : ((fp.wit == 2 && n < kJaeschkeBound4) ? 3 : 6);
-            atomicAdd(fzw + 1, nb * (unsigned long long)(63 - __clzll((long long)d) + __popcll(d) - 1));
+            const uint32_t nb = !cls_c ? (fp.p2 == 1 ? 6u : fp.p2 == 2 ? 1u : 2u)
+                                       : ((fp.wit == 2 && n < kJaeschkeBound4) ? 3u : 6u);
+            w = nb * (uint32_t)(63 - __clzll((long long)d) + __popcll(d) - 1);
         }
+        w = __reduce_add_sync(0xffffffffu, w);
+        if (lane == 0 && w) atomicAdd(fzw + 1, (unsigned long long)w);
     }
     return z;
 }
 
 // One round of base 2 on list a; the passers go to b or c by class.
+template <bool CW>
 __device__ __forceinline__ uint32_t fz_base2(FzWarp& f, uint32_t z, unsigned int* fzc, FzParams fp,
                                             unsigned long long* fzw) {
     const int lane = threadIdx.x & 31;
@@ -1044,12 +1052,12 @@ __device__ __forceinline__ uint32_t fz_base2(FzWarp& f, uint32_t z, unsigned int
     uint32_t idx, na = fz_na(z), nb = fz_nb(z), nc = fz_nc(z);
     const bool act = fz_take(f.av, f.ai, na, lane, n, idx);
     bool pass = false;
-    if (act) {
-        pass = sprp2_f64(n);
-        if (fp.count_work) {
-            const unsigned long long d = (n - 1) >> (__ffsll((long long)(n - 1)) - 1);
-            atomicAdd(fzw, (unsigned long long)(63 - __clzll((long long)d)));
-        }
+    if (act) pass = sprp2_f64(n);
+    if (CW) {  // ladder squarings, one atomic per warp
+        uint32_t w = 0;
+        if (act) w = (uint32_t)(63 - __clzll((long long)((n - 1) >> (__ffsll((long long)(n - 1)) - 1))));
+        w = __reduce_add_sync(0xffffffffu, w);
+        if (lane == 0 && w) atomicAdd(fzw, (unsigned long long)w);
     }
     const bool small = n < (1ull << 32);
     const uint32_t m32 = __ballot_sync(0xffffffffu, pass && small), mf = __ballot_sync(0xffffffffu, pass && !small);
@@ -1063,32 +1071,34 @@ __device__ __forceinline__ uint32_t fz_base2(FzWarp& f, uint32_t z, unsigned int
 }
 
 // Run every full round the lists hold.
+template <bool CW>
 __device__ __forceinline__ uint32_t fz_drain(FzWarp& f, uint32_t z, unsigned int* fzc, FzParams fp, uint32_t tlo,
                                              uint8_t* res, uint8_t* __restrict__ out, const double* p2tab,
                                              unsigned long long* fzw) {
     while (fz_na(z) >= 32u) {
-        z = fz_base2(f, z, fzc, fp, fzw);
-        while (fz_nb(z) >= 32u) z = fz_phase2(f, z, false, fp, tlo, res, out, p2tab, fzw);
-        while (fz_nc(z) >= 32u) z = fz_phase2(f, z, true, fp, tlo, res, out, p2tab, fzw);
+        z = fz_base2<CW>(f, z, fzc, fp, fzw);
+        while (fz_nb(z) >= 32u) z = fz_phase2<CW>(f, z, false, fp, tlo, res, out, p2tab, fzw);
+        while (fz_nc(z) >= 32u) z = fz_phase2<CW>(f, z, true, fp, tlo, res, out, p2tab, fzw);
     }
     return z;
 }
 
 // Every round left, partial ones too (once per warp, after its last tile:
 // not inlined, so the tile loop's registers are not shaped by a second copy).
+template <bool CW>
 __device__ __noinline__ void fz_flush(FzWarp& f, uint32_t z, unsigned int* fzc, FzParams fp,
                                       uint8_t* __restrict__ out, const double* p2tab, unsigned long long* fzw) {
     constexpr uint32_t tlo = 0xFFFFFF00u;  // no tile pending: every result goes to out
     while (fz_na(z)) {
-        z = fz_base2(f, z, fzc, fp, fzw);
-        while (fz_nb(z) >= 32u) z = fz_phase2(f, z, false, fp, tlo, nullptr, out, p2tab, fzw);
-        while (fz_nc(z) >= 32u) z = fz_phase2(f, z, true, fp, tlo, nullptr, out, p2tab, fzw);
+        z = fz_base2<CW>(f, z, fzc, fp, fzw);
+        while (fz_nb(z) >= 32u) z = fz_phase2<CW>(f, z, false, fp, tlo, nullptr, out, p2tab, fzw);
+        while (fz_nc(z) >= 32u) z = fz_phase2<CW>(f, z, true, fp, tlo, nullptr, out, p2tab, fzw);
     }
-    while (fz_nb(z)) z = fz_phase2(f, z, false, fp, tlo, nullptr, out, p2tab, fzw);
-    while (fz_nc(z)) z = fz_phase2(f, z, true, fp, tlo, nullptr, out, p2tab, fzw);
+    while (fz_nb(z)) z = fz_phase2<CW>(f, z, false, fp, tlo, nullptr, out, p2tab, fzw);
+    while (fz_nc(z)) z = fz_phase2<CW>(f, z, true, fp, tlo, nullptr, out, p2tab, fzw);
 }
 
-template <int N32, int N64, bool UNI>
+template <int N32, int N64, bool UNI, bool CW>
 __device__ __forceinline__ void classify_tiles(const unsigned long long* __restrict__ N, uint8_t* __restrict__ out,
                                                uint32_t len, const uint32_t* __restrict__ bitmap, const Queues& q,
                                                const TDParams& td, int vec_in, int vec_out, uint32_t seg_stride,
@@ -1392,7 +1402,7 @@ __device__ __forceinline__ void classify_tiles(const unsigned long long* __restr
                     uint32_t na = fz_na(z);
                     fz_push(valid, x, idx, fw.av, fw.ai, na, lane);
                     z = (z & ~0xFFu) | na;
-                    if (na >= 32u) z = fz_drain(fw, z, sm.fzc, fz, wbase, ws.res, out, sm.p2tab, sm.fzw);
+                    if (na >= 32u) z = fz_drain<CW>(fw, z, sm.fzc, fz, wbase, ws.res, out, sm.p2tab, sm.fzw);
                 }
             }
         }
@@ -1410,10 +1420,10 @@ __device__ __forceinline__ void classify_tiles(const unsigned long long* __restr
         }
     }
     // fused lists: the partial rounds left (every tile is stored: results go to out)
-    if (z) fz_flush(fw, z, sm.fzc, fz, out, sm.p2tab, sm.fzw);
+    if (z) fz_flush<CW>(fw, z, sm.fzc, fz, out, sm.p2tab, sm.fzw);
 }
 
-template <int N32, int N64>
+template <int N32, int N64, bool CW = false>
 __global__ void __launch_bounds__(CLS_THREADS)
 classify_kernel(const unsigned long long* __restrict__ N, uint8_t* __restrict__ out, uint32_t len,
                 DevPlan* __restrict__ plan, const uint32_t* __restrict__ bitmap, Queues q, TDParams td,
@@ -1441,10 +1451,10 @@ classify_kernel(const unsigned long long* __restrict__ N, uint8_t* __restrict__ 
     small_base_table<2>(sm.p2tab, c_bases32_red64);
     __syncthreads();
     if (span == 0)
-        classify_tiles<N32, N64, true>(N, out, len, bitmap, q, td, vec_in, vec_out, seg_stride, segbase, span, wlo32,
+        classify_tiles<N32, N64, true, CW>(N, out, len, bitmap, q, td, vec_in, vec_out, seg_stride, segbase, span, wlo32,
                                        spanm1, spanm1w, ntiles, sm, ws, lane, wid, fz);
     else
-        classify_tiles<N32, N64, false>(N, out, len, bitmap, q, td, vec_in, vec_out, seg_stride, segbase, span, wlo32,
+        classify_tiles<N32, N64, false, CW>(N, out, len, bitmap, q, td, vec_in, vec_out, seg_stride, segbase, span, wlo32,
                                         spanm1, spanm1w, ntiles, sm, ws, lane, wid, fz);
     __syncthreads();
     for (int b = tid; b < 65; b += CLS_THREADS)

@@ -52,7 +52,7 @@ def assert_same(got, exp, N=None):
 def _default_options():
     saved = {k: isp.get_option(k) for k in ("force_path", "bases32", "td_primes32", "td_primes64",
                                              "chunk_log2", "win64", "warp_p", "small_max", "warp_max",
-                                             "witness", "sieve_cache", "sched", "fuse_bits")}
+                                             "witness", "sieve_cache", "sched", "fuse_bits", "count_work")}
     yield
     for k, v in saved.items():
         isp.set_option(k, v)
@@ -644,6 +644,26 @@ def test_fused_stats_count_like_the_queues():
         st = isp.get_stats()
         res[fb] = tuple(st[k] for k in ("queued32", "queued64", "passed32", "passed64"))
     assert res[0] == res[32] == res[51], res
+
+
+def test_count_work_instantiations_change_nothing():
+    """Option count_work runs separate kernel instantiations that count the
+    algorithmic products; the result stays bit-exact and every class reports
+    work (fused 32-bit tests in classify, FP64 and Montgomery classes in the
+    witness kernels)."""
+    isp.set_option("small_max", 0)
+    N = np.concatenate([workloads.generate("C5", count=1 << 19), workloads.generate("C2", count=1 << 18)])
+    exp = oracle.isprime(N)
+    isp.set_option("count_work", 1)
+    isp.reset_stats()
+    assert_same(gpu(N), exp, N)
+    st = isp.get_stats()
+    isp.set_option("count_work", 0)
+    assert st["mulmods_fused"][0] > 0 and st["mulmods_fused"][1] > 0
+    assert st["mulmods"][1] > 0 and st["mulmods"][3] > 0 and st["mulmods_fp64"][0] > 0
+    isp.reset_stats()
+    assert_same(gpu(N), exp, N)
+    assert sum(isp.get_stats()["mulmods_fused"]) == 0  # counting off: nothing counted
 
 
 # ------------------------------------------------------------------ boundary edge cases
