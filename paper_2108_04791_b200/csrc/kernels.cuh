@@ -392,7 +392,10 @@ __global__ void init_presieve_kernel(uint8_t* patt) {
 // MATLAB fits.  The plan changes only the time, never the result: any element
 // outside the window takes the trial-division / Miller-Rabin route.
 constexpr int PLAN_THREADS = 1024;
-constexpr int PLAN_SAMPLES = 4096;
+#ifndef PLAN_SAMPLES_DEF
+#define PLAN_SAMPLES_DEF 4096
+#endif
+constexpr int PLAN_SAMPLES = PLAN_SAMPLES_DEF;
 #ifndef PLAN_RUN
 #define PLAN_RUN 4                                    // consecutive elements per sampled stratum
 #endif
