@@ -484,8 +484,7 @@ int device_impl(Ctx* c, const unsigned long long* dN, uint8_t* dout, size_t n, c
             launch_k(plan_kernel, 1, PLAN_THREADS, 0, s, N, (unsigned long long)len, c->plan, P);
             CKL("plan_kernel");
         }
-        static const int exp_skip = getenv("ISPRIME_EXP_SKIP") ? atoi(getenv("ISPRIME_EXP_SKIP")) : 0;  // TEMP experiment
-        if (!(exp_skip & 1)) {
+        {
             KScope ks(K_SIEVE, s);
             // first base prime >= warp_p (the warp-cooperative / per-thread split)
             int first_large = FIRST_CROSS_PRIME_IDX;
@@ -494,7 +493,7 @@ int device_impl(Ctx* c, const unsigned long long* dN, uint8_t* dout, size_t n, c
                      first_large);
             CKL("sieve_kernel");
         }
-        if (!(exp_skip & 2)) {
+        {
             KScope ks(K_DENSE, s);
             int first_large = FIRST_CROSS_PRIME_IDX;
             while (first_large < c->nbp && c->hbp[first_large].x < (uint32_t)g_opt.warp_p) first_large++;
@@ -516,18 +515,18 @@ int device_impl(Ctx* c, const unsigned long long* dN, uint8_t* dout, size_t n, c
             launch_classify(td.n32, td.n64, gcls, s, N, out, len, c, td, vin, vout, seg_stride);
             CKL("classify_kernel");
         }
-        if (!(exp_skip & 4)) {
+        {
             KScope ks(K_SORT, s);
             launch_k(qscatter_kernel, gcls, SORT_THREADS, 0, s, c->plan, c->q, gcls, seg_stride);  // one block per segment
             CKL("qscatter_kernel");
         }
-        if (!(exp_skip & 4)) {
+        {
             KScope ks(K_MR1, s);
             launch_k(mr1_kernel, mr_grid(c->grid_mr1, len), MR1_THREADS, 0, s, c->plan, c->q, N, len,
                      g_opt.count_work, g_opt.sched);
             CKL("mr1_kernel");
         }
-        if (!(exp_skip & 4)) {
+        {
             KScope ks(K_MR2, s);
             rc = launch_mr2(c, s, N, out, len, mr_grid(c->grid_mr2, len));
         }

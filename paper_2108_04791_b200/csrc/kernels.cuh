@@ -23,6 +23,7 @@
 // (choosing the array path from the element count and the maximum).
 #pragma once
 #include <stdint.h>
+#include <cooperative_groups.h>
 #include "witness.cuh"
 #include "witness32_table.h"
 
@@ -1890,6 +1891,33 @@ mr2_kernel(DevPlan* __restrict__ plan, Queues q, const unsigned long long* __res
 // magnitude class's arithmetic -- so the result is the same bit for bit; lanes
 // diverge, which only matters when n is large (the host sends those down the
 // pipeline).
+// The strong tests of a block's compacted list (short-array kernels): slots
+// [0, nf) hold FP64-pipe entries, the last nm slots (from the back of a CAP-slot
+// list) Montgomery entries, taken from the next warp boundary on so warps are
+// uniform in arithmetic.  Caller: a block barrier after filling the list.
+template <bool FULL32, int CAP>
+__device__ __forceinline__ void small_witness_tail(const unsigned long long* s_v, const uint32_t* s_i, unsigned int nf,
+                                                   unsigned int nm, const double* p2tab, uint8_t* __restrict__ out) {
+    const unsigned int m0 = (nf + 31u) & ~31u;
+    for (unsigned int t = threadIdx.x; t < m0 + nm; t += blockDim.x) {
+        if (t >= nf && t < m0) continue;
+        const unsigned int at = t < nf ? t : (unsigned int)(CAP - 1) - (t - m0);
+        const unsigned long long v = s_v[at];
+        bool r;
+        if (v < FP_LIMIT) {  // 32-bit and FP64 classes on the FP64 pipe (lazy residues)
+            r = sprp2_f64(v);
+            if (v < (1ull << 32) && !FULL32) {
+                if (r) r = v >= kSmallBaseMinN ? sprp_small32_f64<2>(v, p2tab) : sprp_multi_f64<2, 2, 2>(v, c_bases32_red64);
+            } else if (r) {
+                r = sprp_multi_f64<6, 3, 2>(v, c_bases64);
+            }
+        } else {
+            r = sprp2_64(v) && sprp_multi64<6, 3, 2>(v, c_bases64);
+        }
+        out[s_i[at]] = (uint8_t)r;
+    }
+}
+
 template <bool FULL32>
 __global__ void __launch_bounds__(256) small_kernel(const unsigned long long* __restrict__ N, uint8_t* __restrict__ out,
                                                     uint32_t len, TDParams td) {
@@ -1926,26 +1954,7 @@ __global__ void __launch_bounds__(256) small_kernel(const unsigned long long* __
         }
     }
     __syncthreads();
-    // slots: [0, nf) FP64-pipe entries, then from the next warp boundary the
-    // Montgomery entries, so warps are uniform in arithmetic
-    const unsigned int nf = s_n[0], nm = s_n[1], m0 = (nf + 31u) & ~31u;
-    for (unsigned int t = threadIdx.x; t < m0 + nm; t += blockDim.x) {
-        if (t >= nf && t < m0) continue;
-        const unsigned int at = t < nf ? t : 255u - (t - m0);
-        const unsigned long long v = s_v[at];
-        bool r;
-        if (v < FP_LIMIT) {  // 32-bit and FP64 classes on the FP64 pipe (lazy residues)
-            r = sprp2_f64(v);
-            if (v < (1ull << 32) && !FULL32) {
-                if (r) r = v >= kSmallBaseMinN ? sprp_small32_f64<2>(v, s_p2tab) : sprp_multi_f64<2, 2, 2>(v, c_bases32_red64);
-            } else if (r) {
-                r = sprp_multi_f64<6, 3, 2>(v, c_bases64);
-            }
-        } else {
-            r = sprp2_64(v) && sprp_multi64<6, 3, 2>(v, c_bases64);
-        }
-        out[s_i[at]] = (uint8_t)r;
-    }
+    small_witness_tail<FULL32, 256>(s_v, s_i, s_n[0], s_n[1], s_p2tab, out);
 }
 
 // Scalars and very short arrays: one warp per element, one Eq 4 base per lane
@@ -1955,6 +1964,92 @@ __global__ void __launch_bounds__(256) small_kernel(const unsigned long long* __
 // never splits.  Same trivial cases and trial division as small_kernel.
 __constant__ unsigned long long c_bases7[7] = {2ull, 325ull, 9375ull, 28178ull, 450775ull, 9780504ull, 1795265022ull};
 __constant__ uint32_t c_bases32_3[3] = {2u, 7u, 61u};
+
+// Short arrays with small values (round 2; north_star (c), PAPER.md:22 / 279:
+// "sieve to M, then membership"): one launch of 8-block thread-block clusters.
+// The 8 blocks of a cluster sieve [0, 2^20) together -- block r the odd values
+// of [r 2^17, (r + 1) 2^17), one byte each, in its own shared memory
+// (sieve_segment) -- and every element below 2^20 reads its byte from the
+// owning block through distributed shared memory (ld.shared::cluster).
+// Elements at or above 2^20 take small_kernel's trial division + strong tests.
+// A cluster whose elements hold no odd value in [3, 2^20) skips the sieve (a
+// cluster-wide vote), so 64-bit inputs pay one cluster barrier for it.
+constexpr int SSV_THREADS = 512;
+constexpr int SSV_PER = 4;                                    // elements per thread
+constexpr int SSV_ELEMS = SSV_THREADS * SSV_PER;              // per block
+constexpr int SSV_CLUSTER = 8;
+constexpr uint32_t SSV_SEG = 65536;                           // odd values per block
+constexpr unsigned long long SSV_LIMIT = 2ull * SSV_SEG * SSV_CLUSTER;  // 2^20
+static_assert(SSV_SEG <= SEG_ODD, "sieve_segment initialises SEG_ODD bytes");
+struct SsvSmem {
+    uint8_t seg[SEG_ODD];                 // this block's sieve segment (sieve_segment writes SEG_ODD bytes)
+    unsigned long long v[SSV_ELEMS];      // elements for the strong tests
+    uint32_t i[SSV_ELEMS];
+    double p2tab[8];
+    unsigned int n[2];
+    int any;
+};
+
+template <bool FULL32>
+__global__ void __launch_bounds__(SSV_THREADS) small_sieve_kernel(const unsigned long long* __restrict__ N,
+                                                                  uint8_t* __restrict__ out, uint32_t len,
+                                                                  TDParams td, const uint2* __restrict__ bp, int nbp,
+                                                                  const uint8_t* __restrict__ patt, int first_large) {
+    extern __shared__ __align__(16) unsigned char ssv_raw[];
+    SsvSmem& sm = *reinterpret_cast<SsvSmem*>(ssv_raw);
+    namespace cg = cooperative_groups;
+    cg::cluster_group cl = cg::this_cluster();
+    const int tid = threadIdx.x;
+    if (tid < 2) sm.n[tid] = 0;
+    small_base_table<2>(sm.p2tab, c_bases32_red64);
+    const uint32_t base = blockIdx.x * (uint32_t)SSV_ELEMS;
+    unsigned long long v[SSV_PER];
+    bool want = false;
+#pragma unroll
+    for (int k = 0; k < SSV_PER; k++) {
+        const uint32_t i = base + k * SSV_THREADS + tid;
+        v[k] = i < len ? N[i] : 0ull;
+        want |= (v[k] & 1ull) && v[k] >= 3ull && v[k] < SSV_LIMIT;
+    }
+    const int blk_want = __syncthreads_or(want);
+    if (tid == 0) sm.any = blk_want;
+    cl.sync();
+    int any = 0;
+    if (tid < SSV_CLUSTER) any = *cl.map_shared_rank(&sm.any, (unsigned int)tid);
+    any = __syncthreads_or(any);  // cluster-uniform
+    const unsigned int rank = cl.block_rank();
+    if (any) sieve_segment<false, SSV_THREADS>(sm.seg, 2ull * SSV_SEG * rank, SSV_SEG, bp, nbp, patt, first_large);
+    cl.sync();  // every block's segment is complete
+#pragma unroll
+    for (int k = 0; k < SSV_PER; k++) {
+        const uint32_t i = base + k * SSV_THREADS + tid;
+        if (i >= len) continue;
+        const unsigned long long x = v[k];
+        int r = -1;
+        if (x < 2ull) r = 0;
+        else if (!(x & 1ull)) r = (x == 2ull);
+        else if (any && x < SSV_LIMIT) {
+            const uint32_t o = (uint32_t)(x >> 1);  // byte o % SSV_SEG of block o / SSV_SEG
+            r = *cl.map_shared_rank(sm.seg + (o % SSV_SEG), o / SSV_SEG);
+        } else if (x < (1ull << 32)) {
+            const uint32_t y = (uint32_t)x;
+            bool comp = false;
+            for (int t = 0; t < td.n32; t++) comp |= (y * c_td_inv32[t] <= c_td_lim32[t]) && (y != c_td_p[t]);
+            if (comp) r = 0;
+            else if (y < td.sq32) r = 1;
+        }
+        if (r >= 0) out[i] = (uint8_t)r;
+        else {
+            const bool fp = x < FP_LIMIT;
+            const unsigned int kk = atomicAdd(&sm.n[fp ? 0 : 1], 1u);
+            const unsigned int at = fp ? kk : (unsigned int)(SSV_ELEMS - 1) - kk;
+            sm.v[at] = x;
+            sm.i[at] = i;
+        }
+    }
+    cl.sync();  // no block leaves while another may still read its segment (also orders the lists)
+    small_witness_tail<FULL32, SSV_ELEMS>(sm.v, sm.i, sm.n[0], sm.n[1], sm.p2tab, out);
+}
 
 template <bool FULL32>
 __global__ void __launch_bounds__(256) small_warp_kernel(const unsigned long long* __restrict__ N,
