@@ -116,6 +116,12 @@ void isprime_shutdown(void);
  *                    take one fused launch (trial division + Miller-Rabin per
  *                    element) instead of the plan / sieve / queue pipeline;
  *                    0 disables it; accepted in 0..2^32-1.  Never changes a bit of out.
+ * "small_sieve"      0 (default) or 1: within the short-array path, arrays longer
+ *                    than warp_max run as 8-block thread-block clusters that sieve
+ *                    [0, 2^20) in their shared memory and read each small element's
+ *                    byte through distributed shared memory (north_star (c),
+ *                    PAPER.md:279); larger elements keep trial division + strong
+ *                    tests.  Never changes a bit of out
  * "warp_max"         within the short-array path, n <= warp_max (default 4096)
  *                    runs one warp per element with one Eq 4 base per lane
  *                    (latency of one exponentiation instead of seven)

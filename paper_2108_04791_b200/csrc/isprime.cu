@@ -43,6 +43,8 @@ struct Options {
     int mr2_group = 3;       // 64-bit phase-2 bases run G at a time in lockstep (3 or 6)
     long long small_max = 1 << 17;  // n <= small_max (and force_path auto): one fused launch
     long long warp_max = 4096;      // n <= warp_max: one warp per element (one base per lane)
+    int small_sieve = 0;     // short arrays: 8-block clusters sieve [0, 2^20) in shared memory for their small values
+                             // (measured on par with small_kernel on C1: 13.6-15.3 vs 13.6-14.1 us; kept as an option)
     int sched = 2;           // witness kernels: 0 dynamic guided claims (atomics), 1 static interleaved rounds,
                              // 2 static for the 32-bit class then dynamic for the 64-bit classes
     int fuse_bits = 32;      // classify runs the strong tests itself below 2^fuse_bits: 0 (off), 32, 51
@@ -458,6 +460,39 @@ int device_impl(Ctx* c, const unsigned long long* dN, uint8_t* dout, size_t n, c
                 const unsigned blocks = (unsigned)(((size_t)len * 32 + 255) / 256);
                 if (g_opt.bases32 == 7) small_warp_kernel<true><<<blocks, 256, 0, s>>>(dN, dout, len, td);
                 else small_warp_kernel<false><<<blocks, 256, 0, s>>>(dN, dout, len, td);
+            } else if (g_opt.small_sieve) {
+                // cluster sieve of [0, 2^20) + gather; the grid is a whole number of clusters
+                const unsigned blocks = (unsigned)((((size_t)len + SSV_ELEMS - 1) / SSV_ELEMS + SSV_CLUSTER - 1) /
+                                                   SSV_CLUSTER * SSV_CLUSTER);
+                int first_large = FIRST_CROSS_PRIME_IDX;
+                while (first_large < c->nbp && c->hbp[first_large].x < (uint32_t)g_opt.warp_p) first_large++;
+                cudaLaunchConfig_t cfg = {};
+                cfg.gridDim = dim3(blocks);
+                cfg.blockDim = dim3(SSV_THREADS);
+                cfg.dynamicSmemBytes = sizeof(SsvSmem);
+                cfg.stream = s;
+                cudaLaunchAttribute at[1];
+                at[0].id = cudaLaunchAttributeClusterDimension;
+                at[0].val.clusterDim.x = SSV_CLUSTER;
+                at[0].val.clusterDim.y = 1;
+                at[0].val.clusterDim.z = 1;
+                cfg.attrs = at;
+                cfg.numAttrs = 1;
+                if (SSV_CLUSTER > 8) {
+                    cudaFuncSetAttribute((const void*)small_sieve_kernel<true>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+                    cudaFuncSetAttribute((const void*)small_sieve_kernel<false>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+                }
+                if (g_opt.bases32 == 7) {
+                    cudaFuncSetAttribute((const void*)small_sieve_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)sizeof(SsvSmem));
+                    cudaLaunchKernelEx(&cfg, small_sieve_kernel<true>, dN, dout, len, td, (const uint2*)c->bp, c->nbp,
+                                       (const uint8_t*)c->patt, first_large);
+                } else {
+                    cudaFuncSetAttribute((const void*)small_sieve_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)sizeof(SsvSmem));
+                    cudaLaunchKernelEx(&cfg, small_sieve_kernel<false>, dN, dout, len, td, (const uint2*)c->bp, c->nbp,
+                                       (const uint8_t*)c->patt, first_large);
+                }
             } else if (g_opt.bases32 == 7) {
                 small_kernel<true><<<(len + 255) / 256, 256, 0, s>>>(dN, dout, len, td);
             } else {
@@ -720,6 +755,7 @@ int isprime_set_option(const char* key, long long v) {
     else if (!strcmp(key, "mr_fixed_ns")) { if (v < 0) return ISP_EINVAL; g_opt.mr_fixed_ns = v; }
     else if (!strcmp(key, "kernel_timing")) { if (v < 0 || v > 1) return ISP_EINVAL; g_opt.kernel_timing = (int)v; }
     else if (!strcmp(key, "count_work")) { if (v < 0 || v > 1) return ISP_EINVAL; g_opt.count_work = (int)v; }
+    else if (!strcmp(key, "small_sieve")) { if (v < 0 || v > 1) return ISP_EINVAL; g_opt.small_sieve = (int)v; }
     else if (!strcmp(key, "mr2_group")) { if (v != 3 && v != 6) return ISP_EINVAL; g_opt.mr2_group = (int)v; }
     else if (!strcmp(key, "pdl")) { if (v < 0 || v > 1) return ISP_EINVAL; g_opt.pdl = (int)v; }
     else if (!strcmp(key, "sieve_cache")) { if (v < 0 || v > 1) return ISP_EINVAL; g_opt.sieve_cache = (int)v; }
@@ -749,6 +785,7 @@ long long isprime_get_option(const char* key) {
     if (!strcmp(key, "mr_fixed_ns")) return g_opt.mr_fixed_ns;
     if (!strcmp(key, "kernel_timing")) return g_opt.kernel_timing;
     if (!strcmp(key, "count_work")) return g_opt.count_work;
+    if (!strcmp(key, "small_sieve")) return g_opt.small_sieve;
     if (!strcmp(key, "sieve_cache")) return g_opt.sieve_cache;
     if (!strcmp(key, "mr2_group")) return g_opt.mr2_group;
     if (!strcmp(key, "pdl")) return g_opt.pdl;

@@ -657,7 +657,7 @@ __device__ __forceinline__ void sieve_segment(uint8_t* seg, unsigned long long s
         const uint32_t r = g0mod & 15u;
         const uint4* src = reinterpret_cast<const uint4*>(patt + (size_t)r * PRESIEVE_LEN + (g0mod - r));
         uint4* dst = reinterpret_cast<uint4*>(seg);
-        for (uint32_t k = tid; k < SEG_ODD / 16; k += NT) dst[k] = __ldg(src + k);
+        for (uint32_t k = tid; k < (seg_len + 15u) / 16u; k += NT) dst[k] = __ldg(src + k);
     }
     sieve_sync<NAMED, NT>();
     if (seg_lo == 0 && tid == 0) {  // v = 1 is not prime; 3, 5, 7, 11, 13 are
@@ -1974,15 +1974,21 @@ __constant__ uint32_t c_bases32_3[3] = {2u, 7u, 61u};
 // Elements at or above 2^20 take small_kernel's trial division + strong tests.
 // A cluster whose elements hold no odd value in [3, 2^20) skips the sieve (a
 // cluster-wide vote), so 64-bit inputs pay one cluster barrier for it.
-constexpr int SSV_THREADS = 512;
-constexpr int SSV_PER = 4;                                    // elements per thread
-constexpr int SSV_ELEMS = SSV_THREADS * SSV_PER;              // per block
-constexpr int SSV_CLUSTER = 8;
-constexpr uint32_t SSV_SEG = 65536;                           // odd values per block
-constexpr unsigned long long SSV_LIMIT = 2ull * SSV_SEG * SSV_CLUSTER;  // 2^20
-static_assert(SSV_SEG <= SEG_ODD, "sieve_segment initialises SEG_ODD bytes");
+#ifndef SSV_THREADS_DEF
+#define SSV_THREADS_DEF 512
+#endif
+#ifndef SSV_CLUSTER_DEF
+#define SSV_CLUSTER_DEF 8
+#endif
+constexpr int SSV_THREADS = SSV_THREADS_DEF;
+constexpr int SSV_ELEMS = 2048;                               // per block
+constexpr int SSV_PER = SSV_ELEMS / SSV_THREADS;              // elements per thread
+constexpr int SSV_CLUSTER = SSV_CLUSTER_DEF;                  // 8 portable, 16 with the non-portable opt-in
+constexpr unsigned long long SSV_LIMIT = 1ull << 20;          // the cluster sieves [0, 2^20)
+constexpr uint32_t SSV_SEG = (uint32_t)(SSV_LIMIT / 2 / SSV_CLUSTER);  // odd values per block
+static_assert(SSV_SEG <= SEG_ODD && SSV_SEG % 32 == 0, "sieve_segment: segment length");
 struct SsvSmem {
-    uint8_t seg[SEG_ODD];                 // this block's sieve segment (sieve_segment writes SEG_ODD bytes)
+    uint8_t seg[SSV_SEG];                 // this block's sieve segment, byte k <-> odd value 2 (rank SSV_SEG + k) + 1
     unsigned long long v[SSV_ELEMS];      // elements for the strong tests
     uint32_t i[SSV_ELEMS];
     double p2tab[8];

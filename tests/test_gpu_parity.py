@@ -52,7 +52,8 @@ def assert_same(got, exp, N=None):
 def _default_options():
     saved = {k: isp.get_option(k) for k in ("force_path", "bases32", "td_primes32", "td_primes64",
                                              "chunk_log2", "win64", "warp_p", "small_max", "warp_max",
-                                             "witness", "sieve_cache", "sched", "fuse_bits", "count_work")}
+                                             "witness", "sieve_cache", "sched", "fuse_bits", "count_work",
+                                             "small_sieve")}
     yield
     for k, v in saved.items():
         isp.set_option(k, v)
@@ -135,8 +136,9 @@ def test_all_below_2_20_every_path():
     assert exp.sum() == 82025
 
 
-@pytest.mark.parametrize("small_max,warp_max", [(0, 4096), (1 << 17, 0), (1 << 17, 4096), (1 << 17, 1 << 17)])
-def test_short_array_path_vs_pipeline(small_max, warp_max):
+@pytest.mark.parametrize("small_max,warp_max,small_sieve", [(0, 4096, 1), (1 << 17, 0, 1), (1 << 17, 0, 0),
+                                                             (1 << 17, 4096, 1), (1 << 17, 1 << 17, 1)])
+def test_short_array_path_vs_pipeline(small_max, warp_max, small_sieve):
     """Short arrays (n <= small_max) take one fused launch -- one warp per
     element with one base per lane up to warp_max elements (small_warp_kernel),
     one thread per element above (small_kernel); longer ones the plan / sieve /
@@ -144,6 +146,7 @@ def test_short_array_path_vs_pipeline(small_max, warp_max):
     every magnitude class through each must equal the oracle."""
     isp.set_option("small_max", small_max)
     isp.set_option("warp_max", warp_max)
+    isp.set_option("small_sieve", small_sieve)
     vals = np.array([int(r[0]) for r in _rows("special_values.txt")], dtype=np.uint64)
     cs = np.array(workloads.chernick_numbers(), dtype=np.uint64)
     near = np.concatenate([np.arange(max(0, c - 500), c + 500, dtype=np.uint64)
@@ -154,6 +157,39 @@ def test_short_array_path_vs_pipeline(small_max, warp_max):
         assert_same(gpu(N), exp, N)
         for n in (1, 31, 257):
             assert_same(gpu(N[:n]), exp[:n], N[:n])
+
+
+@pytest.mark.parametrize("bases32", [3, 7])
+def test_cluster_sieve_short_arrays(bases32):
+    """Short arrays through the cluster-sieve launch (small_sieve_kernel: 8
+    blocks sieve [0, 2^20) in their shared memory, elements read their byte
+    through distributed shared memory): every element of [0, 2^20) in shuffled
+    order, the values around the 2^20 limit and around each block's segment
+    boundary (multiples of 2^17), lengths that end mid-block and mid-cluster,
+    and clusters with no small odd value (the vote skips the sieve) beside
+    clusters with some."""
+    isp.set_option("small_max", 1 << 17)
+    isp.set_option("warp_max", 0)
+    isp.set_option("small_sieve", 1)  # an option (default 0: small_kernel)
+    isp.set_option("bases32", bases32)
+    rng = np.random.default_rng(2020 + bases32)
+    allv = rng.permutation(np.arange(1 << 20, dtype=np.uint64))
+    s20 = oracle.sieve(1 << 20)
+    for lo in range(0, 1 << 20, 1 << 17):
+        seg = allv[lo:lo + (1 << 17)]
+        assert_same(gpu(seg), s20[seg.astype(np.int64)], seg)
+    edges = np.concatenate([np.arange(max(0, b - 300), b + 300, dtype=np.uint64)
+                            for b in [k << 17 for k in range(1, 9)]])
+    for n in (1, 2047, 2048, 2049, 16383, 16384, 16385, 100_000):
+        N = np.resize(np.concatenate([edges, workloads.generate("C1", count=4096)]), n)
+        assert_same(gpu(N), oracle.isprime(N), N)
+    # 64-bit values only in the first clusters, small ones only in the last
+    big = workloads.generate("C3", count=40_000)
+    small = workloads.generate("C1", count=60_000)
+    N = np.concatenate([big, small])
+    assert_same(gpu(N), oracle.isprime(N), N)
+    N = np.concatenate([small[:20_000], big[:20_000] | np.uint64(1), np.array([2, 4, 1, 0], dtype=np.uint64)])
+    assert_same(gpu(N), oracle.isprime(N), N)
 
 
 def test_bpsw_witness_option():
