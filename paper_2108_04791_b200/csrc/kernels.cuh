@@ -1625,20 +1625,24 @@ __device__ __forceinline__ void stage_flush(WarpStage& st, unsigned int& n, unsi
 // start costs an atomic round trip per round, which cheap 32-bit entries
 // cannot hide.  div[r] = 0: fixed MR_CHUNK for region r.
 constexpr unsigned int MR_CHUNK = 128;
+#ifndef MR1_CHUNK_DEF
+#define MR1_CHUNK_DEF 512
+#endif
+constexpr unsigned int MR1_CHUNK = MR1_CHUNK_DEF;  // phase 1: largest claim (128 / 256 / 512: C5 mr1 0.937 / 0.931 / 0.928 ms, C3 equal)
 constexpr unsigned int MR_CHUNK_TAIL = 32;
 
 __device__ __forceinline__ bool next_chunk(const unsigned int (&size)[3], unsigned int* cur, int& r, int& tried,
                                            unsigned int& start, unsigned int& end, unsigned int nw,
-                                           const unsigned int (&div)[3]) {
+                                           const unsigned int (&div)[3], unsigned int maxch = MR_CHUNK) {
     const int lane = threadIdx.x & 31;
     while (tried != 7) {
         if (!((tried >> r) & 1)) {
-            unsigned int s0 = 0xFFFFFFFFu, ch = MR_CHUNK;
+            unsigned int s0 = 0xFFFFFFFFu, ch = maxch;
             if (size[r] && lane == 0) {
                 const unsigned int seen = *reinterpret_cast<volatile unsigned int*>(&cur[r]);  // racy estimate
                 if (div[r] && seen < size[r]) {
                     const unsigned int g = ((size[r] - seen) / (div[r] * nw) + 31u) & ~31u;
-                    ch = g < MR_CHUNK_TAIL ? MR_CHUNK_TAIL : (g > MR_CHUNK ? MR_CHUNK : g);
+                    ch = g < MR_CHUNK_TAIL ? MR_CHUNK_TAIL : (g > maxch ? maxch : g);
                 }
                 s0 = seen < size[r] ? atomicAdd(&cur[r], ch) : seen;
             }
@@ -1660,7 +1664,8 @@ __device__ __forceinline__ bool next_chunk(const unsigned int (&size)[3], unsign
 // interleaved share of every warp is balanced to within a round.
 __device__ __forceinline__ bool next_work(int sched, const unsigned int (&size)[3], unsigned int* cur, int& r,
                                           int& tried, unsigned int& start, unsigned int& end, unsigned int& step,
-                                          unsigned int nw, unsigned int gw, const unsigned int (&div)[3]) {
+                                          unsigned int nw, unsigned int gw, const unsigned int (&div)[3],
+                                          unsigned int maxch = MR_CHUNK) {
     if (sched == 2) {
         // static rounds of region 0 (short, uniform 32-bit entries: claims would
         // cost an atomic per few hundred cycles of work), then dynamic claims
@@ -1677,7 +1682,7 @@ __device__ __forceinline__ bool next_work(int sched, const unsigned int (&size)[
         }
         if (r == 0) r = 1 + (int)(gw & 1u);
         step = 32u;
-        return next_chunk(size, cur, r, tried, start, end, nw, div);
+        return next_chunk(size, cur, r, tried, start, end, nw, div, maxch);
     }
     if (sched) {
         while (tried != 7) {
@@ -1695,7 +1700,7 @@ __device__ __forceinline__ bool next_work(int sched, const unsigned int (&size)[
         return false;
     }
     step = 32u;
-    return next_chunk(size, cur, r, tried, start, end, nw, div);
+    return next_chunk(size, cur, r, tried, start, end, nw, div, maxch);
 }
 
 __device__ __forceinline__ unsigned long long warp_sum(unsigned long long v) {
@@ -1744,7 +1749,7 @@ mr1_kernel(DevPlan* __restrict__ plan, Queues q, const unsigned long long* __res
     // 64-bit classes shrink their chunks towards the end
     const unsigned int div[3] = {0u, 2u, 2u};
     const unsigned int nw = gridDim.x * (MR1_THREADS / 32);
-    while (next_work(sched, size, plan->cur1, r, tried, start, end, step, nw, gwarp, div)) {
+    while (next_work(sched, size, plan->cur1, r, tried, start, end, step, nw, gwarp, div, MR1_CHUNK)) {
         const uint32_t* const sr = q.s + (r == 0 ? 0u : r == 1 ? c32 : c32 + nf);  // region of s
         // values are gathered from N by index; the next round's index and value
         // are loaded before this round's ladder (one gather latency per claim)
