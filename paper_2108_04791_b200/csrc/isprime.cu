@@ -243,6 +243,7 @@ int init_ctx(Ctx* c) {
     c->q.segh = c->segh;
     CK(cudaFuncSetAttribute(sieve_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SEG_ODD));
     CK(cudaFuncSetAttribute(dense_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * SEG_ODD));
+    CK(cudaFuncSetAttribute(dense2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * SEG_ODD));
     c->grid_sieve = c->sms * occupancy((const void*)sieve_kernel, SIEVE_THREADS, SEG_ODD);
     CK(cudaFuncSetAttribute((const void*)classify_kernel<24, 24>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                             (int)sizeof(ClsSmem)));
@@ -537,6 +538,9 @@ int device_impl(Ctx* c, const unsigned long long* dN, uint8_t* dout, size_t n, c
             launch_k(dense_kernel, c->sms, DENSE_THREADS, 2 * SEG_ODD, s, c->plan, N, out, len, c->bp, c->nbp, c->patt,
                      first_large, vec);
             CKL("dense_kernel");
+            launch_k(dense2_kernel, c->sms, DENSE_THREADS, 2 * SEG_ODD, s, c->plan, N, out, len, c->bp, c->nbp,
+                     c->patt, first_large, vec);
+            CKL("dense2_kernel");
         }
         const uint32_t ntiles = (len + CLS_TILE - 1) / CLS_TILE;
         const int gcls = (int)(ntiles < (uint32_t)c->grid_cls ? ntiles : (uint32_t)c->grid_cls);

@@ -897,17 +897,27 @@ __device__ __forceinline__ void dense_body(DevPlan* __restrict__ plan, uint8_t* 
 // Stride 1 and stride 2 are separate kernels (both are launched; the one
 // whose stride the plan did not find exits at once): one kernel with both
 // bodies made ptxas spill and cost C4 4.5 % (tools/ab.sh).
-// One launch for both strides (a chunk that is not a dense range costs one
-// early-exit launch instead of two).
+// One kernel per stride: a single kernel holding both bodies spills more and
+// ran C4 4 % slower (6.26 -> 6.52 ms, round 2), worth more than the second
+// early-exit launch it saves a chunk that is not a dense range (~1 us).
 __global__ void __launch_bounds__(DENSE_THREADS, 1)
 dense_kernel(DevPlan* __restrict__ plan, const unsigned long long* __restrict__ N, uint8_t* __restrict__ out,
              uint32_t len, const uint2* __restrict__ bp, int nbp, const uint8_t* __restrict__ patt, int first_large,
              int vec) {
     pdl_wait();
     extern __shared__ __align__(16) uint8_t dseg[];  // two SEG_ODD buffers
-    if (!plan->dense) return;
-    if (plan->dense_d == 1) dense_body<1, DENSE_PRODUCERS1>(plan, dseg, N, out, len, bp, nbp, patt, first_large, vec);
-    else dense_body<2, DENSE_PRODUCERS2>(plan, dseg, N, out, len, bp, nbp, patt, first_large, vec);
+    if (!plan->dense || plan->dense_d != 1) return;
+    dense_body<1, DENSE_PRODUCERS1>(plan, dseg, N, out, len, bp, nbp, patt, first_large, vec);
+}
+
+__global__ void __launch_bounds__(DENSE_THREADS, 1)
+dense2_kernel(DevPlan* __restrict__ plan, const unsigned long long* __restrict__ N, uint8_t* __restrict__ out,
+              uint32_t len, const uint2* __restrict__ bp, int nbp, const uint8_t* __restrict__ patt, int first_large,
+              int vec) {
+    pdl_wait();
+    extern __shared__ __align__(16) uint8_t dseg[];
+    if (!plan->dense || plan->dense_d != 2) return;
+    dense_body<2, DENSE_PRODUCERS2>(plan, dseg, N, out, len, bp, nbp, patt, first_large, vec);
 }
 
 // ------------------------------------------------------------- A2: classify
