@@ -2091,8 +2091,15 @@ __global__ void __launch_bounds__(256) small_warp_kernel(const unsigned long lon
     else if (!(v & 1ull)) r = (v == 2ull);
     else if (v < (1ull << 32)) {
         const uint32_t x = (uint32_t)v;
-        bool comp = false;
-        for (int t = 0; t < td.n32; t++) comp |= (x * c_td_inv32[t] <= c_td_lim32[t]) && (x != c_td_p[t]);
+        bool comp;
+        if (td.n32 == 16) {  // the default depth with immediate operands
+            constexpr uint32_t kLast16 = kOddPrimes[15];
+            comp = td_primes<0, 16>(x);
+            if (x <= kLast16) comp = !((kSmallOddPrimeMask[x >> 6] >> ((x >> 1) & 31u)) & 1u);
+        } else {
+            comp = false;
+            for (int t = 0; t < td.n32; t++) comp |= (x * c_td_inv32[t] <= c_td_lim32[t]) && (x != c_td_p[t]);
+        }
         if (comp) r = 0;
         else if (x < td.sq32) r = 1;
     }
