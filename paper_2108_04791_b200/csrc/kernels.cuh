@@ -965,6 +965,7 @@ struct ClsSmem {
     ClsWarp w[CLS_THREADS / 32];
     FzWarp f[CLS_THREADS / 32];
     unsigned int cur;     // entries used in this block's queue segment
+    unsigned int wt_next; // next warp-tile of this block to classify
     unsigned int h[65];   // bit-length histogram of this block's survivors (for the sort)
     unsigned int fzc[4];  // fused: base-2 tests (32-bit, FP64 class), base-2 passes (32-bit, FP64 class)
     double p2tab[8];      // {1, a, a^2, a^3} for a = 7, 61 (sprp_small32_f64)
@@ -1119,11 +1120,21 @@ __device__ __forceinline__ void classify_tiles(const unsigned long long* __restr
                                                uint32_t segbase, unsigned long long span, uint32_t wlo32,
                                                uint32_t spanm1, uint32_t spanm1w, uint32_t ntiles, ClsSmem& sm,
                                                ClsWarp& ws, int lane, int wid, FzParams fz) {
-    uint32_t tk = 0;  // tile number within this block (packed queue entries)
     FzWarp& fw = sm.f[wid];
     uint32_t z = 0;   // fused lists' lengths (fz_na / fz_nb / fz_nc)
-    for (uint32_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, tk++) {
-        const uint32_t wbase = tile * CLS_TILE + 256u * wid;
+    // The block's warp-tiles (its tiles blockIdx.x + k gridDim.x, 32 warp-tiles
+    // each) are claimed one at a time from a shared counter (round 2): a warp
+    // whose tiles held more candidates does not hold up the block at its end.
+    constexpr uint32_t WPT = CLS_THREADS / 32;  // warp-tiles per tile
+    const uint32_t nwt = ((ntiles - blockIdx.x + gridDim.x - 1) / gridDim.x) * WPT;
+    for (;;) {
+        uint32_t jw = 0;
+        if (lane == 0) jw = atomicAdd(&sm.wt_next, 1u);
+        jw = __shfl_sync(0xffffffffu, jw, 0);
+        if (jw >= nwt) break;
+        const uint32_t tk = jw / WPT, slot = jw % WPT;  // tile number within this block, warp-tile in it
+        const uint32_t tile = blockIdx.x + tk * gridDim.x;
+        const uint32_t wbase = tile * CLS_TILE + 256u * slot;
         const bool full = wbase + 256u <= len;
         // ---- load, trivial cases, window gather, class
         unsigned long long v[8];
@@ -1305,7 +1316,7 @@ __device__ __forceinline__ void classify_tiles(const unsigned long long* __restr
             // in the tile, the tile number within the block and the value's bit
             // length (the sort key); the value itself is re-read from N by the
             // witness kernels.
-            const uint32_t tag = (tk << QE_TILE_BITS) | (256u * wid);
+            const uint32_t tag = (tk << QE_TILE_BITS) | (256u * slot);
             uint32_t s32 = 0, s64 = 0;  // fused: survivors compacted in list32 / list64
             // fused 32-bit class only for warp-tiles with at least a round of
             // candidates (config C2: ~128); a few per tile (C5: the window takes
@@ -1459,7 +1470,7 @@ classify_kernel(const unsigned long long* __restrict__ N, uint8_t* __restrict__ 
     ClsWarp& ws = sm.w[wid];
     const uint32_t ntiles = (len + CLS_TILE - 1) / CLS_TILE;
     for (int b = tid; b < 65; b += CLS_THREADS) sm.h[b] = 0;
-    if (tid == 0) sm.cur = 0;
+    if (tid == 0) { sm.cur = 0; sm.wt_next = 0; }
     if (tid < 4) sm.fzc[tid] = 0;
     if (tid < 2) sm.fzw[tid] = 0;
     small_base_table<2>(sm.p2tab, c_bases32_red64);
