@@ -961,9 +961,21 @@ struct FzParams {
     int p2;       // remaining bases below 2^32: 0 {7, 61}; 1 the six of Eq 4; 2 one hashed base
     int wit;      // option witness (2: Jaeschke's set below kJaeschkeBound4 in the FP64 class)
 };
+// Trial-division candidates carried between warp-tiles (round 2): a
+// warp-tile's candidates beyond its last full round of 32 wait here, and a
+// round runs when 32 have gathered, so the TD loops run on full warps (C5: 8
+// candidates below 2^32 and 64 +- 8 above per warp-tile).  t: the packed queue
+// entry's tag (tile number within the block, offset in the tile).
+struct TdCarry {
+    unsigned long long v64[64];
+    uint32_t t64[64];
+    uint32_t v32[64];
+    uint32_t t32[64];
+};
 struct ClsSmem {
     ClsWarp w[CLS_THREADS / 32];
     FzWarp f[CLS_THREADS / 32];
+    TdCarry c[CLS_THREADS / 32];
     unsigned int cur;     // entries used in this block's queue segment
     unsigned int wt_next; // next warp-tile of this block to classify
     unsigned int h[65];   // bit-length histogram of this block's survivors (for the sort)
@@ -1113,6 +1125,86 @@ __device__ __noinline__ void fz_flush(FzWarp& f, uint32_t z, unsigned int* fzc, 
     while (fz_nc(z)) z = fz_phase2<CW>(f, z, true, fp, tlo, nullptr, out, p2tab, fzw);
 }
 
+// Element index in the chunk of a carried candidate (tag: tile number within
+// the block << QE_TILE_BITS | offset in the tile).
+__device__ __forceinline__ uint32_t tag_index(uint32_t t) {
+    return (blockIdx.x + (t >> QE_TILE_BITS) * gridDim.x) * (uint32_t)CLS_TILE + (t & (uint32_t)(CLS_TILE - 1));
+}
+
+// Queue one survivor group (shared-memory cursor, bit-length histogram).
+__device__ __forceinline__ void queue_survivors(bool surv, uint32_t entry_tag, uint32_t bl, ClsSmem& sm,
+                                                const Queues& q, uint32_t segbase, uint32_t seg_stride, int lane) {
+    const uint32_t m = __ballot_sync(0xffffffffu, surv);
+    if (!m) return;
+    uint32_t o = 0;
+    if (lane == 0) o = atomicAdd(&sm.cur, (unsigned int)__popc(m));
+    o = segbase + __shfl_sync(0xffffffffu, o, 0);
+    if (surv) {
+        const uint32_t at = o + __popc(m & ((1u << lane) - 1u));
+        ISP_CHECK(at < segbase + seg_stride && at < q.cap, 104);
+        q.q[at] = entry_tag | ((bl - 1u) << 26);
+        atomicAdd(&sm.h[bl], 1u);
+    }
+}
+
+// One trial-division round over the first min(n, 32) carried 32-bit
+// candidates (the rest shift down).  A candidate that is prime by the
+// (p_next)^2 bound is marked in the warp's result tile while its warp-tile
+// (key = tag >> 8) is the one being classified, straight in out otherwise.
+template <int N32>
+__device__ __forceinline__ void carry_round32(TdCarry& c, uint32_t& n, uint32_t key, uint8_t* res,
+                                              uint8_t* __restrict__ out, const TDParams& td, ClsSmem& sm,
+                                              const Queues& q, uint32_t segbase, uint32_t seg_stride, int lane) {
+    const bool act = (uint32_t)lane < n;
+    const uint32_t x = act ? c.v32[lane] : 0u, t = act ? c.t32[lane] : 0u;
+    __syncwarp();
+    if ((uint32_t)lane + 32u < n) { c.v32[lane] = c.v32[lane + 32]; c.t32[lane] = c.t32[lane + 32]; }
+    n = n > 32u ? n - 32u : 0u;
+    __syncwarp();
+    bool surv = false;
+    if (act) {
+        bool comp = td_primes<0, N32>(x);
+        if constexpr (N32 > 0) {
+            constexpr uint32_t kLast = kOddPrimes[N32 - 1];
+            if (x <= kLast) comp = !((kSmallOddPrimeMask[x >> 6] >> ((x >> 1) & 31u)) & 1u);
+        }
+        surv = !comp;
+    }
+    const bool small = surv && x < td.sq32;
+    if (small) {
+        if ((t >> 8) == key) res[t & 255u] = 1;
+        else out[tag_index(t)] = 1;
+    }
+    surv &= !small;
+    queue_survivors(surv, t, 32u - __clz(x), sm, q, segbase, seg_stride, lane);
+}
+
+// The same for the carried candidates at or above 2^32 (always queued).
+template <int N64>
+__device__ __forceinline__ void carry_round64(TdCarry& c, uint32_t& n, const TDParams& td, ClsSmem& sm,
+                                              const Queues& q, uint32_t segbase, uint32_t seg_stride, int lane) {
+    const bool act = (uint32_t)lane < n;
+    const unsigned long long x = act ? c.v64[lane] : 0ull;
+    const uint32_t t = act ? c.t64[lane] : 0u;
+    __syncwarp();
+    if ((uint32_t)lane + 32u < n) { c.v64[lane] = c.v64[lane + 32]; c.t64[lane] = c.t64[lane + 32]; }
+    n = n > 32u ? n - 32u : 0u;
+    __syncwarp();
+    bool surv = false;
+    if (act) surv = !(N64 > 0 && td64_fp<N64>(x, td.rnd));
+    queue_survivors(surv, t, 64u - __clzll((long long)x), sm, q, segbase, seg_stride, lane);
+}
+
+// Every carried candidate left, after the last warp-tile (results go to out).
+template <int N32, int N64>
+__device__ __noinline__ void carry_flush(TdCarry& c, uint32_t n32, uint32_t n64, uint8_t* __restrict__ out,
+                                         const TDParams& td, ClsSmem& sm, const Queues& q, uint32_t segbase,
+                                         uint32_t seg_stride) {
+    const int lane = threadIdx.x & 31;
+    while (n32) carry_round32<N32>(c, n32, 0xFFFFFFFFu, nullptr, out, td, sm, q, segbase, seg_stride, lane);
+    while (n64) carry_round64<N64>(c, n64, td, sm, q, segbase, seg_stride, lane);
+}
+
 template <int N32, int N64, bool UNI, bool CW>
 __device__ __forceinline__ void classify_tiles(const unsigned long long* __restrict__ N, uint8_t* __restrict__ out,
                                                uint32_t len, const uint32_t* __restrict__ bitmap, const Queues& q,
@@ -1122,6 +1214,8 @@ __device__ __forceinline__ void classify_tiles(const unsigned long long* __restr
                                                ClsWarp& ws, int lane, int wid, FzParams fz) {
     FzWarp& fw = sm.f[wid];
     uint32_t z = 0;   // fused lists' lengths (fz_na / fz_nb / fz_nc)
+    TdCarry& cw = sm.c[wid];
+    uint32_t nc32 = 0, nc64 = 0;  // carried trial-division candidates (< 32 between warp-tiles)
     // The block's warp-tiles (its tiles blockIdx.x + k gridDim.x, 32 warp-tiles
     // each) are claimed one at a time from a shared counter (round 2): a warp
     // whose tiles held more candidates does not hold up the block at its end.
@@ -1322,7 +1416,12 @@ __device__ __forceinline__ void classify_tiles(const unsigned long long* __restr
             // candidates (config C2: ~128); a few per tile (C5: the window takes
             // most small values) cost classify more than the queue round trip
             const bool fz32 = fz.bits && n32 >= 32u;
-            for (uint32_t k0 = 0; k0 < n32; k0 += 32) {
+            // queue path: full rounds from the list, the remainder is carried
+            // (chunks with a sieve window, config C5; the single-class
+            // instantiation without a window (C2, C3) keeps whole-list rounds:
+            // its tiles carry little, and the extra code cost C2 4 %)
+            const uint32_t n32d = (UNI || fz32) ? n32 : (n32 & ~31u), n64d = UNI ? n64 : (n64 & ~31u);
+            for (uint32_t k0 = 0; k0 < n32d; k0 += 32) {
                 const uint32_t k = k0 + lane;
                 bool surv = false;
                 uint32_t x = 0;
@@ -1370,7 +1469,7 @@ __device__ __forceinline__ void classify_tiles(const unsigned long long* __restr
                     }
                 }
             }
-            for (uint32_t k0 = 0; k0 < n64; k0 += 32) {
+            for (uint32_t k0 = 0; k0 < n64d; k0 += 32) {
                 const uint32_t k = k0 + lane;  // back index: slot 255 - k
                 bool surv = false;
                 unsigned long long x = 0;
@@ -1406,6 +1505,31 @@ __device__ __forceinline__ void classify_tiles(const unsigned long long* __restr
                         q.q[at] = (tag + pk) | ((bl - 1u) << 26);
                         atomicAdd(&sm.h[bl], 1u);
                     }
+                }
+            }
+            // remainders to the carries; full carried rounds at once (their
+            // small primes of this warp-tile still land in ws.res)
+            if constexpr (!UNI) {
+                const uint32_t key = tag >> 8;
+                const uint32_t r32 = n32 - n32d, r64 = n64 - n64d;
+                if (r32) {
+                    if ((uint32_t)lane < r32) {
+                        cw.v32[nc32 + lane] = (uint32_t)ws.val[n32d + lane];
+                        cw.t32[nc32 + lane] = tag + ws.pos[n32d + lane];
+                    }
+                    nc32 += r32;
+                    __syncwarp();
+                    if (nc32 >= 32u)
+                        carry_round32<N32>(cw, nc32, key, ws.res, out, td, sm, q, segbase, seg_stride, lane);
+                }
+                if (r64) {
+                    if ((uint32_t)lane < r64) {
+                        cw.v64[nc64 + lane] = ws.val[255u - (n64d + lane)];
+                        cw.t64[nc64 + lane] = tag + ws.pos[255u - (n64d + lane)];
+                    }
+                    nc64 += r64;
+                    __syncwarp();
+                    if (nc64 >= 32u) carry_round64<N64>(cw, nc64, td, sm, q, segbase, seg_stride, lane);
                 }
             }
             // fused: this tile's survivors join list a (< 32 entries between
@@ -1445,6 +1569,9 @@ __device__ __forceinline__ void classify_tiles(const unsigned long long* __restr
         }
     }
     // fused lists: the partial rounds left (every tile is stored: results go to out)
+    if constexpr (!UNI) {
+        if (nc32 | nc64) carry_flush<N32, N64>(cw, nc32, nc64, out, td, sm, q, segbase, seg_stride);
+    }
     if (z) fz_flush<CW>(fw, z, sm.fzc, fz, out, sm.p2tab, sm.fzw);
 }
 
