@@ -23,10 +23,13 @@ CHECKED = os.path.join(ROOT, "paper_2108_04791_b200", "libisprime_checked.so")
 
 @pytest.mark.parametrize("workload", ["dense", "pipeline", "c3", "small", "chunks", "full"])
 def test_checked_build(workload):
-    if not os.path.exists(CHECKED):
+    sys.path.insert(0, ROOT)
+    from paper_2108_04791_b200 import _build
+    if not os.path.exists(CHECKED) or any(os.path.getmtime(src) > os.path.getmtime(CHECKED)
+                                          for src in _build._sources()):
         sys.path.insert(0, os.path.join(ROOT, "tools"))
         import build_checked
-        build_checked.build()
+        build_checked.build()  # absent or older than the sources it checks
     env = dict(os.environ, ISPRIME_LIB=CHECKED)
     r = subprocess.run([sys.executable, os.path.join(ROOT, "tools", "sanitize.py"), workload], env=env,
                        capture_output=True, text=True, timeout=900)
