@@ -112,6 +112,17 @@ void isprime_shutdown(void);
  *                    selected witness set) itself, per warp on rounds of 32, on
  *                    the FP64 pipe.  0 queues every survivor for the witness
  *                    kernels.  Same tests, same bases: never changes a bit of out
+ * "graph"            0 (default) or 1: the pipeline of a call is captured once into a
+ *                    CUDA graph (cached per device, keyed by the call's pointers,
+ *                    n, the options and the scratch buffers; 8 kept, least recently
+ *                    used evicted) and replayed; conditional nodes that the plan and
+ *                    classify kernels set on the device skip the sieve, the dense-range
+ *                    kernels and the sort + witness kernels when they have nothing to
+ *                    do.  Each replay reads the current contents of N, so a graph
+ *                    never caches a result.  0: one stream launch per stage, chained
+ *                    by programmatic dependent launch (measured faster on B200: a
+ *                    conditional node costs more than the early-exit launch it
+ *                    skips).  Never changes a bit of out
  * "small_max"        arrays with n <= small_max (default 131072) and force_path 0
  *                    take one fused launch (trial division + Miller-Rabin per
  *                    element) instead of the plan / sieve / queue pipeline;

@@ -48,6 +48,11 @@ struct Options {
     int sched = 2;           // witness kernels: 0 dynamic guided claims (atomics), 1 static interleaved rounds,
                              // 2 static for the 32-bit class then dynamic for the 64-bit classes
     int fuse_bits = 32;      // classify runs the strong tests itself below 2^fuse_bits: 0 (off), 32, 51
+    int graph = 0;           // 1: pipeline calls replay a cached CUDA graph whose conditional nodes skip the stages
+                             // the plan / classify find empty (sieve, dense, sort + witness kernels).  Measured
+                             // slower than the PDL-chained stream launches (C2 0.159 -> 0.177 ms, C5 3.632 ->
+                             // 3.663 ms, C4 6.52 -> 6.63 ms: a conditional node breaks the programmatic edges
+                             // and costs more than the ~1.3 us early-exit launch it skips), so off by default
     int witness = 0;         // 0: Eq 4 bases; 1: Baillie-PSW for n >= 2^50; 2: reduced sets by magnitude     // 1: a call may reuse the bitmap sieved by an earlier call
 };
 
@@ -56,6 +61,10 @@ bool g_opt_env_read = false;
 std::mutex g_mu;
 std::string g_err;
 unsigned long long g_launches = 0;
+unsigned long long g_opt_epoch = 0;  // bumped by every option change: a cached graph bakes the options in
+bool g_pdl_ok = true;                // false: the next launch follows a conditional node (no programmatic edge)
+int g_gon = 0;                       // launches are being captured into a graph with conditional stages
+unsigned long long g_gh_tail = 0;    // conditional handle classify sets when it queued survivors
 
 struct Ctx {
     int dev = -1;
@@ -83,6 +92,15 @@ struct Ctx {
     unsigned long long* hin[2] = {nullptr, nullptr};
     uint8_t* hout[2] = {nullptr, nullptr};
     size_t hcap = 0;
+    // CUDA graphs of the pipeline (option "graph"), keyed by the call's
+    // pointers, size, options and scratch; least recently used evicted past 8
+    struct GraphEntry {
+        const void* N; const void* out; size_t n; unsigned long long epoch; const void* qmem; size_t qcap;
+        cudaGraphExec_t exec; unsigned long long used;
+    };
+    std::vector<GraphEntry> graphs;
+    unsigned long long graph_clock = 0;
+    cudaStream_t gs = nullptr, gs2 = nullptr;  // capture streams (the caller's may be the legacy stream)
 };
 
 std::vector<Ctx*> g_ctx;
@@ -178,9 +196,10 @@ cudaError_t launch_k(void (*k)(KArgs...), unsigned grid, unsigned block, size_t 
     cfg.stream = s;
     cudaLaunchAttribute at[1];
     at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-    at[0].val.programmaticStreamSerializationAllowed = g_opt.pdl ? 1 : 0;
+    at[0].val.programmaticStreamSerializationAllowed = (g_opt.pdl && g_pdl_ok) ? 1 : 0;
     cfg.attrs = at;
     cfg.numAttrs = 1;
+    g_pdl_ok = true;
     return cudaLaunchKernelEx(&cfg, k, static_cast<KArgs>(args)...);
 }
 
@@ -346,6 +365,8 @@ void launch_cls(K k, int g, cudaStream_t s, const unsigned long long* N, uint8_t
     fz.bits = g_opt.fuse_bits;
     fz.p2 = (g_opt.witness == 2 && g_opt.bases32 != 7) ? 2 : g_opt.bases32 == 7 ? 1 : 0;
     fz.wit = g_opt.witness;
+    fz.gon = g_gon;
+    fz.gh_tail = g_gh_tail;
     launch_k(k, g, CLS_THREADS, sizeof(ClsSmem), s, N, out, len, c->plan, c->bitmap, c->q, td, vin, vout, ss, fz);
 }
 
@@ -417,6 +438,177 @@ int launch_mr2(Ctx* c, cudaStream_t s, const unsigned long long* N, uint8_t* out
         default: launch_mr2_w<3, 6>(c, s, N, out, len, grid, full, cw); break;
     }
     CKL("mr2_kernel");
+    return ISP_OK;
+}
+
+// Graph capture of the pipeline (option "graph"): the capture stream and the
+// graph being built.  nullptr: plain stream launches.
+struct GBuild { cudaGraph_t g; cudaStream_t s2; };
+
+// One stage of the pipeline that may find nothing to do.  Plain launches: the
+// stage's kernels are enqueued on s (each exits at once when the plan says so).
+// Graph capture: the stage becomes the body of an IF conditional node on handle
+// h, which the plan or classify kernel sets on the device, so an empty stage
+// costs no launch at all.  The kernel after a conditional node has no
+// programmatic (PDL) edge to it.
+template <typename F>
+int cond_stage(GBuild* gb, cudaStream_t s, cudaGraphConditionalHandle h, F&& body) {
+    if (!gb) return body(s);
+    const cudaGraphNode_t* deps = nullptr;
+    size_t nd = 0;
+    cudaStreamCaptureStatus st;
+    CK(cudaStreamGetCaptureInfo(s, &st, nullptr, nullptr, &deps, &nd));
+    cudaGraphNodeParams np = {};
+    np.type = cudaGraphNodeTypeConditional;
+    np.conditional.handle = h;
+    np.conditional.type = cudaGraphCondTypeIf;
+    np.conditional.size = 1;
+    cudaGraphNode_t node;
+    CK(cudaGraphAddNode(&node, gb->g, deps, nd, &np));
+    CK(cudaStreamUpdateCaptureDependencies(s, &node, 1, cudaStreamSetCaptureDependencies));
+    CK(cudaStreamBeginCaptureToGraph(gb->s2, np.conditional.phGraph_out[0], nullptr, nullptr, 0,
+                                     cudaStreamCaptureModeRelaxed));
+    g_pdl_ok = false;
+    const int rc = body(gb->s2);
+    cudaGraph_t bg = nullptr;
+    const cudaError_t e = cudaStreamEndCapture(gb->s2, &bg);
+    g_pdl_ok = false;
+    if (rc != ISP_OK) return rc;
+    if (e != cudaSuccess) return cuda_fail(e, "cudaStreamEndCapture (conditional stage)");
+    return ISP_OK;
+}
+
+// The pipeline stages of every device chunk of dN[0..n), on s (or captured
+// into gb's graph).
+int enqueue_chunks(Ctx* c, const unsigned long long* dN, uint8_t* dout, size_t n, size_t chunk, PlanParams P,
+                   const TDParams& td, cudaStream_t s, GBuild* gb) {
+    int rc = ISP_OK;
+    for (size_t base = 0; base < n; base += chunk) {
+        const uint32_t len = (uint32_t)((n - base) < chunk ? (n - base) : chunk);
+        const unsigned long long* N = dN + base;
+        uint8_t* out = dout + base;
+        P.invalidate = (base == 0 && !g_opt.sieve_cache) ? 1 : 0;
+        cudaGraphConditionalHandle gh[4] = {0, 0, 0, 0};  // sieve, dense stride 1, dense stride 2, tail
+        if (gb)
+            for (int k = 0; k < 4; k++) CK(cudaGraphConditionalHandleCreate(&gh[k], gb->g, 0u, cudaGraphCondAssignDefault));
+        P.gon = gb ? 1 : 0;
+        for (int k = 0; k < 3; k++) P.gh[k] = (unsigned long long)gh[k];
+        g_gon = gb ? 1 : 0;
+        g_gh_tail = (unsigned long long)gh[3];
+        {
+            KScope ks(K_PLAN, s);
+            launch_k(plan_kernel, 1, PLAN_THREADS, 0, s, N, (unsigned long long)len, c->plan, P);
+            CKL("plan_kernel");
+        }
+        // first base prime >= warp_p (the warp-cooperative / per-thread split)
+        int first_large = FIRST_CROSS_PRIME_IDX;
+        while (first_large < c->nbp && c->hbp[first_large].x < (uint32_t)g_opt.warp_p) first_large++;
+        rc = cond_stage(gb, s, gh[0], [&](cudaStream_t st) -> int {
+            KScope ks(K_SIEVE, st);
+            launch_k(sieve_kernel, c->grid_sieve, SIEVE_THREADS, SEG_ODD, st, c->plan, c->bitmap, c->bp, c->nbp, c->patt,
+                     first_large);
+            CKL("sieve_kernel");
+            return ISP_OK;
+        });
+        if (rc != ISP_OK) return rc;
+        {
+            // 16-byte loads of element pairs need N 16-B aligned and out 2-B aligned
+            const int vec = ((((uintptr_t)N & 15) == 0) && (((uintptr_t)out & 1) == 0)) ? 1 : 0;
+            rc = cond_stage(gb, s, gh[1], [&](cudaStream_t st) -> int {
+                KScope ks(K_DENSE, st);
+                launch_k(dense_kernel, c->sms, DENSE_THREADS, 2 * SEG_ODD, st, c->plan, N, out, len, c->bp, c->nbp,
+                         c->patt, first_large, vec);
+                CKL("dense_kernel");
+                return ISP_OK;
+            });
+            if (rc != ISP_OK) return rc;
+            rc = cond_stage(gb, s, gh[2], [&](cudaStream_t st) -> int {
+                KScope ks(K_DENSE, st);
+                launch_k(dense2_kernel, c->sms, DENSE_THREADS, 2 * SEG_ODD, st, c->plan, N, out, len, c->bp, c->nbp,
+                         c->patt, first_large, vec);
+                CKL("dense2_kernel");
+                return ISP_OK;
+            });
+            if (rc != ISP_OK) return rc;
+        }
+        const uint32_t ntiles = (len + CLS_TILE - 1) / CLS_TILE;
+        const int gcls = (int)(ntiles < (uint32_t)c->grid_cls ? ntiles : (uint32_t)c->grid_cls);
+        // block b of classify owns queue entries [b * seg_stride, (b + 1) * seg_stride):
+        // at most ceil(ntiles / gcls) tiles of CLS_TILE elements each
+        const uint32_t seg_stride = ((ntiles + gcls - 1) / gcls) * CLS_TILE;
+        const int vin = (((uintptr_t)N & 15) == 0) ? 1 : 0;
+        const int vout = (((uintptr_t)out & 7) == 0) ? 1 : 0;
+        {
+            KScope ks(K_CLASSIFY, s);
+            launch_classify(td.n32, td.n64, gcls, s, N, out, len, c, td, vin, vout, seg_stride);
+            CKL("classify_kernel");
+        }
+        // the sort and the witness kernels, when classify queued anything
+        rc = cond_stage(gb, s, gh[3], [&](cudaStream_t st) -> int {
+            {
+                KScope ks(K_SORT, st);
+                launch_k(qscatter_kernel, gcls, SORT_THREADS, 0, st, c->plan, c->q, gcls, seg_stride);  // one block per segment
+                CKL("qscatter_kernel");
+            }
+            {
+                KScope ks(K_MR1, st);
+                launch_k(mr1_kernel, mr_grid(c->grid_mr1, len), MR1_THREADS, 0, st, c->plan, c->q, N, len,
+                         g_opt.count_work, g_opt.sched);
+                CKL("mr1_kernel");
+            }
+            KScope ks(K_MR2, st);
+            return launch_mr2(c, st, N, out, len, mr_grid(c->grid_mr2, len));
+        });
+        if (rc != ISP_OK) return rc;
+    }
+    g_gon = 0;
+    return ISP_OK;
+}
+
+// Replay (or capture, instantiate and cache) the graph of this call's pipeline.
+int graph_launch(Ctx* c, const unsigned long long* dN, uint8_t* dout, size_t n, size_t chunk, const PlanParams& P,
+                 const TDParams& td, cudaStream_t s) {
+    for (auto& g : c->graphs) {
+        if (g.N == dN && g.out == dout && g.n == n && g.epoch == g_opt_epoch && g.qmem == c->qmem && g.qcap == c->qcap) {
+            g.used = ++c->graph_clock;
+            CK(cudaGraphLaunch(g.exec, s));
+            return ISP_OK;
+        }
+    }
+    if (!c->gs) {
+        CK(cudaStreamCreateWithFlags(&c->gs, cudaStreamNonBlocking));
+        CK(cudaStreamCreateWithFlags(&c->gs2, cudaStreamNonBlocking));
+    }
+    GBuild gb;
+    gb.s2 = c->gs2;
+    CK(cudaStreamBeginCapture(c->gs, cudaStreamCaptureModeRelaxed));
+    cudaStreamCaptureStatus st;
+    cudaError_t e = cudaStreamGetCaptureInfo(c->gs, &st, nullptr, &gb.g, nullptr, nullptr);
+    g_pdl_ok = false;
+    int rc = e == cudaSuccess ? enqueue_chunks(c, dN, dout, n, chunk, P, td, c->gs, &gb) : cuda_fail(e, "cudaStreamGetCaptureInfo");
+    g_gon = 0;
+    g_pdl_ok = true;
+    cudaGraph_t graph = nullptr;
+    e = cudaStreamEndCapture(c->gs, &graph);
+    if (rc != ISP_OK) {
+        if (graph) cudaGraphDestroy(graph);
+        return rc;
+    }
+    if (e != cudaSuccess) return cuda_fail(e, "cudaStreamEndCapture");
+    cudaGraphExec_t exec = nullptr;
+    e = cudaGraphInstantiate(&exec, graph, 0);
+    cudaGraphDestroy(graph);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaGraphInstantiate");
+    if (c->graphs.size() >= 8) {
+        size_t lru = 0;
+        for (size_t k = 1; k < c->graphs.size(); k++)
+            if (c->graphs[k].used < c->graphs[lru].used) lru = k;
+        if (c->has_last) CK(cudaEventSynchronize(c->last_done));
+        cudaGraphExecDestroy(c->graphs[lru].exec);
+        c->graphs.erase(c->graphs.begin() + (long)lru);
+    }
+    c->graphs.push_back({dN, dout, n, g_opt_epoch, c->qmem, c->qcap, exec, ++c->graph_clock});
+    CK(cudaGraphLaunch(exec, s));
     return ISP_OK;
 }
 
@@ -510,65 +702,11 @@ int device_impl(Ctx* c, const unsigned long long* dN, uint8_t* dout, size_t n, c
         return ISP_OK;
 #endif
     }
-    for (size_t base = 0; base < n; base += chunk) {
-        const uint32_t len = (uint32_t)((n - base) < chunk ? (n - base) : chunk);
-        const unsigned long long* N = dN + base;
-        uint8_t* out = dout + base;
-        P.invalidate = (base == 0 && !g_opt.sieve_cache) ? 1 : 0;
-        {
-            KScope ks(K_PLAN, s);
-            launch_k(plan_kernel, 1, PLAN_THREADS, 0, s, N, (unsigned long long)len, c->plan, P);
-            CKL("plan_kernel");
-        }
-        {
-            KScope ks(K_SIEVE, s);
-            // first base prime >= warp_p (the warp-cooperative / per-thread split)
-            int first_large = FIRST_CROSS_PRIME_IDX;
-            while (first_large < c->nbp && c->hbp[first_large].x < (uint32_t)g_opt.warp_p) first_large++;
-            launch_k(sieve_kernel, c->grid_sieve, SIEVE_THREADS, SEG_ODD, s, c->plan, c->bitmap, c->bp, c->nbp, c->patt,
-                     first_large);
-            CKL("sieve_kernel");
-        }
-        {
-            KScope ks(K_DENSE, s);
-            int first_large = FIRST_CROSS_PRIME_IDX;
-            while (first_large < c->nbp && c->hbp[first_large].x < (uint32_t)g_opt.warp_p) first_large++;
-            // 16-byte loads of element pairs need N 16-B aligned and out 2-B aligned
-            const int vec = ((((uintptr_t)N & 15) == 0) && (((uintptr_t)out & 1) == 0)) ? 1 : 0;
-            launch_k(dense_kernel, c->sms, DENSE_THREADS, 2 * SEG_ODD, s, c->plan, N, out, len, c->bp, c->nbp, c->patt,
-                     first_large, vec);
-            CKL("dense_kernel");
-            launch_k(dense2_kernel, c->sms, DENSE_THREADS, 2 * SEG_ODD, s, c->plan, N, out, len, c->bp, c->nbp,
-                     c->patt, first_large, vec);
-            CKL("dense2_kernel");
-        }
-        const uint32_t ntiles = (len + CLS_TILE - 1) / CLS_TILE;
-        const int gcls = (int)(ntiles < (uint32_t)c->grid_cls ? ntiles : (uint32_t)c->grid_cls);
-        // block b of classify owns queue entries [b * seg_stride, (b + 1) * seg_stride):
-        // at most ceil(ntiles / gcls) tiles of CLS_TILE elements each
-        const uint32_t seg_stride = ((ntiles + gcls - 1) / gcls) * CLS_TILE;
-        const int vin = (((uintptr_t)N & 15) == 0) ? 1 : 0;
-        const int vout = (((uintptr_t)out & 7) == 0) ? 1 : 0;
-        {
-            KScope ks(K_CLASSIFY, s);
-            launch_classify(td.n32, td.n64, gcls, s, N, out, len, c, td, vin, vout, seg_stride);
-            CKL("classify_kernel");
-        }
-        {
-            KScope ks(K_SORT, s);
-            launch_k(qscatter_kernel, gcls, SORT_THREADS, 0, s, c->plan, c->q, gcls, seg_stride);  // one block per segment
-            CKL("qscatter_kernel");
-        }
-        {
-            KScope ks(K_MR1, s);
-            launch_k(mr1_kernel, mr_grid(c->grid_mr1, len), MR1_THREADS, 0, s, c->plan, c->q, N, len,
-                     g_opt.count_work, g_opt.sched);
-            CKL("mr1_kernel");
-        }
-        {
-            KScope ks(K_MR2, s);
-            rc = launch_mr2(c, s, N, out, len, mr_grid(c->grid_mr2, len));
-        }
+    if (g_opt.graph && !g_opt.kernel_timing && !ISP_CHECKS) {
+        rc = graph_launch(c, dN, dout, n, chunk, P, td, s);
+        if (rc != ISP_OK) return rc;
+    } else {
+        rc = enqueue_chunks(c, dN, dout, n, chunk, P, td, s, nullptr);
         if (rc != ISP_OK) return rc;
     }
 #if ISP_CHECKS
@@ -736,6 +874,9 @@ void isprime_shutdown(void) {
             if (c->ev_d2h[k]) cudaEventDestroy(c->ev_d2h[k]);
         }
         if (c->last_done) cudaEventDestroy(c->last_done);
+        for (auto& g : c->graphs) cudaGraphExecDestroy(g.exec);
+        if (c->gs) cudaStreamDestroy(c->gs);
+        if (c->gs2) cudaStreamDestroy(c->gs2);
         delete c;
         g_ctx[d] = nullptr;
     }
@@ -768,7 +909,9 @@ int isprime_set_option(const char* key, long long v) {
     else if (!strcmp(key, "witness")) { if (v < 0 || v > 2) return ISP_EINVAL; g_opt.witness = (int)v; }
     else if (!strcmp(key, "sched")) { if (v < 0 || v > 2) return ISP_EINVAL; g_opt.sched = (int)v; }
     else if (!strcmp(key, "fuse_bits")) { if (v != 0 && v != 32 && v != 51) return ISP_EINVAL; g_opt.fuse_bits = (int)v; }
+    else if (!strcmp(key, "graph")) { if (v < 0 || v > 1) return ISP_EINVAL; g_opt.graph = (int)v; }
     else return ISP_EINVAL;
+    g_opt_epoch++;
     return ISP_OK;
 }
 
@@ -793,6 +936,7 @@ long long isprime_get_option(const char* key) {
     if (!strcmp(key, "sieve_cache")) return g_opt.sieve_cache;
     if (!strcmp(key, "mr2_group")) return g_opt.mr2_group;
     if (!strcmp(key, "pdl")) return g_opt.pdl;
+    if (!strcmp(key, "graph")) return g_opt.graph;
     if (!strcmp(key, "small_max")) return g_opt.small_max;
     if (!strcmp(key, "warp_max")) return g_opt.warp_max;
     if (!strcmp(key, "witness")) return g_opt.witness;

@@ -54,7 +54,21 @@ constexpr int MAX_SEG = 4096;                         // classify blocks (queue 
 // launch overlaps the tail of the one before it; each waits here, before its
 // first global access, until the previous grid has completed and its writes
 // are visible.  A no-op when the kernel was launched without the attribute.
-__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+// ISP_PDL_EARLY (A/B): 0 -- the next kernel launches as this grid's blocks
+// exit (implicit trigger); 1 -- each block triggers right after its wait;
+// 2 -- before it.  The dependent still waits for this grid's completion.
+#ifndef ISP_PDL_EARLY
+#define ISP_PDL_EARLY 0
+#endif
+__device__ __forceinline__ void pdl_wait() {
+#if ISP_PDL_EARLY == 2
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+#endif
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+#if ISP_PDL_EARLY == 1
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+#endif
+}
 // Ask the TMA unit to pull [p, p + bytes) into L2 (p 16-B aligned, bytes a
 // multiple of 16): a streaming kernel prefetches its next tile with one
 // instruction instead of holding more loads in flight in registers.
@@ -123,6 +137,11 @@ struct PlanParams {
     float mr32_ps_per_bit;     // MR cost per odd element per bit (n < 2^32)
     float mr_fixed_ps;         // latency floor of the witness kernels when any element needs them
     int invalidate;            // 1: forget the bitmap held from an earlier call (first chunk of a call)
+    // graph launch (isprime.cu option "graph"): conditional-node handles the
+    // plan sets -- [0] sieve, [1] dense stride 1, [2] dense stride 2 -- so the
+    // stages it does not need are not launched at all (gon = 0: plain launches)
+    int gon;
+    unsigned long long gh[3];
 };
 
 // Scratch queues of a chunk, 8 bytes per element in all (isprime.cu
@@ -610,6 +629,11 @@ __global__ void __launch_bounds__(PLAN_THREADS) plan_kernel(const unsigned long 
     }
     plan->pf = 0;
     plan->chunks = chunks0 + 1;
+    if (P.gon) {
+        cudaGraphSetConditional((cudaGraphConditionalHandle)P.gh[0], need);
+        cudaGraphSetConditional((cudaGraphConditionalHandle)P.gh[1], dense && ds == 1ull ? 1u : 0u);
+        cudaGraphSetConditional((cudaGraphConditionalHandle)P.gh[2], dense && ds == 2ull ? 1u : 0u);
+    }
 }
 
 // ------------------------------------------------------------- A1: sieve
@@ -960,6 +984,8 @@ struct FzParams {
     int bits;     // 0: off (everything queued); 32: n < 2^32; 51: n < FP_LIMIT
     int p2;       // remaining bases below 2^32: 0 {7, 61}; 1 the six of Eq 4; 2 one hashed base
     int wit;      // option witness (2: Jaeschke's set below kJaeschkeBound4 in the FP64 class)
+    int gon;      // graph launch: a block that queued survivors sets gh_tail (sort, mr1, mr2 run)
+    unsigned long long gh_tail;
 };
 // Trial-division candidates carried between warp-tiles (round 2): a
 // warp-tile's candidates beyond its last full round of 32 wait here, and a
@@ -1623,6 +1649,7 @@ classify_kernel(const unsigned long long* __restrict__ N, uint8_t* __restrict__ 
         ISP_CHECK(sm.cur <= seg_stride, 103);
         if (c32) atomicAdd(&plan->counts[0], c32);
         if (sm.cur - c32) atomicAdd(&plan->counts[1], sm.cur - c32);
+        if (fz.gon && sm.cur) cudaGraphSetConditional((cudaGraphConditionalHandle)fz.gh_tail, 1u);
     }
 }
 

@@ -82,7 +82,7 @@ def test_options_validate():
         isp.set_option(key, saved)
     for key, bad, good in (("witness", 3, 2), ("small_max", -1, 0), ("small_max", 1 << 32, (1 << 32) - 1),
                            ("warp_max", -1, 64), ("fuse_bits", 33, 51), ("fuse_bits", -1, 0), ("small_sieve", 2, 0),
-                           ("count_work", 2, 0)):
+                           ("count_work", 2, 0), ("graph", 2, 0), ("graph", -1, 1)):
         saved = isp.get_option(key)
         with pytest.raises(isp.IsPrimeError):
             isp.set_option(key, bad)

@@ -53,7 +53,7 @@ def _default_options():
     saved = {k: isp.get_option(k) for k in ("force_path", "bases32", "td_primes32", "td_primes64",
                                              "chunk_log2", "win64", "warp_p", "small_max", "warp_max",
                                              "witness", "sieve_cache", "sched", "fuse_bits", "count_work",
-                                             "small_sieve")}
+                                             "small_sieve", "graph")}
     yield
     for k, v in saved.items():
         isp.set_option(k, v)
@@ -626,7 +626,8 @@ def test_options_do_not_change_results():
     exp = oracle.isprime(N)
     for key, vals in (("td_primes32", (0, 1, 5, 128)), ("td_primes64", (0, 3, 128)), ("win64", (1, 2, 3)),
                       ("force_path", (0, 1, 2)), ("chunk_log2", (16, 17, 28)), ("warp_p", (17, 600, 65536)),
-                      ("witness", (1, 2, 0)), ("sched", (0, 1, 2)), ("fuse_bits", (0, 51, 32))):
+                      ("witness", (1, 2, 0)), ("sched", (0, 1, 2)), ("fuse_bits", (0, 51, 32)),
+                      ("graph", (0, 1))):
         saved = isp.get_option(key)
         for v in vals:
             isp.set_option(key, v)
@@ -817,3 +818,38 @@ def test_sprp_device_vs_oracle(win):
         isp.isprime_sprp_device(dn, da, out)
         torch.cuda.synchronize()
         assert_same(out.cpu().numpy(), oracle.sprp_array(ns, av), ns)
+
+
+# ------------------------------------------------------------------ graph replay (option "graph")
+def test_graph_replay_reads_current_inputs():
+    """Option graph: a call's pipeline is captured once per (pointers, n,
+    options, scratch) and replayed; conditional nodes set on the device skip
+    the stages a chunk does not need.  The same device buffers refilled with
+    inputs that need different stages -- witness kernels (C5), fused tests only
+    (C2), a dense range (dense_kernel), a stride-2 range (dense2_kernel), a
+    sieve window only (C1 values) -- must each equal the oracle on replay, and
+    equal the plain-launch path (graph = 0); so must several chunks of one call
+    whose stages differ (chunk_log2 = 20: a dense chunk beside random ones)."""
+    n = 3 << 20
+    lo = 1_000_001
+    inputs = [workloads.generate("C5", count=n), workloads.generate("C2", count=n),
+              np.arange(lo, lo + n, dtype=np.uint64), np.arange(lo, lo + 2 * n, 2, dtype=np.uint64),
+              workloads.generate("C1", count=n)]
+    dN = torch.empty(n, dtype=torch.int64, device=DEV)
+    dout = torch.empty(n, dtype=torch.uint8, device=DEV)
+    for graph in (1, 0):
+        isp.set_option("graph", graph)
+        for rep in range(2):
+            for N in inputs:
+                dN.copy_(torch.from_numpy(np.ascontiguousarray(N).view(np.int64)))
+                dout.fill_(7)
+                isp.isprime_device(dN, dout, n)
+                torch.cuda.synchronize()
+                assert_same(dout.cpu().numpy(), oracle.isprime(N), N)
+    isp.set_option("graph", 1)
+    isp.set_option("chunk_log2", 20)
+    N = np.concatenate([workloads.generate("C5", count=1 << 20), np.arange(lo, lo + (1 << 20), dtype=np.uint64),
+                        workloads.generate("C2", count=1 << 20), workloads.generate("C1", count=(1 << 20) - 5)])
+    exp = oracle.isprime(N)
+    for _ in range(3):
+        assert_same(gpu(N), exp, N)
