@@ -86,7 +86,8 @@ void isprime_shutdown(void);
  *                    below 2^32 before Miller-Rabin (0..ISP_MAX_TD)
  * "td_primes64"      same for values >= 2^32.  Both are accepted in 0..ISP_MAX_TD
  *                    and rounded down to the compiled variants 0, 8, 16, 24, 32
- *                    (defaults 16 / 32; a v18 sweep found these the fastest).
+ *                    (defaults 24 / 32: the round-2 re-sweep on the fused classify,
+ *                    C2 8 / 16 / 24 primes 0.169 / 0.159 / 0.154 ms; C5 flat).
  * "chunk_log2"       device chunk size (elements) = 2^value, 16..31 (default 30;
  *                    halved while the queues of a chunk do not fit in memory)
  * "win64"            exponent window width for the 64-bit multi-base phase (1..3,

@@ -25,7 +25,7 @@ namespace {
 struct Options {
     int force_path = 0;      // 0 auto, 1 sieve, 2 mr
     int bases32 = 3;         // 3 -> {2,7,61}; 7 -> full Eq 4 set
-    int td32 = 16;           // odd primes 3..59 (profiles: C2 best at 16)
+    int td32 = kTD32Default; // odd primes 3..97 (round-2 re-sweep with the fused classify: C2 best at 24)
     int td64 = 32;
     int chunk_log2 = 30;     // device chunk: 2^30 elements need <= 64 GB of queues (of 180 GB); halved on ENOMEM
     int win64 = 3;           // phase-2 window bits (tables in shared memory; 3 measured best)
@@ -384,8 +384,8 @@ void launch_classify_b(int n64, int g, cudaStream_t s, const unsigned long long*
 
 void launch_classify(int n32, int n64, int g, cudaStream_t s, const unsigned long long* N, uint8_t* out,
                      uint32_t len, Ctx* c, const TDParams& td, int vin, int vout, uint32_t ss) {
-    if (g_opt.count_work && n32 == 16 && n64 == 32) {  // the work-counting instantiation (default TD only)
-        launch_cls(classify_kernel<16, 32, true>, g, s, N, out, len, c, td, vin, vout, ss);
+    if (g_opt.count_work && n32 == kTD32Default && n64 == 32) {  // the work-counting instantiation (default TD only)
+        launch_cls(classify_kernel<kTD32Default, 32, true>, g, s, N, out, len, c, td, vin, vout, ss);
         return;
     }
     switch (n32) {

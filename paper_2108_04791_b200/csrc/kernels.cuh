@@ -213,6 +213,13 @@ __device__ __forceinline__ unsigned long long hash_base32(uint32_t n) {
 constexpr uint32_t kOddPrimes[32] = {3, 5, 7, 11, 13, 17, 19, 23, 29, 31, 37, 41, 43, 47, 53, 59,
                                      61, 67, 71, 73, 79, 83, 89, 97, 101, 103, 107, 109, 113, 127, 131, 137};
 constexpr uint64_t kGroupLimit = 1ull << 21;
+// Default trial-division depth of the 32-bit class (option td_primes32; the
+// short-array kernels test it with immediate operands).  Round 2 re-sweep on
+// the fused classify: C2 8 / 16 / 24 primes 0.169 / 0.159 / 0.154 ms, C5 flat.
+#ifndef ISP_TD32_DEFAULT
+#define ISP_TD32_DEFAULT 24
+#endif
+constexpr int kTD32Default = ISP_TD32_DEFAULT;
 
 // index of the first prime of group g when the first `np` odd primes are grouped greedily
 __host__ __device__ constexpr int group_start(int np, int g) {
@@ -2120,10 +2127,10 @@ __global__ void __launch_bounds__(256) small_kernel(const unsigned long long* __
         else if (v < (1ull << 32)) {
             const uint32_t x = (uint32_t)v;
             bool comp;
-            if (td.n32 == 16) {  // the default depth with immediate operands (as classify)
-                constexpr uint32_t kLast16 = kOddPrimes[15];
-                comp = td_primes<0, 16>(x);
-                if (x <= kLast16) comp = !((kSmallOddPrimeMask[x >> 6] >> ((x >> 1) & 31u)) & 1u);
+            if (td.n32 == kTD32Default) {  // the default depth with immediate operands (as classify)
+                constexpr uint32_t kLastD = kOddPrimes[kTD32Default - 1];
+                comp = td_primes<0, kTD32Default>(x);
+                if (x <= kLastD) comp = !((kSmallOddPrimeMask[x >> 6] >> ((x >> 1) & 31u)) & 1u);
             } else {
                 comp = false;
                 for (int t = 0; t < td.n32; t++) comp |= (x * c_td_inv32[t] <= c_td_lim32[t]) && (x != c_td_p[t]);
@@ -2257,10 +2264,10 @@ __global__ void __launch_bounds__(256) small_warp_kernel(const unsigned long lon
     else if (v < (1ull << 32)) {
         const uint32_t x = (uint32_t)v;
         bool comp;
-        if (td.n32 == 16) {  // the default depth with immediate operands
-            constexpr uint32_t kLast16 = kOddPrimes[15];
-            comp = td_primes<0, 16>(x);
-            if (x <= kLast16) comp = !((kSmallOddPrimeMask[x >> 6] >> ((x >> 1) & 31u)) & 1u);
+        if (td.n32 == kTD32Default) {  // the default depth with immediate operands
+            constexpr uint32_t kLastD = kOddPrimes[kTD32Default - 1];
+            comp = td_primes<0, kTD32Default>(x);
+            if (x <= kLastD) comp = !((kSmallOddPrimeMask[x >> 6] >> ((x >> 1) & 31u)) & 1u);
         } else {
             comp = false;
             for (int t = 0; t < td.n32; t++) comp |= (x * c_td_inv32[t] <= c_td_lim32[t]) && (x != c_td_p[t]);
