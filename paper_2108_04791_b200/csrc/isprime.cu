@@ -161,7 +161,11 @@ void read_env_once() {
     if (const char* e = getenv("ISPRIME_TD64")) g_opt.td64 = atoi(e);
     if (const char* e = getenv("ISPRIME_WIN64")) g_opt.win64 = atoi(e);
     if (const char* e = getenv("ISPRIME_CHUNK_LOG2")) g_opt.chunk_log2 = atoi(e);
-    if (const char* e = getenv("ISPRIME_SIEVE_MAX")) g_opt.sieve_max = strtoull(e, nullptr, 0);
+    if (const char* e = getenv("ISPRIME_SIEVE_MAX")) {
+        // the sieve works on whole 64-value bitmap words below 2^32
+        unsigned long long v = strtoull(e, nullptr, 0) & ~63ull;
+        g_opt.sieve_max = v > (1ull << 32) ? (1ull << 32) : v;
+    }
     if (const char* e = getenv("ISPRIME_FUSE_BITS")) { const int v = atoi(e); if (v == 0 || v == 32 || v == 51) g_opt.fuse_bits = v; }
 }
 

@@ -549,7 +549,9 @@ __global__ void __launch_bounds__(PLAN_THREADS) plan_kernel(const unsigned long 
         const double fixed_all = (double)P.mr_fixed_ps;
         // candidate of this lane: [0, 2^b)
         double cost = 1e300;
-        unsigned long long clo = 0, chi = 1ull << b;
+        // the sieve packs whole 64-value bitmap words: a window of fewer than
+        // 64 values (every sampled small value below 64) is widened to [0, 64)
+        unsigned long long clo = 0, chi = b < 6 ? 64ull : 1ull << b;
         if (chi <= wmax)
             cost = P.sieve_fixed_ps + (double)chi * P.sieve_ps_per_int + (mr_all - covered) +
                    ((big || mr_all - covered > 0.0) ? fixed_all : 0.0);

@@ -853,3 +853,27 @@ def test_graph_replay_reads_current_inputs():
     exp = oracle.isprime(N)
     for _ in range(3):
         assert_same(gpu(N), exp, N)
+
+
+# ------------------------------------------------------------------ tiny windows
+@pytest.mark.parametrize("vals", [(3,), (3, 5, 7), (2, 3, 61), (31,), (61, 59, 63)])
+@pytest.mark.parametrize("with_big", [False, True])
+def test_window_below_64_values(vals, with_big):
+    """Found by tools/fuzz_gpu.py: when every small odd value sampled by the plan
+    lies below 64 (a long run of 3s), the chosen window [0, 2^b) with b < 6 held
+    no whole 64-value bitmap word, the sieve wrote nothing, and classify read a
+    stale word.  The plan widens such a window to [0, 64)."""
+    rng = np.random.default_rng(64)
+    n = 400_468
+    N = np.array(vals, dtype=np.uint64)[rng.integers(0, len(vals), size=n)]
+    if with_big:
+        big = workloads.generate("C3", count=n)
+        N = np.where(rng.integers(0, 2, size=n) == 0, N, big)
+    exp = oracle.isprime(N)
+    for sieve_cache in (0, 1):
+        isp.set_option("sieve_cache", sieve_cache)
+        assert_same(gpu(N), exp, N)
+        # a wider window right after (and the held bitmap, when cached)
+        M = workloads.generate("C1", count=n)
+        assert_same(gpu(M), oracle.isprime(M), M)
+        assert_same(gpu(N), exp, N)
