@@ -7,7 +7,8 @@ Each case draws a size, a mixture of structured pieces (log-uniform bit
 lengths, narrow windows, arithmetic progressions of stride 1 / 2 / other,
 values hugging 2^32 / 2^51 / 2^63 / 2^64, all-even runs, constant runs,
 repeated primes), an element misalignment of both buffers and a random set of
-options, runs isprime_device into a poisoned buffer and compares every byte
+options, runs isprime_device into a poisoned buffer (and, for a third of the
+cases up to 2^22 elements, the host call isprime) and compares every byte
 with oracle.isprime (out[i] = 1 iff N[i] is prime).  One JSON
 line per case, a summary line at the end; exit code 1 on any mismatch.
 """
@@ -125,6 +126,11 @@ def main():
                "primes": int(exp.sum()), "mismatches": int(bad.size), "guard_intact": guard}
         if bad.size:
             rec["first"] = [[int(i), int(N[i]), int(got[i]), int(exp[i])] for i in bad[:8]]
+        if n <= (1 << 22) and rng.integers(0, 3) == 0:  # the host C-ABI call on the same input
+            hbad = int(np.count_nonzero(isp.isprime(N) != exp))
+            rec["host_mismatches"] = hbad
+            if hbad:
+                bad_cases += 1
         if bad.size or not guard:
             bad_cases += 1
         total += n
