@@ -58,8 +58,12 @@ def piece(rng, m):
         top = (1 << 32) if rng.integers(0, 4) else (1 << 64)
         hi = top - d * m - 1
         lo = int(rng.integers(0, max(hi, 1), dtype=np.uint64)) if hi > 0 else 0
-        if rng.integers(0, 3) == 0:
+        t = int(rng.integers(0, 6))
+        if t < 2:
             lo = max(0, min(lo, 5))  # ranges that start at 0 .. 5
+        elif t == 2 and d * m < (1 << 32):
+            lo = (1 << 32) - d * m + int(rng.integers(-3, 4)) * d  # ending at / crossing 2^32
+            lo = max(lo, 0)
         return kind, U64(lo) + U64(d) * np.arange(m, dtype=np.uint64)
     if kind == 5:  # hugging a class boundary
         b = (1 << int(rng.choice([16, 20, 31, 32, 33, 50, 51, 52, 53, 55, 59, 62, 63, 64])))
@@ -95,6 +99,9 @@ def main():
         n = int(2 ** rng.uniform(0, 23.5))
         if rng.integers(0, 12) == 0:
             n = int(rng.integers((1 << 24), (1 << 25)))
+        if rng.integers(0, 4) == 0:  # sizes at the paths' thresholds (short-array limits, tiles, dense minimum, chunks)
+            t = (4096, 8192, 1 << 16, 1 << 17, 1 << 20, 1 << 21, (1 << 20) + 8192, 1 << 24)
+            n = max(1, int(t[int(rng.integers(0, len(t)))]) + int(rng.integers(-2, 3)))
         parts, kinds, left = [], [], n
         while left > 0:
             m = left if rng.integers(0, 3) == 0 else int(rng.integers(1, left + 1))
@@ -103,8 +110,16 @@ def main():
             parts.append(v)
             left -= m
         N = np.concatenate(parts)
-        if rng.integers(0, 4) == 0:
+        r = int(rng.integers(0, 8))
+        if r < 2:
             rng.shuffle(N)
+        elif r == 2:
+            N = np.sort(N)
+        if rng.integers(0, 4) == 0:  # a few foreign elements where the plan's samples may miss them
+            k = int(rng.integers(1, 5))
+            pos = rng.integers(0, n, size=k)
+            N = N.copy()
+            N[pos] = piece(rng, k)[1]
         opts = {}
         for k, vals in OPTS.items():
             if rng.integers(0, 3) == 0:
