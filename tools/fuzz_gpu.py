@@ -1,7 +1,7 @@
 """Randomized structured stress of the CUDA path against the CPU oracle (test
 infrastructure: calls oracle/, never part of the product path).
 
-    python tools/fuzz_gpu.py [cases] [seed] > gpurun_out/fuzz.jsonl
+    python tools/fuzz_gpu.py [cases] [seed] [log2 min size] [log2 max size] > gpurun_out/fuzz.jsonl
 
 Each case draws a size, a mixture of structured pieces (log-uniform bit
 lengths, narrow windows, arithmetic progressions of stride 1 / 2 / other,
@@ -89,6 +89,10 @@ def piece(rng, m):
 def main():
     cases = int(sys.argv[1]) if len(sys.argv) > 1 else 200
     seed = int(sys.argv[2]) if len(sys.argv) > 2 else 20211
+    # optional size range (log2): python tools/fuzz_gpu.py 24 5 25.5 27.5 for multi-chunk sizes
+    lg_lo = float(sys.argv[3]) if len(sys.argv) > 3 else 0.0
+    lg_hi = float(sys.argv[4]) if len(sys.argv) > 4 else 23.5
+    big_ok = len(sys.argv) <= 3
     rng = np.random.default_rng(seed)
     dev = torch.device("cuda:0")
     defaults = {k: isp.get_option(k) for k in OPTS}
@@ -96,10 +100,10 @@ def main():
     total = 0
     t0 = time.time()
     for c in range(cases):
-        n = int(2 ** rng.uniform(0, 23.5))
-        if rng.integers(0, 12) == 0:
+        n = int(2 ** rng.uniform(lg_lo, lg_hi))
+        if big_ok and rng.integers(0, 12) == 0:
             n = int(rng.integers((1 << 24), (1 << 25)))
-        if rng.integers(0, 4) == 0:  # sizes at the paths' thresholds (short-array limits, tiles, dense minimum, chunks)
+        if big_ok and rng.integers(0, 4) == 0:  # sizes at the paths' thresholds (short-array limits, tiles, dense minimum, chunks)
             t = (4096, 8192, 1 << 16, 1 << 17, 1 << 20, 1 << 21, (1 << 20) + 8192, 1 << 24)
             n = max(1, int(t[int(rng.integers(0, len(t)))]) + int(rng.integers(-2, 3)))
         parts, kinds, left = [], [], n
